@@ -1,0 +1,225 @@
+/*
+ * ds_gpu.h -- C ABI of the B200-native DiffServe hot path.
+ *
+ * Plain C: POD structs, pointers and sizes, integer status codes. No CUDA,
+ * torch or C++ types appear in any signature, so the reference's C++ host
+ * (or a ctypes / cgo / JNI stub) can bind it directly.
+ *
+ * Two halves, mirroring the reference hot path:
+ *   planner  : ds_plan_batch*        replaces diffserve::solve and variants
+ *                                    (reference proj/src/allocator.cpp:153-313)
+ *   score    : ds_score_latent*      replaces diffserve::sample_query
+ *                                    (reference proj/src/workload.cpp:108-129)
+ *              ds_disc_score*        discriminator network (no reference;
+ *                                    SURVEY 8a row S9)
+ *   route    : ds_route*             replaces the Policy::defers loop
+ *                                    (reference proj/src/cluster.cpp:290-306,
+ *                                     proj/src/policies.cpp:37-39)
+ *   curve    : ds_curve_observe*     replaces diffserve::observe_confidence
+ *                                    (reference proj/src/profiles.cpp:108-120)
+ *
+ * Functions without the _device suffix take HOST buffers and copy in/out
+ * inside the call (the reference-facing drop-in). The _device variants take
+ * device pointers and a cudaStream_t passed as void*; they are stream-ordered
+ * and do not synchronize.
+ *
+ * Errors: the reference throws C++ exceptions (allocator.cpp:12-36,
+ * profiles.cpp:20-26,98-100,108-112). Across this ABI each exception type maps
+ * to one status code; ds_last_error() returns the reference's message text
+ * for the calling thread. Infeasibility is NOT an error (plan.feasible = 0).
+ */
+#ifndef DS_GPU_H
+#define DS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DS_ABI_VERSION 1
+#define DS_MAX_BATCHES 64   /* profiled batch sizes per model               */
+#define DS_CURVE_BINS 101   /* DeferralCurve::kBins, profiles.hpp:50         */
+
+typedef enum {
+    DS_OK = 0,
+    DS_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument                  */
+    DS_ERR_DOMAIN = 2,           /* std::domain_error                      */
+    DS_ERR_INVARIANT = 3,        /* diffserve::InvariantError              */
+    DS_ERR_OUT_OF_RANGE = 4,     /* std::out_of_range (unprofiled batch)   */
+    DS_ERR_CUDA = 5,             /* CUDA runtime / launch failure          */
+    DS_ERR_NO_DEVICE = 6,        /* no sm_100 device visible               */
+    DS_ERR_CAPACITY = 7          /* input exceeds a compiled-in ABI limit  */
+} ds_status;
+
+typedef enum {
+    DS_QUEUING_LITTLES_LAW = 0, /* QueuingModel::littles_law, allocator.hpp:23 */
+    DS_QUEUING_TWICE_EXEC = 1   /* QueuingModel::twice_exec,  allocator.hpp:24 */
+} ds_queuing;
+
+/* Which reference entry point a planner problem runs (allocator.hpp:64-91). */
+typedef enum {
+    DS_SOLVE = 0,               /* solve()                  allocator.cpp:153 */
+    DS_SOLVE_PINNED = 1,        /* solve_pinned_threshold() allocator.cpp:176 */
+    DS_SOLVE_FIXED_BATCHES = 2, /* solve_fixed_batches()    allocator.cpp:213 */
+    DS_SOLVE_EVEN_SPLIT = 3,    /* solve_even_split()       allocator.cpp:270 */
+    DS_SOLVE_SINGLE_LIGHT = 4,  /* solve_single_model(light) allocator.cpp:232 */
+    DS_SOLVE_SINGLE_HEAVY = 5   /* solve_single_model(heavy) allocator.cpp:232 */
+} ds_solve_mode;
+/* solve_static_peak (allocator.cpp:171) is DS_SOLVE with demand := peak. */
+
+/* ModelProfile (profiles.hpp:11-19): batch sizes strictly ascending. */
+typedef struct {
+    int32_t n;
+    int32_t _pad;
+    int32_t batch[DS_MAX_BATCHES];
+    double latency[DS_MAX_BATCHES];
+} ds_model_profile;
+
+/* DeferralCurve (profiles.hpp:35-48); bin lower edges are implicitly k/100. */
+typedef struct {
+    double bin_mass[DS_CURVE_BINS];
+    double total_mass;
+} ds_curve;
+
+/* CascadeProfile (profiles.hpp:62-68). */
+typedef struct {
+    ds_model_profile light;
+    ds_model_profile heavy;
+    ds_curve deferral;
+    double slo_seconds;
+} ds_cascade;
+
+/* AllocationProblem (allocator.hpp:27-37) plus the variant selector. */
+typedef struct {
+    double demand_qps;
+    double overprovision_lambda;
+    double queue_sentinel_seconds;
+    double light_rate;        /* light_queue.arrival_rate */
+    double heavy_rate;        /* heavy_queue.arrival_rate */
+    int64_t light_len;        /* light_queue.queue_length */
+    int64_t heavy_len;        /* heavy_queue.queue_length */
+    double fixed_threshold;   /* DS_SOLVE_PINNED                    */
+    int32_t fixed_b1;         /* DS_SOLVE_FIXED_BATCHES             */
+    int32_t fixed_b2;
+    int32_t total_servers;
+    int32_t queuing;          /* ds_queuing                         */
+    int32_t cascade;          /* index into the cascades array      */
+    int32_t grid;             /* index into the grid table          */
+    int32_t mode;             /* ds_solve_mode                      */
+    int32_t _pad;
+} ds_problem;
+
+/* AllocationPlan (allocator.hpp:39-46). */
+typedef struct {
+    int32_t x1, x2, b1, b2;
+    double threshold;
+    int32_t feasible;
+    int32_t _pad;
+} ds_plan;
+
+/* QueryOutcomeModel (workload.hpp:52-58). */
+typedef struct {
+    double easy_fraction;
+    double quality_gap_scale;
+    double confidence_fidelity;
+    double noise_sigma;
+    uint64_t seed;
+} ds_query_model;
+
+typedef struct ds_ctx ds_ctx;
+
+/* ---- context -------------------------------------------------------- */
+const char* ds_version(void);
+const char* ds_last_error(void);
+ds_status ds_ctx_create(int device, ds_ctx** out);
+ds_status ds_ctx_destroy(ds_ctx* ctx);
+ds_status ds_ctx_synchronize(ds_ctx* ctx);
+/* Number of device kernels this context launched so far (for bench audits). */
+int64_t ds_ctx_launch_count(const ds_ctx* ctx);
+void* ds_ctx_stream(ds_ctx* ctx); /* the context's cudaStream_t */
+
+/* ---- planner (K1 plan_sweep) ---------------------------------------- */
+/* Validates every problem with the reference's checks (allocator.cpp:22-36,
+ * profiles.cpp:20-26), then solves all n problems in one launch.
+ * grid_offsets has n_grids+1 entries; grid g is
+ * grid_values[grid_offsets[g] .. grid_offsets[g+1]). */
+ds_status ds_plan_batch(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                        const ds_cascade* cascades, int32_t n_cascades,
+                        const double* grid_values, const int32_t* grid_offsets,
+                        int32_t n_grids, ds_plan* out);
+/* Same, all pointers on the device, no validation, no sync. */
+ds_status ds_plan_batch_device(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                               const ds_cascade* cascades, int32_t n_cascades,
+                               const double* grid_values, const int32_t* grid_offsets,
+                               int32_t n_grids, ds_plan* out, void* stream);
+/* Host-side validation only (the checks ds_plan_batch runs before launch). */
+ds_status ds_plan_validate(const ds_problem* problems, int32_t n, const ds_cascade* cascades,
+                           int32_t n_cascades, const double* grid_values,
+                           const int32_t* grid_offsets, int32_t n_grids);
+
+/* ---- latent scorer (K4 latent_score) ---------------------------------- */
+/* conf[i] / quality_light[i] of query id0+i, bit-identical streams to
+ * sample_query (workload.cpp:108-129). quality_light may be NULL. */
+ds_status ds_score_latent(ds_ctx* ctx, const ds_query_model* model, uint64_t id0, int64_t n,
+                          double* conf, double* quality_light);
+ds_status ds_score_latent_device(ds_ctx* ctx, const ds_query_model* model, uint64_t id0,
+                                 int64_t n, double* conf, double* quality_light, void* stream);
+
+/* ---- router (K2 route_compact) ---------------------------------------- */
+/* For every threshold t_k: heavy list k = ascending indices i with
+ * conf[i] < t_k (strict, policies.cpp:37-39), written to
+ * heavy_idx[k*n .. k*n + counts[k]). conf is f64 (dtype 0) or f32 (dtype 1).
+ * index_base is added to every written index (global ids of a shard). */
+#define DS_CONF_F64 0
+#define DS_CONF_F32 1
+ds_status ds_route(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t n,
+                   const double* thresholds, int32_t n_thresholds, int64_t index_base,
+                   int64_t* heavy_idx, int64_t* counts);
+ds_status ds_route_device(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t n,
+                          const double* thresholds, int32_t n_thresholds, int64_t index_base,
+                          int64_t* heavy_idx, int64_t* counts, void* stream);
+/* Scratch bytes ds_route_device needs for n queries and nt thresholds. */
+size_t ds_route_scratch_bytes(int64_t n, int32_t n_thresholds);
+
+/* ---- deferral curve (K3 curve_observe) -------------------------------- */
+/* Applies observe_confidence(curve, conf[i], decay) for i = 0..n-1 in order;
+ * bit-identical to the reference's sequential loop. */
+ds_status ds_curve_observe(ds_ctx* ctx, ds_curve* curve, const void* conf, int32_t dtype,
+                           int64_t n, double decay);
+ds_status ds_curve_observe_device(ds_ctx* ctx, ds_curve* curve, const void* conf,
+                                  int32_t dtype, int64_t n, double decay, void* stream);
+
+/* ---- discriminator (K5-K7: ingest + fused tcgen05 MLP + head) --------- */
+/* PatchDisc: u8 NHWC image -> 16x16 patches -> 768->256 GELU -> 256->1024
+ * ReLU -> 1024->256 ReLU -> mean over patches -> dot(256)+b -> sigmoid.
+ * Weights are generated deterministically from weight_seed. */
+#define DS_DISC_PATCH 16
+#define DS_DISC_D0 768
+#define DS_DISC_D1 256
+#define DS_DISC_D2 1024
+#define DS_DISC_D3 256
+typedef struct ds_disc ds_disc;
+ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc** out);
+ds_status ds_disc_destroy(ds_disc* disc);
+/* Host copies of the bf16 weights/biases in the kernel's logical layout:
+ * w1 [768][256], w2 [256][1024], w3 [1024][256] (row = input feature) as
+ * raw bf16 bit patterns; b1/b2/b3 f32; head w f32[256]; head bias f32. */
+ds_status ds_disc_export(const ds_disc* disc, uint16_t* w1, uint16_t* w2, uint16_t* w3,
+                         float* b1, float* b2, float* b3, float* head_w, float* head_b);
+/* Scores n images (host buffer, n*h*w*3 bytes; h, w multiples of 128). */
+ds_status ds_disc_score(ds_disc* disc, const uint8_t* nhwc, int64_t n, int32_t h, int32_t w,
+                        float* conf);
+ds_status ds_disc_score_device(ds_disc* disc, const uint8_t* nhwc, int64_t n, int32_t h,
+                               int32_t w, float* conf, void* stream);
+
+/* Synthetic image pool: pixel bytes are a pure
+ * function of (seed, image id, pixel index); generated on the device. */
+ds_status ds_synth_images_device(ds_ctx* ctx, uint64_t seed, uint64_t id0, int64_t n,
+                                 int32_t h, int32_t w, uint8_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DS_GPU_H */

@@ -1,0 +1,293 @@
+"""TEST INFRASTRUCTURE ONLY -- regenerates tests/golden/*.npz from the reference.
+
+Every expected value in the fixtures comes from the UNMODIFIED reference built
+by oracle/Makefile (oracle/_ref/libdsref.so): its own instance generators
+(test_allocator.cpp:99-166, acceptance_main.cpp:46-113,175-190), its own
+solver / exhaustive oracles, sample_query, observe_confidence and the
+Policy::defers loop. Run here (where /root/reference exists):
+
+    make -C oracle ref && python oracle/make_golden.py
+
+The fixtures are small and committed; the GPU box reads only them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+
+from oracle import lib  # noqa: E402
+from paper_2411_15381_b200 import abi, workloads  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+P = abi.ptr
+
+
+def _check(rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what}: status {rc}: {lib.ref().dsref_last_error()}")
+
+
+def ref_plan(problems, cascades, gvals, goffs, threads=8):
+    r = lib.ref()
+    out = np.zeros(len(problems), abi.PLAN)
+    _check(r.dsref_plan_batch(P(problems), len(problems), P(cascades), len(cascades), P(gvals),
+                              P(goffs), len(goffs) - 1, P(out), threads), "plan_batch")
+    return out
+
+
+def grids_from_fixed(grids, glen):
+    offs = np.zeros(len(glen) + 1, np.int32)
+    offs[1:] = np.cumsum(glen)
+    vals = np.concatenate([grids[i, :glen[i]] for i in range(len(glen))])
+    return vals, offs
+
+
+def gen_alloc_random():
+    """test_allocator.cpp:266-276: 60 instances, mt19937_64(2024)."""
+    n = 60
+    cas = np.zeros(n, abi.CASCADE)
+    pro = np.zeros(n, abi.PROBLEM)
+    grids = np.zeros((n, 101), np.float64)
+    glen = np.zeros(n, np.int32)
+    want_o = np.zeros(n, abi.PLAN)
+    want_s = np.zeros(n, abi.PLAN)
+    _check(lib.ref().dsref_gen_alloc_random(2024, n, P(cas), P(pro), P(grids), P(glen),
+                                            P(want_o), P(want_s)), "gen_alloc_random")
+    vals, offs = grids_from_fixed(grids, glen)
+    np.savez_compressed(os.path.join(OUT, "alloc_random_2024.npz"), cascades=cas, problems=pro,
+                        grid_values=vals, grid_offsets=offs, want_oracle=want_o, want_solve=want_s)
+    return int(want_s["feasible"].sum())
+
+
+def gen_accept_c1():
+    """acceptance_main.cpp:146-173: 200 instances, mt19937_64(20260825)."""
+    n = 200
+    cas = np.zeros(n, abi.CASCADE)
+    pro = np.zeros(n, abi.PROBLEM)
+    grids = np.zeros((n, 101), np.float64)
+    glen = np.zeros(n, np.int32)
+    want_t = np.zeros(n, np.float64)
+    want_has = np.zeros(n, np.int32)
+    want_s = np.zeros(n, abi.PLAN)
+    _check(lib.ref().dsref_gen_accept_c1(20260825, n, P(cas), P(pro), P(grids), P(glen),
+                                         P(want_t), P(want_has), P(want_s)), "gen_accept_c1")
+    vals, offs = grids_from_fixed(grids, glen)
+    np.savez_compressed(os.path.join(OUT, "accept_c1.npz"), cascades=cas, problems=pro,
+                        grid_values=vals, grid_offsets=offs, want_max_t=want_t,
+                        want_has=want_has, want_solve=want_s)
+    return int(want_has.sum())
+
+
+def sampled_curve(name="cascade1", n=5000):
+    """from_samples of the n sample_query confidences (cascade cfg, seed 1)."""
+    r = lib.ref()
+    m = workloads.query_model()
+    conf = np.zeros(n, np.float64)
+    _check(r.dsref_sample_queries(P(m), 0, n, workloads.SHIPPED[name]["slo"], P(conf), None, 8),
+           "sample")
+    curve = np.zeros((), abi.CURVE)
+    _check(r.dsref_curve_from_samples(P(conf), n, P(curve)), "from_samples")
+    return curve
+
+
+def gen_config4(per_combo=256):
+    """fitted 32x32 tables, C2 recipe seed 7, S in 16..128."""
+    r = lib.ref()
+    cas = np.zeros(3, abi.CASCADE)
+    for i, name in enumerate(["cascade1", "cascade2", "cascade3"]):
+        light, heavy, slo = workloads.fitted_tables(name)
+        cas[i] = workloads.make_cascade(light, heavy, slo, sampled_curve(name))
+    grid = workloads.make_grid(0.01)
+    probs = []
+    for ci in range(3):
+        for s in (16, 32, 64, 128):
+            p = np.zeros(per_combo, abi.PROBLEM)
+            one = cas[ci:ci + 1].copy()  # keep alive across the call
+            _check(r.dsref_gen_c2_recipe(P(one), s, 7, per_combo, P(p)),
+                   "c2 recipe")
+            p["cascade"] = ci
+            probs.append(p)
+    pro = np.concatenate(probs)
+    offs = np.array([0, len(grid)], np.int32)
+    want = ref_plan(pro, cas, grid, offs)
+    np.savez_compressed(os.path.join(OUT, "config4.npz"), cascades=cas, problems=pro,
+                        grid_values=grid, grid_offsets=offs, want_solve=want)
+    return int(want["feasible"].sum()), len(pro)
+
+
+def random_table(rng, base, max_sizes, contiguous):
+    n = int(rng.integers(1, max_sizes + 1))
+    t = {}
+    e = base
+    if contiguous:
+        for b in range(1, n + 1):
+            t[b] = e
+            # e(b+1) in [e(b), e(b)*(b+1)/b]: non-decreasing latency,
+            # non-increasing per-query latency (profiles.cpp:27-48)
+            e *= float(rng.uniform(1.0, (b + 1) / b))
+    else:
+        b = 1
+        for _ in range(n):
+            t[b] = e
+            b *= 2
+            e *= float(rng.uniform(1.0, 2.0))
+    return t
+
+
+def gen_wide(n=3000, seed=99):
+    """Analogue of SURVEY probe A.3: S in [1, 128], up to 6 (doubling) or 32
+    (contiguous) batch sizes, uniform/empty/sampled curves, random queues, 20%
+    twice_exec, both grid flavours, and every solve variant. Inputs come from a
+    numpy stream; expected plans from the reference solver."""
+    rng = np.random.default_rng(seed)
+    r = lib.ref()
+    cas = np.zeros(n, abi.CASCADE)
+    pro = np.zeros(n, abi.PROBLEM)
+    grids = [workloads.full_grid(0.01), workloads.full_grid(0.1), workloads.make_grid(0.01),
+             workloads.make_grid(0.05)]
+    for i in range(n):
+        contiguous = rng.random() < 0.25
+        light = random_table(rng, float(rng.uniform(0.05, 0.5)), 32 if contiguous else 6,
+                             contiguous)
+        heavy = random_table(rng, light[1] * float(rng.uniform(2.0, 12.0)),
+                             32 if contiguous else 4, contiguous)
+        slo = (light[1] + heavy[1]) * float(rng.uniform(1.01, 4.0))
+        kind = int(rng.integers(0, 4))
+        if kind == 0:
+            curve = workloads.uniform_prior()
+        elif kind == 1:
+            curve = workloads.empty_curve()
+        else:
+            s = rng.random(int(rng.integers(1, 400)))
+            if rng.random() < 0.3:
+                s = np.round(s * 100) / 100  # grid-aligned samples exercise bin_of's nudge
+            curve = np.zeros((), abi.CURVE)
+            _check(r.dsref_curve_from_samples(P(s), len(s), P(curve)), "from_samples")
+            if rng.random() < 0.5:
+                more = rng.random(int(rng.integers(1, 200)))
+                _check(r.dsref_curve_observe(P(curve), P(more), len(more), 0.999), "observe")
+        cas[i] = workloads.make_cascade(light, heavy, slo, curve)
+        p = pro[i]
+        S = int(rng.integers(1, 129))
+        p["total_servers"] = S
+        tmax = max(b / e for b, e in light.items())
+        p["demand_qps"] = float(rng.random()) * 1.5 * S * tmax
+        if rng.random() < 0.02:
+            p["demand_qps"] = 0.0
+        p["overprovision_lambda"] = [1.0, 1.05, 1.1, 1.5][int(rng.integers(0, 4))]
+        p["queue_sentinel_seconds"] = 1e6
+        for side in ("light", "heavy"):
+            q = int(rng.integers(0, 4))
+            if q == 1:
+                p[f"{side}_len"] = int(rng.integers(1, 11))
+            elif q == 2:
+                p[f"{side}_len"] = int(rng.integers(1, 11))
+                p[f"{side}_rate"] = 1.0 + float(rng.random()) * 30.0
+            elif q == 3:
+                p[f"{side}_len"] = int(rng.integers(500, 1000))
+                p[f"{side}_rate"] = 1.0 + float(rng.random()) * 5.0
+        p["queuing"] = abi.QUEUING_TWICE_EXEC if rng.random() < 0.2 else abi.QUEUING_LITTLES_LAW
+        p["cascade"] = i
+        p["grid"] = int(rng.integers(0, len(grids)))
+        mode = int(rng.choice([0, 0, 0, 0, 1, 2, 3, 4, 5]))
+        p["mode"] = mode
+        if mode == abi.SOLVE_PINNED:
+            p["fixed_threshold"] = float(rng.choice([0.0, 1.0, round(float(rng.random()), 2),
+                                                     float(rng.random())]))
+        if mode == abi.SOLVE_FIXED_BATCHES:
+            p["fixed_b1"] = int(rng.choice(list(light.keys())))
+            p["fixed_b2"] = int(rng.choice(list(heavy.keys())))
+    gvals = np.concatenate(grids)
+    offs = np.zeros(len(grids) + 1, np.int32)
+    offs[1:] = np.cumsum([len(g) for g in grids])
+    want = ref_plan(pro, cas, gvals, offs)
+    np.savez_compressed(os.path.join(OUT, "wide_random.npz"), cascades=cas, problems=pro,
+                        grid_values=gvals, grid_offsets=offs, want=want)
+    return int(want["feasible"].sum()), n
+
+
+def gen_latent():
+    """sample_query streams, routing and curve replay (workload.cpp:108-129,
+    cluster.cpp:290-306, profiles.cpp:108-120)."""
+    r = lib.ref()
+    out = {}
+    models = [workloads.query_model(),                               # cascade cfg, seed 1
+              workloads.query_model(confidence_fidelity=1.5, noise_sigma=0.15, seed=9),
+              workloads.query_model(easy_fraction=1.0, noise_sigma=0.0, seed=5),
+              workloads.query_model(confidence_fidelity=0.0, noise_sigma=0.0, seed=0),
+              workloads.query_model(seed=0xFFFFFFFFFFFFFFFF)]
+    rng = np.random.default_rng(5)
+    for k, m in enumerate(models):
+        ids = np.arange(5000, dtype=np.uint64) if k == 0 else np.sort(
+            rng.choice(1_000_000, 2000, replace=False)).astype(np.uint64)
+        conf = np.zeros(len(ids), np.float64)
+        ql = np.zeros(len(ids), np.float64)
+        if k == 0:
+            _check(r.dsref_sample_queries(P(m), 0, len(ids), 5.0, P(conf), P(ql), 8), "sample")
+        else:
+            c1 = np.zeros(1, np.float64)
+            q1 = np.zeros(1, np.float64)
+            for j, i in enumerate(ids):
+                _check(r.dsref_sample_queries(P(m), int(i), 1, 5.0, P(c1), P(q1), 1), "sample")
+                conf[j], ql[j] = c1[0], q1[0]
+        out[f"model{k}"] = m
+        out[f"ids{k}"] = ids
+        out[f"conf{k}"] = conf
+        out[f"ql{k}"] = ql
+    # Route + observe over the 5K cascade-1 confidences, every grid threshold,
+    # starting from the shipped prior (cascades.profiles:20) at decay 0.999.
+    conf = out["conf0"]
+    grid = workloads.make_grid(0.01)
+    prior = np.zeros((), abi.CURVE)
+    samples = np.asarray(workloads.SHIPPED_PRIOR_SAMPLES, np.float64)
+    _check(r.dsref_curve_from_samples(P(samples), len(samples), P(prior)), "prior")
+    counts = np.zeros(len(grid), np.int64)
+    digests = np.zeros(len(grid), np.uint64)
+    curve_after = None
+    for k, t in enumerate(grid):
+        curve = prior.copy()
+        idx = np.zeros(len(conf), np.int64)
+        cnt = np.zeros(1, np.int64)
+        _check(r.dsref_route_loop(P(conf), len(conf), float(t), 1, 0.999, P(curve), P(idx),
+                                  P(cnt)), "route_loop")
+        counts[k] = cnt[0]
+        digests[k] = np.uint64(int(np.bitwise_xor.reduce(
+            (idx[:cnt[0]].astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)) ^
+            np.arange(cnt[0], dtype=np.uint64)) if cnt[0] else 0))
+        curve_after = curve
+    out.update(route_grid=grid, route_counts=counts, route_digest=digests, prior=prior,
+               curve_after_0999=curve_after)
+    for decay in (1.0, 0.5):
+        c = prior.copy()
+        _check(r.dsref_curve_observe(P(c), P(conf), len(conf), decay), "observe")
+        out[f"curve_after_{str(decay).replace('.', '')}"] = c
+    raw = np.zeros((4, 8), np.uint64)
+    for k, s in enumerate([0, 1, 0x9E3779B97F4A7C15, 123456789]):
+        # the engine seed RandomStream(s, "query") uses; first 8 outputs
+        g = np.zeros(8, np.uint64)
+        lib.ref().dsref_stream_raw(s, b"query", 8, P(g))
+        raw[k] = g
+    out["raw_seeds"] = np.array([0, 1, 0x9E3779B97F4A7C15, 123456789], np.uint64)
+    out["raw_first8"] = raw
+    np.savez_compressed(os.path.join(OUT, "latent.npz"), **out)
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    print("alloc_random_2024: feasible", gen_alloc_random(), "of 60")
+    print("accept_c1: feasible", gen_accept_c1(), "of 200")
+    print("config4: feasible/total", gen_config4())
+    print("wide_random: feasible/total", gen_wide())
+    gen_latent()
+    print("latent: ok")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+"""CPU suite: pins the plain-C oracle restatement (oracle/ds_oracle.c) to the
+reference, via the golden vectors the reference itself produced
+(tests/golden/, oracle/make_golden.py) and, where the reference library was
+built (oracle/_ref), directly against it on fresh inputs."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import lib
+from paper_2411_15381_b200 import abi, workloads
+from tests.helpers import assert_plans_equal, planner_set, route_digest
+
+P = abi.ptr
+
+
+def port_plan(problems, cascades, gvals, goffs, threads=4):
+    out = np.zeros(len(problems), abi.PLAN)
+    status = np.zeros(len(problems), np.int32)
+    lib.port().dso_plan_batch(P(problems), len(problems), P(cascades), P(gvals), P(goffs), P(out),
+                              P(status), threads)
+    return out, status
+
+
+@pytest.mark.parametrize("name,key", [("alloc_random_2024", "want_oracle"),
+                                      ("alloc_random_2024", "want_solve"),
+                                      ("accept_c1", "want_solve"),
+                                      ("config4", "want_solve"),
+                                      ("wide_random", "want")])
+def test_port_planner_matches_reference_goldens(golden, name, key):
+    g = golden(name)
+    got, status = port_plan(*planner_set(g))
+    assert not status.any()
+    assert_plans_equal(got, g[key], name)
+
+
+def test_accept_c1_thresholds_match_brute_force(golden):
+    """acceptance C1 (acceptance_main.cpp:146-173): max feasible t exactly."""
+    g = golden("accept_c1")
+    got, _ = port_plan(*planner_set(g))
+    has = g["want_has"].astype(bool)
+    assert has.sum() == 50
+    assert np.array_equal(got["feasible"].astype(bool), has)
+    assert np.array_equal(got["threshold"][has], g["want_max_t"][has])
+
+
+def test_port_latent_matches_reference_bits(golden):
+    g = golden("latent")
+    for k in range(5):
+        m = np.ascontiguousarray(g[f"model{k}"])
+        ids = g[f"ids{k}"]
+        c1 = np.zeros(1)
+        q1 = np.zeros(1)
+        conf = np.zeros(len(ids))
+        ql = np.zeros(len(ids))
+        for j, i in enumerate(ids):
+            lib.port().dso_sample_query(P(m), int(i), P(c1), P(q1))
+            conf[j], ql[j] = c1[0], q1[0]
+        assert np.array_equal(conf.view(np.uint64), g[f"conf{k}"].view(np.uint64)), k
+        assert np.array_equal(ql.view(np.uint64), g[f"ql{k}"].view(np.uint64)), k
+
+
+def test_port_mt19937_64_streams(golden):
+    g = golden("latent")
+    for s, want in zip(g["raw_seeds"], g["raw_first8"]):
+        out = np.zeros(8, np.uint64)
+        lib.port().dso_stream_raw(int(s), b"query", 8, P(out))
+        assert np.array_equal(out, want)
+
+
+def test_port_route_and_curve_match_reference(golden):
+    g = golden("latent")
+    conf = g["conf0"]
+    grid = g["route_grid"]
+    idx = np.zeros(len(grid) * len(conf), np.int64)
+    counts = np.zeros(len(grid), np.int64)
+    lib.port().dso_route(P(conf), len(conf), P(grid), len(grid), 0, P(idx), P(counts))
+    assert np.array_equal(counts, g["route_counts"])
+    for k in range(len(grid)):
+        lst = idx[k * len(conf): k * len(conf) + counts[k]]
+        assert route_digest(lst) == g["route_digest"][k]
+    for key, decay in (("curve_after_0999", 0.999), ("curve_after_10", 1.0),
+                       ("curve_after_05", 0.5)):
+        c = g["prior"].copy()
+        assert lib.port().dso_curve_observe(P(c), P(conf), len(conf), decay) == 0
+        want = g[key]
+        assert np.array_equal(c["bin_mass"].view(np.uint64), want["bin_mass"].view(np.uint64))
+        assert c["total_mass"] == want["total_mass"]
+
+
+def test_profiles_golden_known_answers():
+    """test_profiles.cpp:68-92,128-132 known answers through the port."""
+    port = lib.port()
+    c = np.zeros((), abi.CURVE)
+    for s in (0.2, 0.4, 0.6, 0.8):
+        port.dso_observe(P(c), s, 1.0)
+    f = np.zeros(1)
+
+    def frac(t):
+        assert port.dso_deferral_fraction(P(c), t, P(f)) == 0
+        return f[0]
+
+    assert frac(0.5) == pytest.approx(0.5)
+    assert frac(0.0) == 0.0
+    assert frac(1.0) == pytest.approx(1.0)
+    assert frac(0.2) == pytest.approx(0.0)
+    assert frac(0.21) == pytest.approx(0.25)
+    assert port.dso_deferral_fraction(P(c), -0.1, P(f)) == abi.ERR_DOMAIN
+    d = np.zeros((), abi.CURVE)
+    for _ in range(4):
+        port.dso_observe(P(d), 0.25, 1.0)
+    port.dso_observe(P(d), 0.25, 0.5)
+    assert d["total_mass"] == pytest.approx(3.0)
+    assert port.dso_observe(P(d), 1.5, 1.0) == abi.ERR_DOMAIN
+    prior = workloads.uniform_prior()
+    for k in range(0, 101, 10):
+        assert port.dso_deferral_fraction(P(prior), k / 100.0, P(f)) == 0
+        assert f[0] == pytest.approx(k / 100.0)
+
+
+needs_ref = pytest.mark.skipif(not lib.ref_available(), reason="oracle/_ref not built")
+
+
+@needs_ref
+def test_port_vs_reference_fresh_latent():
+    rng = np.random.default_rng(1234)
+    for _ in range(20):
+        m = workloads.query_model(easy_fraction=float(rng.random()),
+                                  quality_gap_scale=float(rng.uniform(0, 3)),
+                                  confidence_fidelity=float(rng.uniform(0, 3)),
+                                  noise_sigma=float(rng.uniform(0, 0.5)),
+                                  seed=int(rng.integers(0, 2**63)))
+        id0 = int(rng.integers(0, 2**62))
+        n = 500
+        a = np.zeros(n)
+        qa = np.zeros(n)
+        b = np.zeros(n)
+        qb = np.zeros(n)
+        assert lib.ref().dsref_sample_queries(P(m), id0, n, 5.0, P(a), P(qa), 1) == 0
+        assert lib.port().dso_sample_queries(P(m), id0, n, P(b), P(qb), 1) == 0
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+        assert np.array_equal(qa.view(np.uint64), qb.view(np.uint64))
+
+
+@needs_ref
+def test_reference_unit_suites_pass_under_oracle_build():
+    """The reference's own 89 doctest cases, built by oracle/Makefile against
+    oracle/doctest_stub, pass (proj/test_output.txt:3-19)."""
+    import os
+    import subprocess
+    exe = os.path.join(lib.HERE, "_ref", "ref_unit_tests")
+    src = "/root/reference/proj"
+    if not (os.path.exists(exe) and os.path.isdir(src)):
+        pytest.skip("reference sources not present")
+    r = subprocess.run([exe], cwd=src, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "0 failed" in r.stdout
