@@ -1,0 +1,287 @@
+"""Reference-shaped operator API over the C ABI.
+
+Mirrors the reference's free functions and types for the hot path
+(proj/include/diffserve/allocator.hpp:12-91, profiles.hpp:11-68,
+workload.hpp:39-63, policies.hpp:30-77) with the same names, argument meaning
+and exception behaviour, so parity tests read like the reference's own
+(tests/test_api_*.py vs proj/tests/test_allocator.cpp). Every call runs on the
+GPU through libds_b200.so; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import dataclasses
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import abi, workloads
+from .native import (CapacityError, Context, DomainError, InvalidArgument, InvariantError,
+                     OutOfRange)
+
+__all__ = ["ModelProfile", "DeferralCurve", "CascadeProfile", "QueueState", "AllocationProblem",
+           "AllocationPlan", "QueryOutcomeModel", "Query", "solve", "solve_static_peak",
+           "solve_pinned_threshold", "solve_fixed_batches", "solve_single_model",
+           "solve_even_split", "solve_batch", "sample_query", "sample_queries",
+           "observe_confidences", "route", "InvalidArgument", "DomainError", "InvariantError",
+           "OutOfRange", "CapacityError", "default_context", "Policy", "make_policy",
+           "PolicyParams"]
+
+_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _ctx
+    if _ctx is None:
+        _ctx = Context(0)
+    return _ctx
+
+
+@dataclass
+class ModelProfile:                       # profiles.hpp:11-19
+    name: str
+    latency_table: dict
+
+    def batch_sizes(self):
+        return sorted(self.latency_table)
+
+    def min_batch(self):
+        return min(self.latency_table)
+
+    def max_batch(self):
+        return max(self.latency_table)
+
+
+@dataclass
+class DeferralCurve:                      # profiles.hpp:35-48
+    bin_mass: np.ndarray = field(default_factory=lambda: np.zeros(abi.CURVE_BINS))
+    total_mass: float = 0.0
+
+    @staticmethod
+    def empty() -> "DeferralCurve":
+        return DeferralCurve()
+
+    @staticmethod
+    def uniform_prior() -> "DeferralCurve":
+        c = workloads.uniform_prior()
+        return DeferralCurve(np.array(c["bin_mass"]), float(c["total_mass"]))
+
+    @staticmethod
+    def from_samples(samples) -> "DeferralCurve":
+        return observe_confidences(DeferralCurve(), np.asarray(samples, np.float64), 1.0)
+
+    def pod(self) -> np.ndarray:
+        c = np.zeros((), abi.CURVE)
+        c["bin_mass"] = self.bin_mass
+        c["total_mass"] = self.total_mass
+        return c
+
+
+@dataclass
+class CascadeProfile:                     # profiles.hpp:62-68
+    name: str
+    light: ModelProfile
+    heavy: ModelProfile
+    deferral: DeferralCurve = field(default_factory=DeferralCurve)
+    slo_seconds: float = 0.0
+
+    def pod(self) -> np.ndarray:
+        return workloads.make_cascade(self.light.latency_table, self.heavy.latency_table,
+                                      self.slo_seconds, self.deferral.pod())
+
+
+@dataclass
+class QueueState:                         # allocator.hpp:12-15
+    queue_length: int = 0
+    arrival_rate: float = 0.0
+
+
+@dataclass
+class AllocationProblem:                  # allocator.hpp:27-37
+    demand_qps: float = 0.0
+    total_servers: int = 0
+    cascade: CascadeProfile | None = None
+    overprovision_lambda: float = 1.05
+    threshold_grid: list = field(default_factory=list)
+    light_queue: QueueState = field(default_factory=QueueState)
+    heavy_queue: QueueState = field(default_factory=QueueState)
+    queuing: str = "littles_law"          # or "twice_exec"
+    queue_sentinel_seconds: float = 1e6
+
+
+@dataclass
+class AllocationPlan:                     # allocator.hpp:39-46
+    x1: int = 0
+    x2: int = 0
+    b1: int = 0
+    b2: int = 0
+    threshold: float = 0.0
+    feasible: bool = False
+
+
+def _problem_pod(p: AllocationProblem, mode: int, **extra) -> np.ndarray:
+    if p.cascade is None:
+        raise InvalidArgument("allocation problem has no cascade")
+    r = np.zeros((), abi.PROBLEM)
+    r["demand_qps"] = p.demand_qps
+    r["overprovision_lambda"] = p.overprovision_lambda
+    r["queue_sentinel_seconds"] = p.queue_sentinel_seconds
+    r["light_len"] = p.light_queue.queue_length
+    r["light_rate"] = p.light_queue.arrival_rate
+    r["heavy_len"] = p.heavy_queue.queue_length
+    r["heavy_rate"] = p.heavy_queue.arrival_rate
+    r["total_servers"] = p.total_servers
+    r["queuing"] = abi.QUEUING_TWICE_EXEC if p.queuing == "twice_exec" else abi.QUEUING_LITTLES_LAW
+    r["mode"] = mode
+    for k, v in extra.items():
+        r[k] = v
+    return r
+
+
+def _run(p: AllocationProblem, mode: int, **extra) -> AllocationPlan:
+    prob = _problem_pod(p, mode, **extra).reshape(1)
+    cas = p.cascade.pod().reshape(1)
+    grid = np.asarray(p.threshold_grid, np.float64)
+    out = default_context().plan_batch(prob, cas, grid if len(grid) else np.zeros(0),
+                                       np.array([0, len(grid)], np.int32))[0]
+    return AllocationPlan(int(out["x1"]), int(out["x2"]), int(out["b1"]), int(out["b2"]),
+                          float(out["threshold"]), bool(out["feasible"]))
+
+
+def solve(p: AllocationProblem) -> AllocationPlan:                    # allocator.cpp:153
+    return _run(p, abi.SOLVE)
+
+
+def solve_static_peak(p: AllocationProblem, peak_demand_qps: float) -> AllocationPlan:
+    return solve(dataclasses.replace(p, demand_qps=peak_demand_qps))   # allocator.cpp:171
+
+
+def solve_pinned_threshold(p: AllocationProblem, fixed_t: float) -> AllocationPlan:
+    return _run(p, abi.SOLVE_PINNED, fixed_threshold=fixed_t)          # allocator.cpp:176
+
+
+def solve_fixed_batches(p: AllocationProblem, b1: int, b2: int) -> AllocationPlan:
+    return _run(p, abi.SOLVE_FIXED_BATCHES, fixed_b1=b1, fixed_b2=b2)  # allocator.cpp:213
+
+
+def solve_even_split(p: AllocationProblem) -> AllocationPlan:          # allocator.cpp:270
+    return _run(p, abi.SOLVE_EVEN_SPLIT)
+
+
+def solve_single_model(m: ModelProfile, is_light: bool, total_servers: int, demand_qps: float,
+                       overprovision_lambda: float, slo_seconds: float) -> AllocationPlan:
+    """allocator.cpp:232-268: all servers host `m` (the other side is unused)."""
+    other = ModelProfile("unused", {1: 1.0})
+    c = CascadeProfile("single", m if is_light else other, other if is_light else m,
+                       DeferralCurve(), slo_seconds)
+    p = AllocationProblem(demand_qps, total_servers, c, overprovision_lambda)
+    return _run(p, abi.SOLVE_SINGLE_LIGHT if is_light else abi.SOLVE_SINGLE_HEAVY)
+
+
+def solve_batch(problems: np.ndarray, cascades: np.ndarray, grid_values: np.ndarray,
+                grid_offsets: np.ndarray, ctx: Context | None = None) -> np.ndarray:
+    """Bulk planner: one launch for many problems (the K1 hot path)."""
+    return (ctx or default_context()).plan_batch(problems, cascades, grid_values, grid_offsets)
+
+
+@dataclass
+class QueryOutcomeModel:                  # workload.hpp:52-58
+    easy_fraction: float = 0.3
+    quality_gap_scale: float = 1.0
+    confidence_fidelity: float = 1.5
+    noise_sigma: float = 0.15
+    seed: int = 0
+
+    def pod(self) -> np.ndarray:
+        m = np.zeros((), abi.QUERY_MODEL)
+        for k in ("easy_fraction", "quality_gap_scale", "confidence_fidelity", "noise_sigma",
+                  "seed"):
+            m[k] = getattr(self, k)
+        return m
+
+
+@dataclass
+class Query:                              # workload.hpp:39-46
+    id: int
+    arrival: float
+    deadline: float
+    quality_light: float
+    quality_heavy: float
+    confidence: float
+
+
+def sample_queries(model: QueryOutcomeModel, n: int, id0: int = 0, ctx: Context | None = None):
+    """(confidence, quality_light) of ids id0..id0+n-1 on the GPU (K4)."""
+    return (ctx or default_context()).score_latent(model.pod(), id0, n, with_quality=True)
+
+
+def sample_query(model: QueryOutcomeModel, id: int, arrival_time: float,
+                 slo_seconds: float) -> Query:                          # workload.cpp:108
+    if not (0.0 <= model.easy_fraction <= 1.0):
+        raise DomainError("easy_fraction must lie in [0, 1]")
+    if not (slo_seconds > 0.0):
+        raise DomainError("slo_seconds must be positive")
+    conf, ql = sample_queries(model, 1, id)
+    return Query(id, arrival_time, arrival_time + slo_seconds, float(ql[0]), 1.0, float(conf[0]))
+
+
+def observe_confidences(curve: DeferralCurve, conf, decay: float) -> DeferralCurve:
+    """observe_confidence (profiles.cpp:108-120) applied in order (K3)."""
+    out = default_context().curve_observe(curve.pod(), np.ascontiguousarray(conf), decay)
+    return DeferralCurve(np.array(out["bin_mass"]), float(out["total_mass"]))
+
+
+def route(conf, thresholds, index_base: int = 0):
+    """Policy::defers (policies.cpp:37-39) over a batch, order-preserving (K2)."""
+    return default_context().route(np.ascontiguousarray(conf), thresholds, index_base)
+
+
+# ---- Policy plugin boundary (policies.hpp:30-77) ------------------------------------
+
+@dataclass
+class PolicyParams:                        # policies.hpp:62-68
+    kind: str = "diffserve"
+    peak_demand_qps: float = 0.0
+    fixed_threshold: float = 0.5
+    aimd_add_step: int = 1
+    aimd_mult_factor: float = 0.5
+
+
+class Policy:
+    """The reference's plugin API; plan() runs on the GPU planner."""
+
+    def __init__(self, params: PolicyParams):
+        self.params = params
+
+    def kind(self) -> str:
+        return self.params.kind
+
+    def defers(self, confidence: float, threshold: float) -> bool:     # policies.cpp:37-39
+        if self.params.kind in ("clipper_light", "clipper_heavy", "proteus_like"):
+            return False
+        return confidence < threshold
+
+    def uses_discriminator(self) -> bool:
+        return self.params.kind not in ("clipper_light", "clipper_heavy", "proteus_like")
+
+    def plan(self, p: AllocationProblem) -> AllocationPlan:
+        k = self.params.kind
+        if k == "diffserve":
+            return solve(p)
+        if k == "diffserve_static":
+            return solve_static_peak(p, self.params.peak_demand_qps)
+        if k == "abl_static_threshold":
+            return solve_pinned_threshold(p, self.params.fixed_threshold)
+        if k == "abl_no_queuing_model":
+            return solve(dataclasses.replace(p, queuing="twice_exec"))
+        if k == "proteus_like":
+            out = solve_even_split(p)
+            if out.b1 == 0:
+                out.b1 = p.cascade.light.min_batch()
+            if out.b2 == 0:
+                out.b2 = p.cascade.heavy.min_batch()
+            return out
+        raise InvalidArgument(f"policy '{k}' has no GPU plan() in this build")
+
+
+def make_policy(params: PolicyParams) -> Policy:                       # policies.cpp:198
+    return Policy(params)

@@ -1,0 +1,117 @@
+// Context lifecycle and error plumbing of the C ABI (include/ds_gpu.h).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "ds_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+namespace dsi {
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+ds_status fail(ds_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+ds_status cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                   cudaGetErrorString(e) + ")";
+    return DS_ERR_CUDA;
+}
+
+ds_status ensure_scratch(ds_ctx* ctx, size_t bytes, void** out) {
+    if (bytes > ctx->scratch_bytes) {
+        if (ctx->scratch) {
+            DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            DS_CUDA_TRY(cudaFree(ctx->scratch));
+            ctx->scratch = nullptr;
+            ctx->scratch_bytes = 0;
+        }
+        size_t want = align_up(bytes < (1u << 20) ? (1u << 20) : bytes, 1u << 20);
+        DS_CUDA_TRY(cudaMalloc(&ctx->scratch, want));
+        ctx->scratch_bytes = want;
+    }
+    *out = ctx->scratch;
+    return DS_OK;
+}
+
+ds_status ensure_pinned(ds_ctx* ctx, size_t bytes, void** out) {
+    if (bytes > ctx->pinned_bytes) {
+        if (ctx->pinned) {
+            DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            DS_CUDA_TRY(cudaFreeHost(ctx->pinned));
+            ctx->pinned = nullptr;
+            ctx->pinned_bytes = 0;
+        }
+        size_t want = align_up(bytes < (1u << 16) ? (1u << 16) : bytes, 1u << 16);
+        DS_CUDA_TRY(cudaMallocHost(&ctx->pinned, want));
+        ctx->pinned_bytes = want;
+    }
+    *out = ctx->pinned;
+    return DS_OK;
+}
+
+} // namespace dsi
+
+extern "C" {
+
+const char* ds_version(void) { return "ds_b200 abi 1 (sm_100a)"; }
+
+const char* ds_last_error(void) { return g_last_error.c_str(); }
+
+ds_status ds_ctx_create(int device, ds_ctx** out) {
+    if (!out) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "ds_ctx_create: out is null");
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return dsi::fail(DS_ERR_NO_DEVICE, "ds_ctx_create: no CUDA device visible");
+    if (device < 0 || device >= n)
+        return dsi::fail(DS_ERR_INVALID_ARGUMENT, "ds_ctx_create: device index out of range");
+    cudaDeviceProp prop;
+    DS_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return dsi::fail(DS_ERR_NO_DEVICE, "ds_ctx_create: kernels are built for sm_100a only, "
+                                           "device is sm_" + std::to_string(prop.major) +
+                                               std::to_string(prop.minor));
+    DS_CUDA_TRY(cudaSetDevice(device));
+    ds_ctx* ctx = new ds_ctx();
+    ctx->device = device;
+    e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return dsi::cuda_fail(e, "cudaStreamCreate");
+    }
+    *out = ctx;
+    return DS_OK;
+}
+
+ds_status ds_ctx_destroy(ds_ctx* ctx) {
+    if (!ctx) return DS_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return DS_OK;
+}
+
+ds_status ds_ctx_synchronize(ds_ctx* ctx) {
+    if (!ctx) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null ctx");
+    DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return DS_OK;
+}
+
+int64_t ds_ctx_launch_count(const ds_ctx* ctx) {
+    return ctx ? ctx->launches.load(std::memory_order_relaxed) : 0;
+}
+
+void* ds_ctx_stream(ds_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+} // extern "C"

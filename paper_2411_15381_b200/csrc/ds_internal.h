@@ -1,0 +1,52 @@
+// Internal host-side plumbing shared by the .cu translation units: the
+// context object behind ds_ctx*, error capture, grow-only device scratch.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "ds_gpu.h"
+
+struct ds_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::atomic<int64_t> launches{0};
+    // grow-only device scratch for the host-buffer (copying) entry points
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    // pinned host staging for small results
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+};
+
+namespace dsi {
+
+// Thread-local last error text (ds_last_error).
+void set_error(const std::string& msg);
+ds_status fail(ds_status s, const std::string& msg);
+ds_status cuda_fail(cudaError_t e, const char* what);
+
+// Device scratch of at least `bytes` (stream-ordered reuse; callers on one
+// ctx are serialized by the stream).
+ds_status ensure_scratch(ds_ctx* ctx, size_t bytes, void** out);
+ds_status ensure_pinned(ds_ctx* ctx, size_t bytes, void** out);
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+} // namespace dsi
+
+#define DS_CUDA_TRY(expr)                                                        \
+    do {                                                                         \
+        cudaError_t e_ = (expr);                                                 \
+        if (e_ != cudaSuccess) return dsi::cuda_fail(e_, #expr);                 \
+    } while (0)
+
+#define DS_LAUNCH_CHECK(ctx, what)                                               \
+    do {                                                                         \
+        (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                 \
+        cudaError_t e_ = cudaGetLastError();                                     \
+        if (e_ != cudaSuccess) return dsi::cuda_fail(e_, what);                  \
+    } while (0)

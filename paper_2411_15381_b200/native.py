@@ -1,0 +1,249 @@
+"""ctypes binding of libds_b200.so (the C ABI in include/ds_gpu.h).
+
+There is no CPU fallback: if the library is missing or no sm_100 device is
+visible, every entry point raises. Status codes map to the exception types the
+reference throws (allocator.cpp:12-36, profiles.cpp:20-26,98-100,108-112):
+
+    DS_ERR_INVALID_ARGUMENT -> InvalidArgument  (std::invalid_argument)
+    DS_ERR_DOMAIN           -> DomainError      (std::domain_error)
+    DS_ERR_INVARIANT        -> InvariantError   (diffserve::InvariantError)
+    DS_ERR_OUT_OF_RANGE     -> OutOfRange       (std::out_of_range)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libds_b200.so")
+
+
+class DsError(RuntimeError):
+    status = -1
+
+
+class InvalidArgument(DsError, ValueError):
+    status = abi.ERR_INVALID_ARGUMENT
+
+
+class DomainError(DsError, ValueError):
+    status = abi.ERR_DOMAIN
+
+
+class InvariantError(DsError):
+    status = abi.ERR_INVARIANT
+
+
+class OutOfRange(DsError, IndexError):
+    status = abi.ERR_OUT_OF_RANGE
+
+
+class CudaError(DsError):
+    status = abi.ERR_CUDA
+
+
+class NoDevice(DsError):
+    status = abi.ERR_NO_DEVICE
+
+
+class CapacityError(DsError):
+    status = abi.ERR_CAPACITY
+
+
+_EXC = {c.status: c for c in (InvalidArgument, DomainError, InvariantError, OutOfRange,
+                              CudaError, NoDevice, CapacityError)}
+
+_lib = None
+c_p = ctypes.c_void_p
+i32 = ctypes.c_int32
+i64 = ctypes.c_int64
+u64 = ctypes.c_uint64
+f64 = ctypes.c_double
+
+# (name, restype, argtypes) for every symbol include/ds_gpu.h declares.
+SIGNATURES = [
+    ("ds_version", ctypes.c_char_p, []),
+    ("ds_last_error", ctypes.c_char_p, []),
+    ("ds_ctx_create", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(c_p)]),
+    ("ds_ctx_destroy", ctypes.c_int, [c_p]),
+    ("ds_ctx_synchronize", ctypes.c_int, [c_p]),
+    ("ds_ctx_launch_count", i64, [c_p]),
+    ("ds_ctx_stream", c_p, [c_p]),
+    ("ds_plan_batch", ctypes.c_int, [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, c_p]),
+    ("ds_plan_batch_device", ctypes.c_int, [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, c_p, c_p]),
+    ("ds_plan_validate", ctypes.c_int, [c_p, i32, c_p, i32, c_p, c_p, i32]),
+    ("ds_score_latent", ctypes.c_int, [c_p, c_p, u64, i64, c_p, c_p]),
+    ("ds_score_latent_device", ctypes.c_int, [c_p, c_p, u64, i64, c_p, c_p, c_p]),
+    ("ds_route", ctypes.c_int, [c_p, c_p, i32, i64, c_p, i32, i64, c_p, c_p]),
+    ("ds_route_device", ctypes.c_int, [c_p, c_p, i32, i64, c_p, i32, i64, c_p, c_p, c_p]),
+    ("ds_route_scratch_bytes", ctypes.c_size_t, [i64, i32]),
+    ("ds_curve_observe", ctypes.c_int, [c_p, c_p, c_p, i32, i64, f64]),
+    ("ds_curve_observe_device", ctypes.c_int, [c_p, c_p, c_p, i32, i64, f64, c_p]),
+    ("ds_disc_create", ctypes.c_int, [c_p, u64, ctypes.POINTER(c_p)]),
+    ("ds_disc_destroy", ctypes.c_int, [c_p]),
+    ("ds_disc_export", ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+    ("ds_disc_score", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p]),
+    ("ds_disc_score_device", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p, c_p]),
+    ("ds_synth_images_device", ctypes.c_int, [c_p, u64, u64, i64, i32, i32, c_p, c_p]),
+]
+
+
+def lib():
+    """Load libds_b200.so (raises if it was not built: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(
+                f"{LIB_PATH} missing: run __graft_entry__.build() (there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != abi.OK:
+        msg = lib().ds_last_error().decode(errors="replace")
+        raise _EXC.get(status, DsError)(msg)
+
+
+class Context:
+    """One ds_ctx (device + stream). Not thread-safe, like the reference's
+    Simulation."""
+
+    def __init__(self, device: int = 0):
+        h = c_p()
+        check(lib().ds_ctx_create(device, ctypes.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            lib().ds_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return lib().ds_ctx_stream(self.handle) or 0
+
+    def launches(self) -> int:
+        return int(lib().ds_ctx_launch_count(self.handle))
+
+    def synchronize(self):
+        check(lib().ds_ctx_synchronize(self.handle))
+
+    # ---- planner ------------------------------------------------------
+    def plan_batch(self, problems: np.ndarray, cascades: np.ndarray, grid_values: np.ndarray,
+                   grid_offsets: np.ndarray) -> np.ndarray:
+        problems = np.ascontiguousarray(problems, abi.PROBLEM)
+        cascades = np.ascontiguousarray(cascades, abi.CASCADE)
+        grid_values = np.ascontiguousarray(grid_values, np.float64)
+        grid_offsets = np.ascontiguousarray(grid_offsets, np.int32)
+        out = np.zeros(len(problems), abi.PLAN)
+        check(lib().ds_plan_batch(self.handle, abi.ptr(problems), len(problems),
+                                  abi.ptr(cascades), len(cascades), abi.ptr(grid_values),
+                                  abi.ptr(grid_offsets), len(grid_offsets) - 1, abi.ptr(out)))
+        return out
+
+    # ---- latent scorer --------------------------------------------------
+    def score_latent(self, model: np.ndarray, id0: int, n: int, with_quality: bool = False):
+        model = np.ascontiguousarray(model, abi.QUERY_MODEL)
+        conf = np.zeros(n, np.float64)
+        ql = np.zeros(n, np.float64) if with_quality else None
+        check(lib().ds_score_latent(self.handle, abi.ptr(model), id0, n, abi.ptr(conf),
+                                    abi.ptr(ql)))
+        return (conf, ql) if with_quality else conf
+
+    # ---- router ---------------------------------------------------------
+    def route(self, conf: np.ndarray, thresholds, index_base: int = 0, with_lists: bool = True):
+        conf = np.ascontiguousarray(conf)
+        if conf.dtype == np.float64:
+            dt = abi.CONF_F64
+        elif conf.dtype == np.float32:
+            dt = abi.CONF_F32
+        else:
+            raise TypeError("confidences must be float64 or float32")
+        thr = np.ascontiguousarray(np.atleast_1d(np.asarray(thresholds, np.float64)))
+        n, nt = len(conf), len(thr)
+        counts = np.zeros(nt, np.int64)
+        idx = np.zeros(nt * max(n, 1), np.int64) if with_lists else None
+        check(lib().ds_route(self.handle, abi.ptr(conf), dt, n, abi.ptr(thr), nt, index_base,
+                             abi.ptr(idx), abi.ptr(counts)))
+        if not with_lists:
+            return counts, None
+        lists = [idx[k * n: k * n + counts[k]].copy() for k in range(nt)]
+        return counts, lists
+
+    # ---- deferral curve -------------------------------------------------
+    def curve_observe(self, curve: np.ndarray, conf: np.ndarray, decay: float) -> np.ndarray:
+        curve = np.array(curve, abi.CURVE)  # copy: the call updates in place
+        conf = np.ascontiguousarray(conf)
+        dt = abi.CONF_F64 if conf.dtype == np.float64 else abi.CONF_F32
+        if conf.dtype not in (np.float64, np.float32):
+            raise TypeError("confidences must be float64 or float32")
+        check(lib().ds_curve_observe(self.handle, abi.ptr(curve), abi.ptr(conf), dt, len(conf),
+                                     decay))
+        return curve
+
+
+class Discriminator:
+    """PatchDisc scorer (ds_disc_*), weights generated on the device from a seed."""
+
+    def __init__(self, ctx: Context, weight_seed: int = 2024):
+        self.ctx = ctx
+        h = c_p()
+        check(lib().ds_disc_create(ctx.handle, weight_seed, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().ds_disc_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def export(self) -> dict:
+        from . import abi as _abi  # noqa: F401
+        w1 = np.zeros((768, 256), np.uint16)
+        w2 = np.zeros((256, 1024), np.uint16)
+        w3 = np.zeros((1024, 256), np.uint16)
+        b1 = np.zeros(256, np.float32)
+        b2 = np.zeros(1024, np.float32)
+        b3 = np.zeros(256, np.float32)
+        hw = np.zeros(256, np.float32)
+        hb = np.zeros(1, np.float32)
+        check(lib().ds_disc_export(self.handle, abi.ptr(w1), abi.ptr(w2), abi.ptr(w3),
+                                   abi.ptr(b1), abi.ptr(b2), abi.ptr(b3), abi.ptr(hw),
+                                   abi.ptr(hb)))
+        return dict(w1=w1, w2=w2, w3=w3, b1=b1, b2=b2, b3=b3, head_w=hw, head_b=float(hb[0]))
+
+    def score(self, images: np.ndarray) -> np.ndarray:
+        images = np.ascontiguousarray(images, np.uint8)
+        n, h, w, c = images.shape
+        if c != 3:
+            raise ValueError("images must be NHWC with 3 channels")
+        conf = np.zeros(n, np.float32)
+        check(lib().ds_disc_score(self.handle, abi.ptr(images), n, h, w, abi.ptr(conf)))
+        return conf
+
+    def score_device(self, images_ptr: int, n: int, h: int, w: int, conf_ptr: int,
+                     stream: int = 0):
+        check(lib().ds_disc_score_device(self.handle, c_p(images_ptr), n, h, w, c_p(conf_ptr),
+                                         c_p(stream)))

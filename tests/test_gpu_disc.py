@@ -1,0 +1,81 @@
+"""GPU parity: the fused tcgen05 discriminator (K5-K7) vs its CPU restatement
+(oracle/disc_oracle.py). Parity is UNPINNED against the reference, which has
+no discriminator network; tolerance is north_star's 1e-3
+relative, floored at |c| = 1e-2 (SURVEY.md section 7 hard part 4)."""
+import numpy as np
+import pytest
+
+from oracle import disc_oracle
+from paper_2411_15381_b200 import native
+from paper_2411_15381_b200.api import default_context
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def disc():
+    return native.Discriminator(default_context(), weight_seed=2024)
+
+
+@pytest.fixture(scope="module")
+def weights(disc):
+    return disc.export()
+
+
+def synth_device(ctx, seed, id0, n, h, w):
+    import torch
+    buf = torch.empty(n * h * w * 3, dtype=torch.uint8, device="cuda")
+    native.check(native.lib().ds_synth_images_device(ctx.handle, seed, id0, n, h, w,
+                                                     native.c_p(buf.data_ptr()),
+                                                     native.c_p(0)))
+    torch.cuda.synchronize()
+    return buf.cpu().numpy().reshape(n, h, w, 3)
+
+
+def test_synth_images_match_host_restatement():
+    ctx = default_context()
+    got = synth_device(ctx, 1, 5, 3, 64, 48)
+    want = disc_oracle.synth_images(1, 5, 3, 64, 48)
+    assert np.array_equal(got, want)
+
+
+def check_conf(got, want):
+    err = np.abs(got.astype(np.float64) - want.astype(np.float64))
+    lim = TOL * np.maximum(np.abs(want), 1e-2)
+    assert np.all(err <= lim), f"max err {err.max():.3e}, worst idx {int(np.argmax(err / lim))}"
+
+
+def test_disc_matches_cpu_restatement_512(disc, weights):
+    imgs = disc_oracle.synth_images(1, 0, 6, 512, 512)
+    got = disc.score(imgs)
+    want = disc_oracle.disc_forward(imgs, weights)
+    check_conf(got, want)
+    assert 0.0 < got.min() and got.max() < 1.0
+
+
+def test_disc_matches_cpu_restatement_1024(disc, weights):
+    imgs = disc_oracle.synth_images(3, 100, 2, 1024, 1024)
+    check_conf(disc.score(imgs), disc_oracle.disc_forward(imgs, weights))
+
+
+def test_disc_non_square_and_ragged_counts(disc, weights):
+    imgs = disc_oracle.synth_images(7, 9, 3, 256, 1024)     # 16 x 64 patches = 1024 tokens
+    check_conf(disc.score(imgs), disc_oracle.disc_forward(imgs, weights))
+
+
+def test_disc_spread_and_determinism(disc):
+    imgs = disc_oracle.synth_images(1, 0, 64, 512, 512)
+    a = disc.score(imgs)
+    b = disc.score(imgs)
+    assert np.array_equal(a, b)                     # fixed reduction order
+    assert a.std() > 0.05                           # calibrated head spreads confidences
+    assert (a < 0.5).any() and (a > 0.5).any()
+
+
+def test_disc_rejects_bad_shapes(disc):
+    with pytest.raises(native.InvalidArgument):
+        disc.score(np.zeros((1, 100, 100, 3), np.uint8))
+    with pytest.raises(native.InvalidArgument):
+        disc.score(np.zeros((1, 128, 128, 3), np.uint8))   # 64 patches: not a 128-token tile
