@@ -1,0 +1,585 @@
+#!/usr/bin/env python
+"""Benchmark of the DiffServe hot path on B200 (BASELINE.json metric:
+"images scored+routed/sec and planner candidates/sec at 1/2/4/8 B200 vs CPU").
+
+One STEP (the headline `value`, SURVEY.md 8(d) config 2 "Cascade 2"):
+  5,000 synthetic 512x512x3 u8 images resident in HBM per GPU
+  -> fused tcgen05 discriminator (K5-K7) -> confidences
+  -> route at the 101 grid thresholds k/100 (K2: ordered heavy-queue ids)
+  -> deferral-curve replay of the 5,000 confidences in id order (K3, decay 0.999)
+  -> (N > 1) NCCL all-gather of the per-GPU routed counts + exclusive scan
+     (global heavy-queue offsets; SURVEY 8(e), config 5 scale-out).
+Per-GPU work is fixed (weak scaling). Inputs (3.9 GB) exceed L2 (126 MB), so
+no flush is needed between steps.
+
+Secondary legs in the same JSON line:
+  planner : K1 over 4,096 config-4 problems (fitted 32x32 tables, 101 thresholds,
+            S in {16,32,64,128}); unit = one (problem, t, b1, b2) candidate.
+  latent  : the reference's own scorer (sample_query, bit-parity mode, K4) +
+            route at t = 0.5 + curve replay over 1M queries per GPU (config 5).
+CPU baselines run on this box's host cores on bounded samples (rank 0, N=1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images scored+routed/sec and planner candidates/sec at 1/2/4/8 B200 vs CPU"
+N_IMG = 5000
+H = W = 512
+IMG_SEED = 1
+WEIGHT_SEED = 2024
+DISC_FLOP_PER_IMG = 2 * (768 * 256 + 256 * 1024 + 1024 * 256) * ((H // 16) * (W // 16))
+N_PLAN = 4096
+CANDS_PER_PROBLEM = 101 * 32 * 32
+N_LATENT = 1_000_000
+DECAY = 0.999
+CPU_DISC_SAMPLE = 96          # images for the CPU port of the discriminator
+CPU_PLAN_SAMPLE = 256         # problems for the CPU reference planner
+CPU_LATENT_SAMPLE = 200_000   # queries for the CPU reference scorer
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 8:
+                continue
+            for k, nm in enumerate(names):
+                if r[4 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU implementation of the same path on the host cores
+# ---------------------------------------------------------------------------
+
+def cpu_images_leg(n_img: int):
+    """The CPU port of the discriminator (oracle/disc_oracle.py, numpy on all
+    cores) + the reference's own route loop (oracle/_ref, cluster.cpp:290-306)
+    at all 101 thresholds over the same confidences."""
+    from oracle import disc_oracle, lib
+    from paper_2411_15381_b200 import abi, workloads
+    # weights: the same deterministic network as the GPU (export needs no GPU
+    # compute beyond creation, so regenerate on the host from the seed)
+    wts = host_weights()
+    imgs = disc_oracle.synth_images(IMG_SEED, 0, n_img, H, W)
+    grid = workloads.make_grid(0.01)
+    prior = np.zeros((), abi.CURVE)
+    s = np.asarray(workloads.SHIPPED_PRIOR_SAMPLES, np.float64)
+    t0 = time.perf_counter()
+    conf = disc_oracle.disc_forward(imgs, wts).astype(np.float64)
+    idx = np.zeros(n_img, np.int64)
+    cnt = np.zeros(1, np.int64)
+    if lib.ref_available():
+        r = lib.ref()
+        for k, t in enumerate(grid):
+            curve = prior.copy()
+            r.dsref_curve_from_samples(abi.ptr(s), len(s), abi.ptr(curve))
+            r.dsref_route_loop(abi.ptr(conf), n_img, float(t), 1 if k == 0 else 0, DECAY,
+                               abi.ptr(curve), abi.ptr(idx), abi.ptr(cnt))
+        kind = "reference+port"
+    else:
+        p = lib.port()
+        for k, t in enumerate(grid):
+            curve = prior.copy()
+            p.dso_route_loop(abi.ptr(conf), n_img, float(t), 1 if k == 0 else 0, DECAY,
+                             abi.ptr(curve), abi.ptr(idx), abi.ptr(cnt))
+        kind = "port"
+    dt = time.perf_counter() - t0
+    return n_img / dt, kind
+
+
+def cpu_planner_leg(problems, cascades, grid, offs, threads):
+    from oracle import lib
+    from paper_2411_15381_b200 import abi
+    out = np.zeros(len(problems), abi.PLAN)
+    t0 = time.perf_counter()
+    if lib.ref_available():
+        lib.ref().dsref_plan_batch(abi.ptr(problems), len(problems), abi.ptr(cascades),
+                                   len(cascades), abi.ptr(grid), abi.ptr(offs), 1, abi.ptr(out),
+                                   threads)
+        kind = "reference"
+    else:
+        st = np.zeros(len(problems), np.int32)
+        lib.port().dso_plan_batch(abi.ptr(problems), len(problems), abi.ptr(cascades),
+                                  abi.ptr(grid), abi.ptr(offs), abi.ptr(out), abi.ptr(st),
+                                  threads)
+        kind = "port"
+    dt = time.perf_counter() - t0
+    return len(problems) * CANDS_PER_PROBLEM / dt, kind, out
+
+
+def cpu_latent_leg(n, threads):
+    """sample_query over ids (all cores) then the sequential observe+defers loop."""
+    from oracle import lib
+    from paper_2411_15381_b200 import abi, workloads
+    m = workloads.query_model()
+    conf = np.zeros(n)
+    idx = np.zeros(n, np.int64)
+    cnt = np.zeros(1, np.int64)
+    curve = workloads.uniform_prior()
+    t0 = time.perf_counter()
+    if lib.ref_available():
+        lib.ref().dsref_sample_queries(abi.ptr(m), 0, n, 5.0, abi.ptr(conf), None, threads)
+        lib.ref().dsref_route_loop(abi.ptr(conf), n, 0.5, 1, DECAY, abi.ptr(curve), abi.ptr(idx),
+                                   abi.ptr(cnt))
+        kind = "reference"
+    else:
+        lib.port().dso_sample_queries(abi.ptr(m), 0, n, abi.ptr(conf), None, threads)
+        lib.port().dso_route_loop(abi.ptr(conf), n, 0.5, 1, DECAY, abi.ptr(curve), abi.ptr(idx),
+                                  abi.ptr(cnt))
+        kind = "port"
+    return n / (time.perf_counter() - t0), kind
+
+
+def host_weights():
+    """The discriminator weights exactly as ds_disc_create makes them, read
+    back from a (cached) GPU export when available; the reference arm on a
+    CPU-only host needs the cached copy under gpurun_out/ or profiles/."""
+    cache = os.path.join(ROOT, "profiles", f"disc_weights_seed{WEIGHT_SEED}.npz")
+    if os.path.exists(cache):
+        d = dict(np.load(cache))
+        d["head_b"] = float(d["head_b"])
+        return d
+    from paper_2411_15381_b200 import native
+    ctx = native.Context(0)
+    disc = native.Discriminator(ctx, WEIGHT_SEED)
+    w = disc.export()
+    disc.close()
+    ctx.close()
+    return w
+
+
+def planner_inputs():
+    from paper_2411_15381_b200 import abi, workloads
+    from oracle import lib  # noqa: F401  (curve via port below)
+    cas = np.zeros(3, abi.CASCADE)
+    for i, name in enumerate(["cascade1", "cascade2", "cascade3"]):
+        light, heavy, slo = workloads.fitted_tables(name)
+        cas[i] = workloads.make_cascade(light, heavy, slo)
+    probs = []
+    per = N_PLAN // 12
+    for ci in range(3):
+        for s in (16, 32, 64, 128):
+            p = workloads.c2_problems(cas[ci], s, per, seed=7 + 100 * ci + s)
+            p["cascade"] = ci
+            probs.append(p)
+    pro = np.concatenate(probs)
+    grid = workloads.make_grid(0.01)
+    offs = np.array([0, len(grid)], np.int32)
+    return pro, cas, grid, offs
+
+
+def sampled_curves(cas):
+    """Each config-4 cascade's curve = from_samples of 5K sample_query
+    confidences; computed with the C restatement."""
+    from oracle import lib
+    from paper_2411_15381_b200 import abi, workloads
+    m = workloads.query_model()
+    conf = np.zeros(5000)
+    lib.port().dso_sample_queries(abi.ptr(m), 0, 5000, abi.ptr(conf), None, 8)
+    for i in range(len(cas)):
+        c = np.zeros((), abi.CURVE)
+        lib.port().dso_curve_observe(abi.ptr(c), abi.ptr(conf), 5000, 1.0)
+        cas[i]["deferral"] = c
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    kind = None
+    for i in range(args.warmup + args.steps):
+        v, kind = cpu_images_leg(max(4, CPU_DISC_SAMPLE // 4))
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "images/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * max(4, CPU_DISC_SAMPLE // 4) / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": "cascade2 5K 512x512 score+route (101 thresholds)",
+                                        "global_batch": N_IMG, "sample_images": max(4, CPU_DISC_SAMPLE // 4)},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": kind,
+                         "sample": f"{max(4, CPU_DISC_SAMPLE // 4)} images 512x512 per step"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_15381_b200 import abi, native, workloads
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = native.Context(local)
+    L = native.lib()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    disc = native.Discriminator(ctx, WEIGHT_SEED)
+    if rank == 0:
+        # cache the exported weights so the CPU reference arm uses the same network
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    dev = torch.device("cuda", local)
+
+    # ---- inputs resident in HBM ---------------------------------------------
+    id0 = rank * N_IMG
+    images = torch.empty(N_IMG * H * W * 3, dtype=torch.uint8, device=dev)
+    native.check(L.ds_synth_images_device(ctx.handle, IMG_SEED, id0, N_IMG, H, W,
+                                          native.c_p(images.data_ptr()), native.c_p(ctx.stream)))
+    grid_t = torch.tensor(workloads.make_grid(0.01), dtype=torch.float64, device=dev)
+    NT = grid_t.numel()
+    conf = torch.empty(N_IMG, dtype=torch.float32, device=dev)
+    heavy = torch.empty(NT * N_IMG, dtype=torch.int64, device=dev)
+    counts = torch.empty(NT, dtype=torch.int64, device=dev)
+    prior = np.zeros((), abi.CURVE)
+    from oracle import lib as _olib  # prior curve = from_samples(shipped samples)
+    s = np.asarray(workloads.SHIPPED_PRIOR_SAMPLES, np.float64)
+    _olib.port().dso_curve_observe(abi.ptr(prior), abi.ptr(s), len(s), 1.0)
+    prior_t = torch.from_numpy(prior.view(np.uint8).copy()).to(dev)
+    curve_t = torch.empty_like(prior_t)
+    gathered = torch.empty(ws * NT, dtype=torch.int64, device=dev)
+
+    def step(ev=None):
+        with torch.cuda.stream(stream):
+            if ev is not None:
+                ev[0].record(stream)
+            native.check(L.ds_disc_score_device(disc.handle, native.c_p(images.data_ptr()),
+                                                N_IMG, H, W, native.c_p(conf.data_ptr()),
+                                                native.c_p(ctx.stream)))
+            if ev is not None:
+                ev[1].record(stream)
+            native.check(L.ds_route_device(ctx.handle, native.c_p(conf.data_ptr()), abi.CONF_F32,
+                                           N_IMG, native.c_p(grid_t.data_ptr()), NT, id0,
+                                           native.c_p(heavy.data_ptr()),
+                                           native.c_p(counts.data_ptr()), native.c_p(ctx.stream)))
+            curve_t.copy_(prior_t)
+            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve_t.data_ptr()),
+                                                   native.c_p(conf.data_ptr()), abi.CONF_F32,
+                                                   N_IMG, DECAY, native.c_p(ctx.stream)))
+            if ws > 1:
+                dist.all_gather_into_tensor(gathered, counts)
+                # exclusive scan over ranks: this rank's offset in each global heavy queue
+                offsets = gathered.view(ws, NT)[:rank].sum(0)  # noqa: F841
+
+    # ---- warmup + timed region -------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    n0 = ctx.launches()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launches() - n0
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    disc_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    t = torch.tensor([total_ms, disc_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, disc_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = ws * N_IMG / (ms_per_step / 1000.0)
+
+    # ---- parity spot-check inside the benchmark: route vs confidences -------
+    c_host = conf.cpu().numpy().astype(np.float64)
+    cnt_host = counts.cpu().numpy()
+    want_cnt = np.array([(c_host < t).sum() for t in workloads.make_grid(0.01)])
+    parity_ok = bool(np.array_equal(cnt_host, want_cnt))
+
+    # ---- e2e: the C-ABI calls with HOST buffers, copies inside the timed region
+    pinned = torch.empty(N_IMG * H * W * 3, dtype=torch.uint8, pin_memory=True)
+    pinned.copy_(images)
+    host_imgs = pinned.numpy().reshape(N_IMG, H, W, 3)
+    grid_np = workloads.make_grid(0.01)
+    e2e_steps = max(2, min(args.steps, 5))
+
+    def e2e_step():
+        c = disc.score(host_imgs)
+        cnts, _ = ctx.route(c, grid_np, index_base=id0, with_lists=True)
+        ctx.curve_observe(prior, c, DECAY)
+        return c, cnts
+
+    e2e_step()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(e2e_steps):
+        c, cnts = e2e_step()
+        d2h = c.nbytes + int(cnts.sum()) * 8 + cnts.nbytes + abi.CURVE.itemsize
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+    e2e_value = ws * N_IMG / float(e[0])
+    h2d = N_IMG * H * W * 3 + grid_np.nbytes + 2 * abi.CURVE.itemsize
+
+    # ---- planner leg (config 4) -------------------------------------------------
+    pro, cas, grid, offs = planner_inputs()
+    sampled_curves(cas)
+    d_pro = torch.from_numpy(pro.view(np.uint8).copy()).to(dev)
+    d_cas = torch.from_numpy(cas.view(np.uint8).copy()).to(dev)
+    d_grid = torch.from_numpy(grid.copy()).to(dev)
+    d_offs = torch.from_numpy(offs.copy()).to(dev)
+    d_out = torch.empty(len(pro) * abi.PLAN.itemsize, dtype=torch.uint8, device=dev)
+
+    def plan_step():
+        native.check(L.ds_plan_batch_device(ctx.handle, native.c_p(d_pro.data_ptr()), len(pro),
+                                            native.c_p(d_cas.data_ptr()), len(cas),
+                                            native.c_p(d_grid.data_ptr()),
+                                            native.c_p(d_offs.data_ptr()), 1,
+                                            native.c_p(d_out.data_ptr()), native.c_p(ctx.stream)))
+    for _ in range(args.warmup):
+        plan_step()
+    torch.cuda.synchronize()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        plan_step()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    plan_ms = p0.elapsed_time(p1) / args.steps
+    pt = torch.tensor([plan_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+    plan_ms = float(pt[0])
+    plan_value = ws * len(pro) * CANDS_PER_PROBLEM / (plan_ms / 1000.0)
+    gpu_plans = d_out.cpu().numpy().view(abi.PLAN)
+    # planner e2e through the host-buffer C-ABI call
+    ctx.plan_batch(pro, cas, grid, offs)
+    t0 = time.perf_counter()
+    for _ in range(3):
+        ctx.plan_batch(pro, cas, grid, offs)
+    plan_e2e = ws * len(pro) * CANDS_PER_PROBLEM / ((time.perf_counter() - t0) / 3)
+
+    # ---- latent leg (config 5: 1M queries per GPU, reference-parity scorer) ------
+    lconf = torch.empty(N_LATENT, dtype=torch.float64, device=dev)
+    lheavy = torch.empty(N_LATENT, dtype=torch.int64, device=dev)
+    lcount = torch.empty(1, dtype=torch.int64, device=dev)
+    lcurve = torch.empty_like(prior_t)
+    thr = torch.tensor([0.5], dtype=torch.float64, device=dev)
+    qm = workloads.query_model()
+    lat_id0 = rank * N_LATENT
+    levs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def latent_step(ev=False):
+        with torch.cuda.stream(stream):
+            if ev:
+                levs[0].record(stream)
+            native.check(L.ds_score_latent_device(ctx.handle, abi.ptr(qm), lat_id0, N_LATENT,
+                                                  native.c_p(lconf.data_ptr()), native.c_p(0),
+                                                  native.c_p(ctx.stream)))
+            if ev:
+                levs[1].record(stream)
+            native.check(L.ds_route_device(ctx.handle, native.c_p(lconf.data_ptr()), abi.CONF_F64,
+                                           N_LATENT, native.c_p(thr.data_ptr()), 1, lat_id0,
+                                           native.c_p(lheavy.data_ptr()),
+                                           native.c_p(lcount.data_ptr()), native.c_p(ctx.stream)))
+            if ev:
+                levs[2].record(stream)
+            lcurve.copy_(prior_t)
+            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(lcurve.data_ptr()),
+                                                   native.c_p(lconf.data_ptr()), abi.CONF_F64,
+                                                   N_LATENT, DECAY, native.c_p(ctx.stream)))
+            if ev:
+                levs[3].record(stream)
+    latent_step()
+    torch.cuda.synchronize()
+    latent_step(ev=True)
+    torch.cuda.synchronize()
+    lat_ms = [levs[i].elapsed_time(levs[i + 1]) for i in range(3)]
+    lt = torch.tensor([sum(lat_ms)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+    latent_value = ws * N_LATENT / (float(lt[0]) / 1000.0)
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        achieved_tflops = N_IMG * DISC_FLOP_PER_IMG / (disc_ms / 1000.0) / 1e12
+        peak_sus = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "disc_ncu_summary.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch_5000img")
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (device-generated 512x512 u8 images; seeded PatchDisc weights)",
+            "config": {"workload": "cascade2: 5K synthetic 512x512 images/GPU, discriminator "
+                                   "score + route at 101 thresholds + curve replay",
+                       "global_batch": ws * N_IMG, "image_hw": [H, W],
+                       "thresholds": NT, "parallelism": f"dp{ws} (query shards)",
+                       "l2": "inputs 3.9 GB/GPU > 126 MB L2, no flush"},
+            "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": peak_sus,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / peak_sus,
+                         "traffic": traffic, "kernel": "disc_kernel",
+                         "peak_source": f"{peak_src} bf16_tflops_sustained",
+                         "frac_of_burst": achieved_tflops / float(peaks["bf16_tflops"]),
+                         "disc_ms_per_step": disc_ms,
+                         "flop_per_image": DISC_FLOP_PER_IMG},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "parity": {"route_counts_vs_confidences": parity_ok},
+            "planner": {"value": plan_value, "unit": "candidates/s", "problems": len(pro),
+                        "candidates_per_problem": CANDS_PER_PROBLEM, "ms_per_batch": plan_ms,
+                        "e2e": {"value": plan_e2e, "unit": "candidates/s"}},
+            "latent": {"value": latent_value, "unit": "queries/s", "queries_per_gpu": N_LATENT,
+                       "ms_score_route_curve": lat_ms,
+                       "roofline": {"bound": "int/fp64 issue (no tensor/HBM bound)"}},
+        }
+        if ws == 1 and not args.no_cpu:
+            threads = os.cpu_count() or 1
+            cv, ck = cpu_images_leg(CPU_DISC_SAMPLE)
+            line["cpu_baseline"] = {"value": cv, "unit": "images/s", "cores": threads,
+                                    "kind": "port" if ck != "reference" else ck,
+                                    "sample": f"{CPU_DISC_SAMPLE} images 512x512: numpy port of "
+                                              "the discriminator (no reference network) + the "
+                                              "reference route loop at 101 thresholds"}
+            sub = slice(0, CPU_PLAN_SAMPLE)
+            pv, pk, cpu_plans = cpu_planner_leg(np.ascontiguousarray(pro[sub]), cas, grid, offs,
+                                                threads)
+            line["planner"]["cpu_baseline"] = {
+                "value": pv, "unit": "candidates/s", "cores": threads, "kind": pk,
+                "sample": f"{CPU_PLAN_SAMPLE} config-4 problems, diffserve::solve on "
+                          f"{threads} threads"}
+            line["planner"]["parity_vs_cpu"] = bool(
+                gpu_plans[sub].tobytes() == cpu_plans.tobytes())
+            lv, lk = cpu_latent_leg(CPU_LATENT_SAMPLE, threads)
+            line["latent"]["cpu_baseline"] = {
+                "value": lv, "unit": "queries/s", "cores": threads, "kind": lk,
+                "sample": f"{CPU_LATENT_SAMPLE} queries: sample_query on {threads} threads + "
+                          "sequential observe/defers loop"}
+        print(json.dumps(line), flush=True)
+        try:
+            np.savez(os.path.join(ROOT, "gpurun_out", f"disc_weights_seed{WEIGHT_SEED}.npz"),
+                     **disc.export())
+        except Exception:
+            pass
+    disc.close()
+    ctx.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline legs")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()
