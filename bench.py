@@ -319,7 +319,7 @@ def run_gpu(args):
     from oracle import lib as _olib  # prior curve = from_samples(shipped samples)
     s = np.asarray(workloads.SHIPPED_PRIOR_SAMPLES, np.float64)
     _olib.port().dso_curve_observe(abi.ptr(prior), abi.ptr(s), len(s), 1.0)
-    prior_t = torch.from_numpy(prior.view(np.uint8).copy()).to(dev)
+    prior_t = torch.from_numpy(prior.reshape(1).view(np.uint8).copy()).to(dev)
     curve_t = torch.empty_like(prior_t)
     gathered = torch.empty(ws * NT, dtype=torch.int64, device=dev)
 

@@ -62,7 +62,16 @@ struct DiscParams {
     float* out;
     long long n_img;
     int h, w, px, tokens, tiles_per_img;
+    long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr = off)
 };
+
+// Trace slots (CTA 0 only): role r, tile t < kTraceTiles, event e < 16.
+constexpr int kTraceTiles = 8;
+#define DS_TRACE(role, tile, ev)                                                          \
+    do {                                                                                  \
+        if (P.trace && blockIdx.x == 0 && (tile) < kTraceTiles)                           \
+            P.trace[((role) * kTraceTiles + (tile)) * 16 + (ev)] = clock64();             \
+    } while (0)
 
 __device__ __forceinline__ float gelu_tanh(float x) {
     const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
@@ -162,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     mbar_wait(&r1_free, r1_phase);
                     r1_phase ^= 1;
                 }
+                if (tid == 0 && (dy == 0 || dy == 15)) DS_TRACE(0, tile, dy == 0 ? 0 : 1);
                 mbar_wait(&a_empty[astage], aphase ^ 1);
                 const uint32_t st = sbase + kR1 + astage * kAChunk;
 #pragma unroll
@@ -173,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 }
                 fence_proxy_async_smem();
                 mbar_arrive(&a_full[astage]);
+                if (tid == 0 && (dy == 0 || dy == 15)) DS_TRACE(0, tile, dy == 0 ? 2 : 3);
                 if (++astage == kAStages) { astage = 0; aphase ^= 1; }
                 const long long gn = g + kDepth;
                 if (gn < total_chunks) {
@@ -197,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 mbar_wait(&acc12_full, p12);
                 p12 ^= 1;
                 tc_fence_after();
+                if (ew == 0 && lane == 0) DS_TRACE(1, tile, 2 * (j + 1));
                 const uint32_t hbase = sbase + (j < 0 ? kR1 : kR2);
 #pragma unroll 1
                 for (int cb = 0; cb < 4; cb += 2) {
@@ -233,11 +245,13 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 fence_proxy_async_smem();
                 tc_fence_before();
                 mbar_arrive(&epi_done);
+                if (ew == 0 && lane == 0) DS_TRACE(1, tile, 2 * (j + 1) + 1);
             }
             // E3: acc3 -> ReLU(+b3) . w_head, summed over this thread's columns
             mbar_wait(&acc3_full, p3);
             p3 ^= 1;
             tc_fence_after();
+            if (ew == 0 && lane == 0) DS_TRACE(1, tile, 10);
             float part = 0.0f;
 #pragma unroll 1
             for (int cb = 0; cb < 4; cb += 2) {
@@ -256,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             }
             tc_fence_before();
             mbar_arrive(&acc3_empty);
+            if (ew == 0 && lane == 0) DS_TRACE(1, tile, 11);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
             const int buf = static_cast<int>(tile & 1);
@@ -318,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 }
             };
             for (long long tile = 0; tile < my_tiles; ++tile) {
+                DS_TRACE(2, tile, 0);
                 // GEMM1: 16 chunks (patch rows), K = 48 each
                 for (int c = 0; c < 16; ++c) {
                     mbar_wait(&a_full[as], ap);
@@ -332,10 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     release_b();
                 }
                 umma_commit(&acc12_full);
+                DS_TRACE(2, tile, 1);
                 for (int j = 0; j < 4; ++j) {
                     mbar_wait(&epi_done, ep);     // E1 (j=0) or E2_{j-1}: acc drained, H written
                     ep ^= 1;
                     tc_fence_after();
+                    DS_TRACE(2, tile, 2 + 2 * j);
                     if (j > 0) {
                         if (j == 1) {             // acc3 drained by the previous tile's E3
                             mbar_wait(&acc3_empty, e3p ^ 1);
@@ -346,13 +364,16 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     }
                     gemm_h(kR1, acc12, false);               // GEMM2, N-chunk j
                     umma_commit(&acc12_full);
+                    DS_TRACE(2, tile, 3 + 2 * j);
                     if (j == 3) umma_commit(&r1_free);       // H1 no longer read
                 }
                 mbar_wait(&epi_done, ep);                    // E2_3
                 ep ^= 1;
                 tc_fence_after();
+                DS_TRACE(2, tile, 10);
                 gemm_h(kR2, acc3, true);                     // GEMM3, K-chunk 3
                 umma_commit(&acc3_full);
+                DS_TRACE(2, tile, 11);
             }
         }
     }
@@ -457,7 +478,7 @@ struct ds_disc {
 namespace {
 
 ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w, float* out,
-                      int logits, cudaStream_t st) {
+                      int logits, cudaStream_t st, long long* trace = nullptr) {
     if (h % 16 || w % 16)
         return dsi::fail(DS_ERR_INVALID_ARGUMENT, "image height and width must be multiples of 16");
     const int tokens = (h / 16) * (w / 16);
@@ -477,6 +498,7 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     p.px = w / 16;
     p.tokens = tokens;
     p.tiles_per_img = tokens / kM;
+    p.trace = trace;
     static bool attr_set = false;
     if (!attr_set) {
         DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -619,4 +641,13 @@ extern "C" ds_status ds_disc_score(ds_disc* d, const uint8_t* nhwc, int64_t n, i
     DS_CUDA_TRY(cudaMemcpyAsync(conf, dconf, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
     DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return DS_OK;
+}
+
+// Debug entry (not part of include/ds_gpu.h): scores device images and writes
+// CTA 0's per-phase clock64 stamps (3 roles x 8 tiles x 16 events) to `trace`.
+extern "C" ds_status ds_disc_trace_device(ds_disc* d, const uint8_t* nhwc, int64_t n, int32_t h,
+                                          int32_t w, float* conf, long long* trace, void* stream) {
+    if (!d) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null disc");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+    return launch_disc(d, nhwc, n, h, w, conf, 0, st, trace);
 }

@@ -1,0 +1,54 @@
+"""Per-phase clock64 trace of disc_kernel CTA 0 (debug build path).
+
+Prints, per token tile, the cycle offsets of: A-builder (r1_free seen, first
+chunk stored, last chunk stored), epilogue (acc ready / done for E1, E2_0..3,
+E3) and the MMA issuer (tile start, GEMM1 issued, epi_done seen / GEMM2 issued
+per j, GEMM3 issued)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2411_15381_b200 import native  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+    ctx = native.Context(0)
+    L = native.lib()
+    L.ds_disc_trace_device.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_int64, ctypes.c_int32,
+                                                                ctypes.c_int32] + [ctypes.c_void_p] * 3
+    disc = native.Discriminator(ctx, 2024)
+    img = torch.empty(n * 512 * 512 * 3, dtype=torch.uint8, device="cuda")
+    native.check(L.ds_synth_images_device(ctx.handle, 1, 0, n, 512, 512,
+                                          native.c_p(img.data_ptr()), native.c_p(ctx.stream)))
+    conf = torch.empty(n, dtype=torch.float32, device="cuda")
+    tr = torch.zeros(3 * 8 * 16, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        native.check(L.ds_disc_trace_device(disc.handle, native.c_p(img.data_ptr()), n, 512, 512,
+                                            native.c_p(conf.data_ptr()), native.c_p(tr.data_ptr()),
+                                            native.c_p(ctx.stream)))
+    ctx.synchronize()
+    t = tr.cpu().numpy().reshape(3, 8, 16)
+    base = t[2, 0, 0]
+    names = {0: ["r1_free", "c0_done?", "c0_stored", "c15_stored"],
+             1: ["E1_rdy", "E1_done", "E20_rdy", "E20_done", "E21_rdy", "E21_done", "E22_rdy",
+                 "E22_done", "E23_rdy", "E23_done", "E3_rdy", "E3_done"],
+             2: ["start", "G1_iss", "ep0", "G20_iss", "ep1", "G21_iss", "ep2", "G22_iss", "ep3",
+                 "G23_iss", "ep4", "G33_iss"]}
+    for tile in range(8):
+        print(f"--- tile {tile}")
+        for role in (2, 1, 0):
+            vals = t[role, tile]
+            s = "  ".join(f"{nm}={int(vals[i] - base) if vals[i] else -1}"
+                          for i, nm in enumerate(names[role]))
+            print(f"  role{role}: {s}")
+    print("per-tile cycles (MMA start deltas):", np.diff(t[2, :, 0]).tolist())
+
+
+if __name__ == "__main__":
+    main()
