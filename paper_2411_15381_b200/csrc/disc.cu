@@ -5,25 +5,32 @@
 //
 //   u8 NHWC image -> 16x16x3 patches (token t = py*(W/16)+px, feature
 //   k = dy*48 + dx*3 + c) -> h1 = GELU_tanh(x @ W1 + b1)  [768 -> 256]
-//   -> h2 = ReLU(bf16(h1) @ W2 + b2) [256 -> 1024] -> h3 = ReLU(bf16(h2) @ W3 + b3)
+//   -> h2 = ReLU(bf16(h1) @ W2)  [256 -> 1024] -> h3 = ReLU(bf16(h2) @ W3)
 //   [1024 -> 256] -> logit = mean_t(h3 . w_head) + b_head -> sigmoid.
-//   (x is the raw pixel value; the (x-128)/64 normalisation is folded into
-//   W1 and b1.)
+// x is the raw pixel value; the (x-128)/64 input normalisation is folded into
+// W1 and b1. Layers 2 and 3 carry their biases as weights of CONSTANT hidden
+// features: W1[:,255] = 0 and b1[255] = 16 give h1[:,255] = GELU(16) = 16
+// exactly, so W2[255,:] is layer 2's bias (/16); W2[:,1023] is zero except
+// W2[255,1023] = 1, so h2[:,1023] = 16 and W3[1023,:] is layer 3's bias.
+// The epilogue therefore never adds a bias after GEMM2/GEMM3.
 //
-// One CTA per SM, persistent over whole images, M = 128 tokens per tile:
-//   warps 0-3   A-builder: 128-bit loads of 16 B pixel runs, u8 -> bf16,
-//               swizzled (SW128, K-major) stores into the A ring (16 chunks,
-//               one per patch row dy, K = 48 each)
-//   warps 4-11  epilogue: tcgen05.ld of the TMEM accumulators, bias +
-//               activation, bf16 pack, swizzled stores of H1/H2 (the next
-//               GEMM's A operand), and the head dot product + per-image sum
-//   warp 12     weight producer: 1-D bulk TMA of pre-swizzled 32 KB weight
-//               tiles (L2-resident, evict-last) into a 3-stage ring
+// One CTA per SM, persistent over whole images, M = 128 tokens per tile.
+//   warps 0-3   A-builder: 128-bit loads of 16 B pixel runs (thread = token,
+//               prefetched kDepth chunks ahead), u8 -> bf16 (exact), SW128
+//               stores into its own 3-stage ring (12 chunks of K=64 per tile)
+//   warps 4-11  epilogue: tcgen05.ld of the TMEM accumulators, activation,
+//               bf16 pack, SW128 stores of H1/H2 (next GEMM's A operand), and
+//               the head dot product + per-image mean
+//   warp 12     weight producer: 1-D bulk TMA of pre-swizzled 16 KB weight
+//               stages (256 x K=32, SW64; L2 evict-last) into a 3-stage ring
 //   warp 13     TMEM allocator + the single thread issuing tcgen05.mma
-// TMEM (512 columns): [0,256) accumulates GEMM1 and each 256-wide N-chunk of
-// GEMM2; [256,512) accumulates GEMM3. Shared memory: R1 (64 KB) holds the A
-// ring during GEMM1 and H1 afterwards; R2 (64 KB) holds one 256-wide chunk of
-// H2; 3 x 32 KB weight stages.
+// TMEM (512 columns): [0,256) accumulates GEMM1 and each 256-wide N-chunk j
+// of GEMM2; [256,512) accumulates GEMM3. MMA issue order per tile i:
+//   G1(i) | G3_3(i-1) | G2_0(i) | G2_1(i) G3_0(i) | G2_2(i) G3_1(i) | G2_3(i) G3_2(i)
+// The epilogue signals "accumulator drained" as soon as its TMEM loads land
+// (packed bf16 values stay in registers) and stores H2_j only after the GEMM3
+// still reading the previous H2 chunk committed, so G2_{j+1} overlaps E2_j and
+// G3_3(i-1) overlaps E1(i).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -40,20 +47,30 @@ using namespace sm100;
 
 constexpr int kM = 128;
 constexpr int kD0 = DS_DISC_D0, kD1 = DS_DISC_D1, kD2 = DS_DISC_D2, kD3 = DS_DISC_D3;
-constexpr int kWTile = 32768;           // 256 rows x 64 bf16, SW128
-constexpr int kWTiles = 48;             // 16 (W1) + 16 (W2) + 16 (W3) per token tile
-constexpr int kAChunk = 16384;          // 128 rows x 64 bf16
-constexpr int kAStages = 4;
-constexpr int kBStages = 3;
+constexpr int kBStage = 16384;          // 256 rows (N) x 32 bf16 (K), SW64
+constexpr int kW1Stages = 24, kWChunkStages = 8;
+constexpr int kBlobStages = kW1Stages + 8 * kWChunkStages;   // W1 | W2_0..3 | W3_0..3 = 88
+constexpr int kAChunk = 16384;          // 128 rows x 64 bf16, SW128
+constexpr int kChunksPerTile = 12;      // K = 768 = 12 x 64
+constexpr int kAStages = 3, kBStages = 3;
 constexpr int kThreads = 448;
-constexpr int kR1 = 0, kR2 = 65536, kBRing = 131072;
-constexpr int kSmemBytes = kBRing + kBStages * kWTile + 1024;   // + alignment slack
+// dynamic shared memory map (base is 1024-aligned; no static __shared__)
+constexpr int kR1 = 0;                          // H1: 4 K-chunks x 16 KB
+constexpr int kR2 = kR1 + 65536;                // H2_j: 4 K-chunks x 16 KB
+constexpr int kARing = kR2 + 65536;
+constexpr int kBRing = kARing + kAStages * kAChunk;
+constexpr int kB1 = kBRing + kBStages * kBStage;   // float b1[256]
+constexpr int kHW = kB1 + 1024;                     // float head_w[256]
+constexpr int kBar = kHW + 1024;                    // mbarriers + misc
+constexpr int kSmemBytes = kBar + 256;
 constexpr uint32_t kIdesc = idesc_bf16_f32(128, 256);
+constexpr float kConst = 16.0f;                     // value of the constant features
+constexpr int kDepth = 4;                           // A-builder prefetch depth (chunks)
+static_assert(kChunksPerTile % kDepth == 0, "slot = chunk % kDepth must be static");
+static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 struct DiscParams {
     float b1[kD1];
-    float b2[kD2];
-    float b3[kD3];
     float hw[kD3];
     float hb;
     int out_logit;
@@ -65,11 +82,10 @@ struct DiscParams {
     long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr = off)
 };
 
-// Trace slots (CTA 0 only): role r, tile t < kTraceTiles, event e < 16.
 constexpr int kTraceTiles = 8;
 #define DS_TRACE(role, tile, ev)                                                          \
     do {                                                                                  \
-        if (P.trace && blockIdx.x == 0 && (tile) < kTraceTiles)                           \
+        if (P.trace && blockIdx.x == 0 && (tile) >= 0 && (tile) < kTraceTiles)            \
             P.trace[((role) * kTraceTiles + (tile)) * 16 + (ev)] = clock64();             \
     } while (0)
 
@@ -78,9 +94,16 @@ __device__ __forceinline__ float gelu_tanh(float x) {
     return 0.5f * x * (1.0f + tanh_approx(u));
 }
 
-// Byte offset of (row, 16-byte chunk) inside a K-major SW128 tile.
+// Byte offset of (row, 16-byte chunk) inside a K-major SW128 tile (128 B rows).
 __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
     return (row >> 3) * 1024u + (row & 7u) * 128u + ((chunk ^ (row & 7u)) << 4);
+}
+
+// K-major SW64 descriptor: 64 B rows (32 bf16), 8-row atoms of 512 B.
+__device__ __forceinline__ uint64_t desc_k_sw64(uint32_t smem_addr) {
+    const uint64_t lo = ((smem_addr >> 4) & 0x3FFFu) | (1u << 16);
+    const uint64_t hi = (512u >> 4) | (1u << 14) | (4u << 29);
+    return lo | (hi << 32);
 }
 
 // 16 pixel bytes -> 16 bf16 (exact: integers < 256 fit the bf16 mantissa).
@@ -91,39 +114,49 @@ __device__ __forceinline__ void u8x16_to_bf16(const uint4 v, uint32_t (&o)[8]) {
         float f[4];
 #pragma unroll
         for (int b = 0; b < 4; ++b)   // 2^23 + byte, exactly; subtract 2^23
-            f[b] = __uint_as_float(__byte_perm(in[q], 0x4B000000u, 0x7650 + b) ) - 8388608.0f;
+            f[b] = __uint_as_float(__byte_perm(in[q], 0x4B000000u, 0x7650 + b)) - 8388608.0f;
         o[2 * q] = pack_bf16x2(f[0], f[1]);
         o[2 * q + 1] = pack_bf16x2(f[2], f[3]);
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant__ DiscParams P) {
-    extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
-    __shared__ uint64_t acc12_full, epi_done, acc3_full, acc3_empty, r1_free;
-    __shared__ uint32_t tmem_base_sh;
-    __shared__ float warp_part[2][8];
+struct Bars {
+    uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
+    uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
+    uint32_t tmem_base;
+    float warp_part[2][8];
+};
+static_assert(sizeof(Bars) <= 256, "barrier block");
 
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+__global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant__ DiscParams P) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    Bars& B = *reinterpret_cast<Bars*>(smem + kBar);
+    float* s_b1 = reinterpret_cast<float*>(smem + kB1);
+    float* s_hw = reinterpret_cast<float*>(smem + kHW);
     const uint32_t sbase = smem_u32(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    if (sbase & 1023u) __trap();   // SW128 operand tiles need 1024-byte alignment
+    if (threadIdx.x < kD1) {
+        s_b1[threadIdx.x] = P.b1[threadIdx.x];
+        s_hw[threadIdx.x] = P.hw[threadIdx.x];
+    }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kAStages; ++s) { mbar_init(&a_full[s], 128); mbar_init(&a_empty[s], 1); }
-        for (int s = 0; s < kBStages; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
-        mbar_init(&acc12_full, 1);
-        mbar_init(&epi_done, 256);
-        mbar_init(&acc3_full, 1);
-        mbar_init(&acc3_empty, 256);
-        mbar_init(&r1_free, 1);
+        for (int s = 0; s < kAStages; ++s) { mbar_init(&B.a_full[s], 128); mbar_init(&B.a_empty[s], 1); }
+        for (int s = 0; s < kBStages; ++s) { mbar_init(&B.b_full[s], 1); mbar_init(&B.b_empty[s], 1); }
+        mbar_init(&B.acc12_full, 1);
+        mbar_init(&B.drained, 256);
+        mbar_init(&B.h2_ready, 256);
+        mbar_init(&B.h2_free, 1);
+        mbar_init(&B.acc3_full, 1);
+        mbar_init(&B.acc3_empty, 256);
         fence_mbar_init();
     }
-    if (warp == 13) tmem_alloc<512>(&tmem_base_sh);
+    if (warp == 13) tmem_alloc<512>(&B.tmem_base);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = tmem_base_sh;
+    const uint32_t tmem = B.tmem_base;
 
     const long long n_img = P.n_img;
     const int tpi = P.tiles_per_img;
@@ -131,65 +164,60 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         blockIdx.x < n_img ? (n_img - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     const long long my_tiles = my_imgs * tpi;
     const long long img_bytes = static_cast<long long>(P.h) * P.w * 3;
+    const long long row_bytes = static_cast<long long>(P.w) * 3;
 
     if (warp < 4) {
-        // ===================== A-builder (128 threads) ======================
-        const int tid = threadIdx.x;
-        // piece r = tid + 128*s: token tl = r/3, 16-byte piece p = r%3 of the
-        // token's 48-byte pixel run in patch row dy (coalesced along px)
-        int tl[3], pp[3];
-#pragma unroll
-        for (int s = 0; s < 3; ++s) {
-            const int r = tid + 128 * s;
-            tl[s] = r / 3;
-            pp[s] = r % 3;
-        }
-        auto src_of = [&](long long tile, int dy, int s) -> const uint8_t* {
+        // ===================== A-builder (128 threads, thread = token) =========
+        const int tl = threadIdx.x;
+        // byte offset of piece q (0..47) of a token's 768-byte patch vector:
+        // patch row dy = q / 3, 16-byte run (q % 3) of that row's 48 bytes
+        auto token_base = [&](long long tile) -> const uint8_t* {
             const long long img = blockIdx.x + (tile / tpi) * gridDim.x;
-            const int tok = static_cast<int>(tile % tpi) * kM + tl[s];
+            const int tok = static_cast<int>(tile % tpi) * kM + tl;
             const int py = tok / P.px, px = tok - py * P.px;
-            return P.images + img * img_bytes +
-                   (static_cast<long long>(py * 16 + dy) * P.w + px * 16) * 3 + pp[s] * 16;
+            return P.images + img * img_bytes + (static_cast<long long>(py) * 16) * row_bytes +
+                   px * 48;
         };
-        const long long total_chunks = my_tiles * 16;
-        constexpr int kDepth = 4;   // chunks of pixel data in flight per thread
-        uint4 buf[kDepth][3];
+        auto piece = [&](const uint8_t* base, int q) -> const uint8_t* {
+            return base + (q / 3) * row_bytes + (q % 3) * 16;
+        };
+        const long long total_chunks = my_tiles * kChunksPerTile;
+        uint4 buf[kDepth][4];
+        const uint8_t* pbase = my_tiles > 0 ? token_base(0) : nullptr;   // tile of chunk g+kDepth
+        long long ptile = 0;
 #pragma unroll
         for (int d = 0; d < kDepth; ++d)
 #pragma unroll
-            for (int s = 0; s < 3; ++s)
-                if (d < total_chunks) buf[d][s] = ld_global_nc_v4(src_of(d / 16, d % 16, s));
+            for (int s = 0; s < 4; ++s)
+                if (d < total_chunks) buf[d][s] = ld_global_nc_v4(piece(pbase, 4 * d + s));
         int astage = 0;
-        uint32_t aphase = 0, r1_phase = 0;
+        uint32_t aphase = 0;
         for (long long g0 = 0; g0 < total_chunks; g0 += kDepth) {
 #pragma unroll
             for (int d = 0; d < kDepth; ++d) {
-                const long long g = g0 + d;     // 16 % kDepth == 0: d == g % kDepth
-                const long long tile = g / 16;
-                const int dy = static_cast<int>(g % 16);
-                if (dy == 0 && tile > 0) {      // R1 still holds the previous tile's H1
-                    mbar_wait(&r1_free, r1_phase);
-                    r1_phase ^= 1;
-                }
-                if (tid == 0 && (dy == 0 || dy == 15)) DS_TRACE(0, tile, dy == 0 ? 0 : 1);
-                mbar_wait(&a_empty[astage], aphase ^ 1);
-                const uint32_t st = sbase + kR1 + astage * kAChunk;
+                const long long g = g0 + d;
+                const int c = static_cast<int>(g % kChunksPerTile);
+                if (tl == 0 && c == 0) DS_TRACE(0, g / kChunksPerTile, 0);
+                mbar_wait(&B.a_empty[astage], aphase ^ 1);
+                const uint32_t st = sbase + kARing + astage * kAChunk;
 #pragma unroll
-                for (int s = 0; s < 3; ++s) {
+                for (int s = 0; s < 4; ++s) {
                     uint32_t o[8];
                     u8x16_to_bf16(buf[d][s], o);
-                    st_shared_v4(st + sw128(tl[s], 2 * pp[s]), o[0], o[1], o[2], o[3]);
-                    st_shared_v4(st + sw128(tl[s], 2 * pp[s] + 1), o[4], o[5], o[6], o[7]);
+                    st_shared_v4(st + sw128(tl, 2 * s), o[0], o[1], o[2], o[3]);
+                    st_shared_v4(st + sw128(tl, 2 * s + 1), o[4], o[5], o[6], o[7]);
                 }
                 fence_proxy_async_smem();
-                mbar_arrive(&a_full[astage]);
-                if (tid == 0 && (dy == 0 || dy == 15)) DS_TRACE(0, tile, dy == 0 ? 2 : 3);
+                mbar_arrive(&B.a_full[astage]);
+                if (tl == 0 && c == kChunksPerTile - 1) DS_TRACE(0, g / kChunksPerTile, 1);
                 if (++astage == kAStages) { astage = 0; aphase ^= 1; }
                 const long long gn = g + kDepth;
                 if (gn < total_chunks) {
+                    const long long tn = gn / kChunksPerTile;
+                    if (tn != ptile) { ptile = tn; pbase = token_base(tn); }
+                    const int cn = static_cast<int>(gn % kChunksPerTile);
 #pragma unroll
-                    for (int s = 0; s < 3; ++s)
-                        buf[d][s] = ld_global_nc_v4(src_of(gn / 16, static_cast<int>(gn % 16), s));
+                    for (int s = 0; s < 4; ++s) buf[d][s] = ld_global_nc_v4(piece(pbase, 4 * cn + s));
                 }
             }
         }
@@ -200,59 +228,16 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         const int half = ew >> 2;          // column half [128*half, 128*half+128)
         const uint32_t row = 32 * q + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
-        uint32_t p12 = 0, p3 = 0;
+        uint32_t p12 = 0, p3 = 0, pfree = 0;
         float img_acc = 0.0f;
-        for (long long tile = 0; tile < my_tiles; ++tile) {
-            // E1 (j = -1) and E2_j (j = 0..3): acc[0,256) -> H1 / H2
-            for (int j = -1; j < 4; ++j) {
-                mbar_wait(&acc12_full, p12);
-                p12 ^= 1;
-                tc_fence_after();
-                if (ew == 0 && lane == 0) DS_TRACE(1, tile, 2 * (j + 1));
-                const uint32_t hbase = sbase + (j < 0 ? kR1 : kR2);
-#pragma unroll 1
-                for (int cb = 0; cb < 4; cb += 2) {
-                    uint32_t v0[32], v1[32];
-                    const int c0 = 128 * half + 32 * cb;
-                    tmem_ld2_x32_sync(tmem + lane_addr + c0, tmem + lane_addr + c0 + 32, v0, v1);
-#pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const uint32_t* v = hh ? v1 : v0;
-                        const int cbase = c0 + 32 * hh;
-#pragma unroll
-                        for (int e = 0; e < 32; e += 8) {
-                            uint32_t pk[4];
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const int c = cbase + e + 2 * u;
-                                float a = __uint_as_float(v[e + 2 * u]);
-                                float b = __uint_as_float(v[e + 2 * u + 1]);
-                                if (j < 0) {
-                                    a = gelu_tanh(a + P.b1[c]);
-                                    b = gelu_tanh(b + P.b1[c + 1]);
-                                } else {
-                                    a = fmaxf(a + P.b2[256 * j + c], 0.0f);
-                                    b = fmaxf(b + P.b2[256 * j + c + 1], 0.0f);
-                                }
-                                pk[u] = pack_bf16x2(a, b);
-                            }
-                            const int f = cbase + e;   // feature within this 256-wide block
-                            const uint32_t addr = hbase + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3);
-                            st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);
-                        }
-                    }
-                }
-                fence_proxy_async_smem();
-                tc_fence_before();
-                mbar_arrive(&epi_done);
-                if (ew == 0 && lane == 0) DS_TRACE(1, tile, 2 * (j + 1) + 1);
-            }
-            // E3: acc3 -> ReLU(+b3) . w_head, summed over this thread's columns
-            mbar_wait(&acc3_full, p3);
+
+        // E3: ReLU(acc3) . w_head over this thread's 128 columns -> per-image mean
+        auto e3 = [&](long long tile) {
+            mbar_wait(&B.acc3_full, p3);
             p3 ^= 1;
             tc_fence_after();
-            if (ew == 0 && lane == 0) DS_TRACE(1, tile, 10);
-            float part = 0.0f;
+            DS_TRACE(1, tile, 10);
+            float part[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
             for (int cb = 0; cb < 4; cb += 2) {
                 uint32_t v0[32], v1[32];
@@ -260,26 +245,25 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 tmem_ld2_x32_sync(tmem + lane_addr + 256 + c0, tmem + lane_addr + 256 + c0 + 32,
                                   v0, v1);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    part += fmaxf(__uint_as_float(v0[e]) + P.b3[c0 + e], 0.0f) * P.hw[c0 + e];
-                }
+                for (int e = 0; e < 32; ++e)
+                    part[e & 3] += fmaxf(__uint_as_float(v0[e]), 0.0f) * s_hw[c0 + e];
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    part += fmaxf(__uint_as_float(v1[e]) + P.b3[c0 + 32 + e], 0.0f) * P.hw[c0 + 32 + e];
-                }
+                for (int e = 0; e < 32; ++e)
+                    part[e & 3] += fmaxf(__uint_as_float(v1[e]), 0.0f) * s_hw[c0 + 32 + e];
             }
             tc_fence_before();
-            mbar_arrive(&acc3_empty);
-            if (ew == 0 && lane == 0) DS_TRACE(1, tile, 11);
+            mbar_arrive(&B.acc3_empty);
+            DS_TRACE(1, tile, 11);
+            float p = (part[0] + part[1]) + (part[2] + part[3]);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
             const int buf = static_cast<int>(tile & 1);
-            if (lane == 0) warp_part[buf][ew] = part;
+            if (lane == 0) B.warp_part[buf][ew] = p;
             named_bar_sync(1, 256);
             if (ew == 0 && lane == 0) {
                 float s = 0.0f;
 #pragma unroll
-                for (int w = 0; w < 8; ++w) s += warp_part[buf][w];
+                for (int w = 0; w < 8; ++w) s += B.warp_part[buf][w];
                 img_acc += s;
                 if (tile % tpi == tpi - 1) {
                     const long long img = blockIdx.x + (tile / tpi) * gridDim.x;
@@ -288,92 +272,189 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     img_acc = 0.0f;
                 }
             }
+        };
+
+        for (long long tile = 0; tile < my_tiles; ++tile) {
+            // ---- E1: acc[0,256) + b1 -> GELU -> bf16 -> H1 (R1) ----------------
+            mbar_wait(&B.acc12_full, p12);
+            p12 ^= 1;
+            tc_fence_after();
+            DS_TRACE(1, tile, 0);
+#pragma unroll 1
+            for (int cb = 0; cb < 4; cb += 2) {
+                uint32_t v0[32], v1[32];
+                const int c0 = 128 * half + 32 * cb;
+                tmem_ld2_x32_sync(tmem + lane_addr + c0, tmem + lane_addr + c0 + 32, v0, v1);
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint32_t* v = hh ? v1 : v0;
+                    const int cbase = c0 + 32 * hh;
+#pragma unroll
+                    for (int e = 0; e < 32; e += 8) {
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int c = cbase + e + 2 * u;
+                            pk[u] = pack_bf16x2(gelu_tanh(__uint_as_float(v[e + 2 * u]) + s_b1[c]),
+                                                gelu_tanh(__uint_as_float(v[e + 2 * u + 1]) + s_b1[c + 1]));
+                        }
+                        const int f = cbase + e;
+                        st_shared_v4(sbase + kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
+                                     pk[0], pk[1], pk[2], pk[3]);
+                    }
+                }
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(&B.drained);
+            DS_TRACE(1, tile, 1);
+
+            // ---- E3 of the previous tile (its G3_3 was issued after G1(tile)) ----
+            if (tile > 0) e3(tile - 1);
+
+            // ---- E2_j: acc[0,256) -> ReLU -> bf16 (registers) -> H2 (R2) --------
+            for (int j = 0; j < 4; ++j) {
+                mbar_wait(&B.acc12_full, p12);
+                p12 ^= 1;
+                tc_fence_after();
+                DS_TRACE(1, tile, 2 + 2 * j);
+                uint32_t pk[64];
+#pragma unroll
+                for (int cb = 0; cb < 4; ++cb) {
+                    uint32_t v[32];
+                    const int c0 = 128 * half + 32 * cb;
+                    tmem_ld_x32_sync(tmem + lane_addr + c0, v);
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        pk[16 * cb + e] = pack_bf16x2(fmaxf(__uint_as_float(v[2 * e]), 0.0f),
+                                                      fmaxf(__uint_as_float(v[2 * e + 1]), 0.0f));
+                }
+                tc_fence_before();
+                mbar_arrive(&B.drained);            // MMA may overwrite acc[0,256) now
+                if (tile > 0 || j > 0) {            // GEMM3 reading the previous H2 chunk done
+                    mbar_wait(&B.h2_free, pfree);
+                    pfree ^= 1;
+                }
+#pragma unroll
+                for (int cb = 0; cb < 4; ++cb) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int f = 128 * half + 32 * cb + 8 * e;
+                        st_shared_v4(sbase + kR2 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
+                                     pk[16 * cb + 4 * e], pk[16 * cb + 4 * e + 1],
+                                     pk[16 * cb + 4 * e + 2], pk[16 * cb + 4 * e + 3]);
+                    }
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&B.h2_ready);
+                DS_TRACE(1, tile, 3 + 2 * j);
+            }
         }
+        if (my_tiles > 0) e3(my_tiles - 1);
     } else if (warp == 12) {
         // ===================== weight producer ==============================
         if (lane == 0) {
             const uint64_t policy = policy_evict_last();
             int bs = 0;
             uint32_t bp = 0;
-            for (long long tile = 0; tile < my_tiles; ++tile) {
-                for (int t = 0; t < kWTiles; ++t) {
-                    mbar_wait(&b_empty[bs], bp ^ 1);
-                    mbar_arrive_expect_tx(&b_full[bs], kWTile);
-                    bulk_g2s_hint(smem + kBRing + bs * kWTile, P.wblob + static_cast<size_t>(t) * kWTile,
-                                  kWTile, &b_full[bs], policy);
+            auto put = [&](int first, int count) {
+                for (int t = first; t < first + count; ++t) {
+                    mbar_wait(&B.b_empty[bs], bp ^ 1);
+                    mbar_arrive_expect_tx(&B.b_full[bs], kBStage);
+                    bulk_g2s_hint(smem + kBRing + bs * kBStage,
+                                  P.wblob + static_cast<size_t>(t) * kBStage, kBStage,
+                                  &B.b_full[bs], policy);
                     if (++bs == kBStages) { bs = 0; bp ^= 1; }
                 }
+            };
+            const int W1 = 0, W2 = kW1Stages, W3 = kW1Stages + 4 * kWChunkStages;
+            for (long long tile = 0; tile < my_tiles; ++tile) {
+                put(W1, kW1Stages);
+                if (tile > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
+                put(W2, kWChunkStages);
+                for (int j = 1; j < 4; ++j) {
+                    put(W2 + j * kWChunkStages, kWChunkStages);
+                    put(W3 + (j - 1) * kWChunkStages, kWChunkStages);
+                }
             }
+            if (my_tiles > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
         }
     } else {
         // ===================== MMA issuer (warp 13, one thread) ==============
         if (lane == 0) {
             int as = 0, bs = 0;
-            uint32_t ap = 0, bp = 0, ep = 0, e3p = 0;
+            uint32_t ap = 0, bp = 0, pdr = 0, prd = 0, pe3 = 0;
             const uint32_t acc12 = tmem, acc3 = tmem + 256;
-            auto wait_b = [&]() {
-                mbar_wait(&b_full[bs], bp);
-                tc_fence_after();
-            };
-            auto release_b = [&]() {
-                umma_commit(&b_empty[bs]);
-                if (++bs == kBStages) { bs = 0; bp ^= 1; }
-            };
-            // K = 256 GEMM from an H region (4 chunks of 64) into `acc`.
-            auto gemm_h = [&](uint32_t hregion, uint32_t acc, bool acc_in) {
-                for (int kc = 0; kc < 4; ++kc) {
-                    wait_b();
-                    const uint64_t ad = desc_k_sw128(sbase + hregion + kc * kAChunk);
-                    const uint64_t bd = desc_k_sw128(sbase + kBRing + bs * kWTile);
+            // K = 64 x nk from an SW128 A region (nk chunks of 16 KB) against
+            // 2*nk weight stages (K = 32 each).
+            auto gemm = [&](uint32_t a_region, int nk, uint32_t acc, bool acc_in) {
+                for (int kc = 0; kc < nk; ++kc) {
+                    const uint64_t ad = desc_k_sw128(a_region + kc * kAChunk);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        umma_bf16(acc, ad + 2 * k, bd + 2 * k, kIdesc,
-                                  (acc_in || kc > 0 || k > 0) ? 1u : 0u);
-                    release_b();
+                    for (int hf = 0; hf < 2; ++hf) {
+                        mbar_wait(&B.b_full[bs], bp);
+                        tc_fence_after();
+                        const uint64_t bd = desc_k_sw64(sbase + kBRing + bs * kBStage);
+#pragma unroll
+                        for (int k = 0; k < 2; ++k)
+                            umma_bf16(acc, ad + 2 * (2 * hf + k), bd + 2 * k, kIdesc,
+                                      (acc_in || kc > 0 || hf > 0 || k > 0) ? 1u : 0u);
+                        umma_commit(&B.b_empty[bs]);
+                        if (++bs == kBStages) { bs = 0; bp ^= 1; }
+                    }
                 }
+            };
+            auto wait_bar = [&](uint64_t* bar, uint32_t& ph) {
+                mbar_wait(bar, ph);
+                ph ^= 1;
+                tc_fence_after();
             };
             for (long long tile = 0; tile < my_tiles; ++tile) {
                 DS_TRACE(2, tile, 0);
-                // GEMM1: 16 chunks (patch rows), K = 48 each
-                for (int c = 0; c < 16; ++c) {
-                    mbar_wait(&a_full[as], ap);
-                    wait_b();
-                    const uint64_t ad = desc_k_sw128(sbase + kR1 + as * kAChunk);
-                    const uint64_t bd = desc_k_sw128(sbase + kBRing + bs * kWTile);
-#pragma unroll
-                    for (int k = 0; k < 3; ++k)
-                        umma_bf16(acc12, ad + 2 * k, bd + 2 * k, kIdesc, (c > 0 || k > 0) ? 1u : 0u);
-                    umma_commit(&a_empty[as]);
-                    if (++as == kAStages) { as = 0; ap ^= 1; }
-                    release_b();
-                }
-                umma_commit(&acc12_full);
-                DS_TRACE(2, tile, 1);
-                for (int j = 0; j < 4; ++j) {
-                    mbar_wait(&epi_done, ep);     // E1 (j=0) or E2_{j-1}: acc drained, H written
-                    ep ^= 1;
+                // G1: 12 A chunks from the ring
+                for (int c = 0; c < kChunksPerTile; ++c) {
+                    mbar_wait(&B.a_full[as], ap);
                     tc_fence_after();
-                    DS_TRACE(2, tile, 2 + 2 * j);
-                    if (j > 0) {
-                        if (j == 1) {             // acc3 drained by the previous tile's E3
-                            mbar_wait(&acc3_empty, e3p ^ 1);
-                            e3p ^= 1;
-                            tc_fence_after();
-                        }
-                        gemm_h(kR2, acc3, j > 1);            // GEMM3, K-chunk j-1
-                    }
-                    gemm_h(kR1, acc12, false);               // GEMM2, N-chunk j
-                    umma_commit(&acc12_full);
-                    DS_TRACE(2, tile, 3 + 2 * j);
-                    if (j == 3) umma_commit(&r1_free);       // H1 no longer read
+                    gemm(sbase + kARing + as * kAChunk, 1, acc12, c > 0);
+                    umma_commit(&B.a_empty[as]);
+                    if (++as == kAStages) { as = 0; ap ^= 1; }
                 }
-                mbar_wait(&epi_done, ep);                    // E2_3
-                ep ^= 1;
-                tc_fence_after();
+                umma_commit(&B.acc12_full);
+                DS_TRACE(2, tile, 1);
+                if (tile > 0) {                      // G3_3 of the previous tile
+                    wait_bar(&B.h2_ready, prd);
+                    gemm(sbase + kR2, 4, acc3, true);
+                    umma_commit(&B.h2_free);
+                    umma_commit(&B.acc3_full);
+                }
+                DS_TRACE(2, tile, 2);
+                wait_bar(&B.drained, pdr);           // E1: acc drained, H1 stored
+                DS_TRACE(2, tile, 3);
+                gemm(sbase + kR1, 4, acc12, false);  // G2_0
+                umma_commit(&B.acc12_full);
+                for (int j = 1; j < 4; ++j) {
+                    wait_bar(&B.drained, pdr);       // E2_{j-1} has the values in registers
+                    DS_TRACE(2, tile, 2 + 2 * j);
+                    gemm(sbase + kR1, 4, acc12, false);          // G2_j
+                    umma_commit(&B.acc12_full);
+                    wait_bar(&B.h2_ready, prd);      // H2_{j-1} stored
+                    DS_TRACE(2, tile, 3 + 2 * j);
+                    if (j == 1) {                    // acc3 drained by E3 of the previous tile
+                        mbar_wait(&B.acc3_empty, pe3 ^ 1);
+                        pe3 ^= 1;
+                        tc_fence_after();
+                    }
+                    gemm(sbase + kR2, 4, acc3, j > 1);           // G3_{j-1}
+                    umma_commit(&B.h2_free);
+                }
+                wait_bar(&B.drained, pdr);           // E2_3 drained: acc[0,256) free
                 DS_TRACE(2, tile, 10);
-                gemm_h(kR2, acc3, true);                     // GEMM3, K-chunk 3
-                umma_commit(&acc3_full);
-                DS_TRACE(2, tile, 11);
+            }
+            if (my_tiles > 0) {
+                wait_bar(&B.h2_ready, prd);
+                gemm(sbase + kR2, 4, acc3, true);    // G3_3 of the last tile
+                umma_commit(&B.h2_free);
+                umma_commit(&B.acc3_full);
             }
         }
     }
@@ -407,7 +488,8 @@ __device__ __forceinline__ float bf_bits2f(uint16_t b) {
     return __uint_as_float(static_cast<uint32_t>(b) << 16);
 }
 
-// Logical weights (row = input feature), bf16 bit patterns.
+// Logical weights (row = input feature), bf16 bit patterns, including the
+// constant-feature bias rows (see the header comment).
 __global__ void gen_weights_kernel(uint64_t seed, uint16_t* w1, uint16_t* w2, uint16_t* w3) {
     const float s1 = 1.7320508f / (64.0f * sqrtf(768.0f));   // U(-a,a): std = a/sqrt(3)
     const float s2 = 1.7320508f * sqrtf(2.0f / 256.0f);
@@ -415,50 +497,61 @@ __global__ void gen_weights_kernel(uint64_t seed, uint16_t* w1, uint16_t* w2, ui
     const int n1 = kD0 * kD1, n2 = kD1 * kD2, n3 = kD2 * kD3;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n1 + n2 + n3;
          i += gridDim.x * blockDim.x) {
-        if (i < n1) w1[i] = f2bf_bits(s1 * unif_pm1(seed ^ 0x1111, i));
-        else if (i < n1 + n2) w2[i - n1] = f2bf_bits(s2 * unif_pm1(seed ^ 0x2222, i - n1));
-        else w3[i - n1 - n2] = f2bf_bits(s3 * unif_pm1(seed ^ 0x3333, i - n1 - n2));
+        if (i < n1) {
+            const int n = i % kD1;
+            w1[i] = n == kD1 - 1 ? 0 : f2bf_bits(s1 * unif_pm1(seed ^ 0x1111, i));
+        } else if (i < n1 + n2) {
+            const int e = i - n1, k = e / kD2, n = e % kD2;
+            float v;
+            if (n == kD2 - 1) v = k == kD1 - 1 ? 1.0f : 0.0f;          // h2[:,1023] = 16
+            else if (k == kD1 - 1) v = 0.05f * unif_pm1(seed ^ 0x5555, n) / kConst;  // b2 / 16
+            else v = s2 * unif_pm1(seed ^ 0x2222, e);
+            w2[e] = f2bf_bits(v);
+        } else {
+            const int e = i - n1 - n2, k = e / kD3, n = e % kD3;
+            const float v = k == kD2 - 1 ? 0.05f * unif_pm1(seed ^ 0x6666, n) / kConst   // b3 / 16
+                                         : s3 * unif_pm1(seed ^ 0x3333, e);
+            w3[e] = f2bf_bits(v);
+        }
     }
 }
 
-// Pre-swizzled blob in the MMA consumption order (see disc_kernel): for each
-// 32 KB tile, element (n, kl) of a 256 x 64 K-major SW128 tile.
+// Pre-swizzled blob of 16 KB stages (256 rows = N x 32 K, SW64):
+//   stages  0..23 : W1, K-range [32s, 32s+32)
+//   stages 24..55 : W2 N-chunk j (rows 256j..), K-range [32k, 32k+32), j-major
+//   stages 56..87 : W3 K-chunk j (input rows 256j + 32k ..), all 256 outputs
 __global__ void tile_weights_kernel(const uint16_t* w1, const uint16_t* w2, const uint16_t* w3,
                                     uint16_t* blob) {
-    const int t = blockIdx.x;          // 0..47
-    int type, j, kc;                   // type 0: W1 chunk j(=dy); 1: W2 (j, kc); 2: W3 (j, kc)
-    if (t < 16) { type = 0; j = t; kc = 0; }
-    else {
-        // per j: [W3(j-1) x4 if j>0], W2(j) x4; then W3(3) x4
-        const int u = t - 16;          // 0..31
-        if (u < 4) { type = 1; j = 0; kc = u; }
-        else if (u < 28) {
-            const int v = u - 4, jj = 1 + v / 8, r = v % 8;
-            if (r < 4) { type = 2; j = jj - 1; kc = r; } else { type = 1; j = jj; kc = r - 4; }
-        } else { type = 2; j = 3; kc = u - 28; }
-    }
-    uint16_t* out = blob + static_cast<size_t>(t) * (kWTile / 2);
-    for (int e = threadIdx.x; e < 256 * 64; e += blockDim.x) {
-        const int n = e / 64, kl = e % 64;
-        uint16_t v = 0;
-        if (type == 0) {
-            if (kl < 48) v = w1[(48 * j + kl) * kD1 + n];
-        } else if (type == 1) {
-            v = w2[(64 * kc + kl) * kD2 + 256 * j + n];
+    const int t = blockIdx.x;
+    uint16_t* out = blob + static_cast<size_t>(t) * (kBStage / 2);
+    for (int e = threadIdx.x; e < 256 * 32; e += blockDim.x) {
+        const int n = e / 32, kl = e % 32;
+        uint16_t v;
+        if (t < kW1Stages) {
+            v = w1[(32 * t + kl) * kD1 + n];
+        } else if (t < kW1Stages + 4 * kWChunkStages) {
+            const int u = t - kW1Stages, j = u / kWChunkStages, k = u % kWChunkStages;
+            v = w2[(32 * k + kl) * kD2 + 256 * j + n];
         } else {
-            v = w3[(256 * j + 64 * kc + kl) * kD3 + n];
+            const int u = t - kW1Stages - 4 * kWChunkStages, j = u / kWChunkStages,
+                      k = u % kWChunkStages;
+            v = w3[(256 * j + 32 * k + kl) * kD3 + n];
         }
-        const uint32_t byte = (n >> 3) * 1024u + (n & 7) * 128u + ((((kl >> 3) ^ (n & 7))) << 4) +
-                              (kl & 7) * 2u;
+        const uint32_t byte = (n >> 3) * 512u + (n & 7) * 64u +
+                              ((((kl >> 3) ^ ((n >> 1) & 3))) << 4) + (kl & 7) * 2u;
         out[byte / 2] = v;
     }
 }
 
-// b1[n] = -128 * sum_k W1[k][n] + small bias: folds the (x - 128) / 64 input
-// normalisation into layer 1 (the 1/64 is in W1's scale).
+// b1[n] = -128 * sum_k W1[k][n] + small bias (folds (x - 128)/64 into layer 1;
+// the 1/64 is in W1's scale); b1[255] = 16 makes h1[:,255] the constant feature.
 __global__ void fold_bias_kernel(const uint16_t* w1, uint64_t seed, float* b1) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= kD1) return;
+    if (n == kD1 - 1) {
+        b1[n] = kConst;
+        return;
+    }
     float s = 0.0f;
     for (int k = 0; k < kD0; ++k) s += bf_bits2f(w1[k * kD1 + n]);
     b1[n] = -128.0f * s + 0.05f * unif_pm1(seed ^ 0x4444, n);
@@ -472,7 +565,7 @@ struct ds_disc {
     uint16_t* d_w = nullptr;   // w1 | w2 | w3 logical
     uint8_t* d_blob = nullptr;
     float* d_b1 = nullptr;
-    DiscParams params{};       // biases + head (device-independent part)
+    DiscParams params{};       // b1 + head (device-independent part)
 };
 
 namespace {
@@ -533,7 +626,7 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
     };
     cudaError_t e;
     if ((e = cudaMalloc(&d->d_w, nw * 2)) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "malloc w"));
-    if ((e = cudaMalloc(&d->d_blob, static_cast<size_t>(kWTiles) * kWTile)) != cudaSuccess)
+    if ((e = cudaMalloc(&d->d_blob, static_cast<size_t>(kBlobStages) * kBStage)) != cudaSuccess)
         return cleanup(dsi::cuda_fail(e, "malloc blob"));
     if ((e = cudaMalloc(&d->d_b1, kD1 * sizeof(float))) != cudaSuccess)
         return cleanup(dsi::cuda_fail(e, "malloc b1"));
@@ -541,7 +634,7 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
     uint16_t* w2 = w1 + kD0 * kD1;
     uint16_t* w3 = w2 + kD1 * kD2;
     gen_weights_kernel<<<148 * 4, 256, 0, st>>>(weight_seed, w1, w2, w3);
-    tile_weights_kernel<<<kWTiles, 256, 0, st>>>(w1, w2, w3, reinterpret_cast<uint16_t*>(d->d_blob));
+    tile_weights_kernel<<<kBlobStages, 256, 0, st>>>(w1, w2, w3, reinterpret_cast<uint16_t*>(d->d_blob));
     fold_bias_kernel<<<1, 256, 0, st>>>(w1, weight_seed, d->d_b1);
     ctx->launches.fetch_add(3);
     if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "weight init"));
@@ -549,8 +642,6 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
                              st)) != cudaSuccess)
         return cleanup(dsi::cuda_fail(e, "copy b1"));
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "sync"));
-    for (int i = 0; i < kD2; ++i) d->params.b2[i] = 0.05f * unif_pm1(weight_seed ^ 0x5555, i);
-    for (int i = 0; i < kD3; ++i) d->params.b3[i] = 0.05f * unif_pm1(weight_seed ^ 0x6666, i);
     for (int i = 0; i < kD3; ++i) d->params.hw[i] = unif_pm1(weight_seed ^ 0x7777, i) / 16.0f;
     d->params.hb = 0.0f;
 
@@ -599,6 +690,7 @@ extern "C" ds_status ds_disc_destroy(ds_disc* d) {
     return DS_OK;
 }
 
+// b2/b3 are carried inside W2/W3 (constant features), so they export as zeros.
 extern "C" ds_status ds_disc_export(const ds_disc* d, uint16_t* w1, uint16_t* w2, uint16_t* w3,
                                     float* b1, float* b2, float* b3, float* head_w, float* head_b) {
     if (!d) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null disc");
@@ -609,8 +701,8 @@ extern "C" ds_status ds_disc_export(const ds_disc* d, uint16_t* w1, uint16_t* w2
     if (w2) DS_CUDA_TRY(cudaMemcpy(w2, d2, sizeof(uint16_t) * kD1 * kD2, cudaMemcpyDeviceToHost));
     if (w3) DS_CUDA_TRY(cudaMemcpy(w3, d3, sizeof(uint16_t) * kD2 * kD3, cudaMemcpyDeviceToHost));
     if (b1) std::memcpy(b1, d->params.b1, sizeof(d->params.b1));
-    if (b2) std::memcpy(b2, d->params.b2, sizeof(d->params.b2));
-    if (b3) std::memcpy(b3, d->params.b3, sizeof(d->params.b3));
+    if (b2) std::memset(b2, 0, sizeof(float) * kD2);
+    if (b3) std::memset(b3, 0, sizeof(float) * kD3);
     if (head_w) std::memcpy(head_w, d->params.hw, sizeof(d->params.hw));
     if (head_b) *head_b = d->params.hb;
     return DS_OK;

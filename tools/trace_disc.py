@@ -35,11 +35,11 @@ def main():
     ctx.synchronize()
     t = tr.cpu().numpy().reshape(3, 8, 16)
     base = t[2, 0, 0]
-    names = {0: ["r1_free", "c0_done?", "c0_stored", "c15_stored"],
+    names = {0: ["c0_start", "c11_stored"],
              1: ["E1_rdy", "E1_done", "E20_rdy", "E20_done", "E21_rdy", "E21_done", "E22_rdy",
                  "E22_done", "E23_rdy", "E23_done", "E3_rdy", "E3_done"],
-             2: ["start", "G1_iss", "ep0", "G20_iss", "ep1", "G21_iss", "ep2", "G22_iss", "ep3",
-                 "G23_iss", "ep4", "G33_iss"]}
+             2: ["start", "G1_iss", "G33prev_iss", "E1_seen", "dr0", "rd0", "dr1", "rd1", "dr2",
+                 "rd2", "dr3"]}
     for tile in range(8):
         print(f"--- tile {tile}")
         for role in (2, 1, 0):
