@@ -22,18 +22,25 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads)
 curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int64_t n,
                      double decay, int* __restrict__ bad) {
-    __shared__ unsigned char bins[kChunk];
+    __shared__ __align__(16) unsigned char bins[kChunk];
+    __shared__ int chunk_bad;
     const int tid = threadIdx.x;
     double m = 0.0;
     if (tid < DS_CURVE_BINS) m = curve->bin_mass[tid];
     else if (tid == DS_CURVE_BINS) m = curve->total_mass;
     const bool scale = decay != 1.0;
+    // the total-mass thread matches every observation; bin threads their own bin
+    const unsigned mine = tid < DS_CURVE_BINS ? static_cast<unsigned>(tid) : 0xFFu;
+    const bool is_total = tid == DS_CURVE_BINS;
     for (int64_t base = 0; base < n; base += kChunk) {
         const int cnt = static_cast<int>(n - base < kChunk ? n - base : kChunk);
+        if (tid == 0) chunk_bad = 0;
+        __syncthreads();
         for (int k = tid; k < cnt; k += kThreads) {
             const double c = static_cast<double>(conf[base + k]);
             if (!(c >= 0.0) || !(c <= 1.0)) {
                 atomicMin(bad, static_cast<int>(base + k < 0x7fffffff ? base + k : 0x7fffffff));
+                chunk_bad = 1;
                 bins[k] = 255;
                 continue;
             }
@@ -42,19 +49,34 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
             b = b < 0 ? 0 : (b > DS_CURVE_BINS - 1 ? DS_CURVE_BINS - 1 : b);
             bins[k] = static_cast<unsigned char>(b);
         }
+        for (int k = cnt + tid; k < ((cnt + 7) & ~7); k += kThreads) bins[k] = 254;  // pad
         __syncthreads();
         if (tid <= DS_CURVE_BINS) {
-            const unsigned char mine = static_cast<unsigned char>(tid);
-            const bool is_total = tid == DS_CURVE_BINS;
-            for (int k = 0; k < cnt; ++k) {
-                const unsigned char b = bins[k];
-                if (b == 255) break;   // the reference throws here; state stops
-                if (scale) m = __dmul_rn(m, decay);
-                if (is_total || b == mine) m = __dadd_rn(m, 1.0);
+            if (!chunk_bad) {
+                // replay, 8 observations per 64-bit shared load; the hit add is
+                // predicated (a miss must leave m untouched, including -0.0)
+                for (int k = 0; k < cnt; k += 8) {
+                    const uint2 w = *reinterpret_cast<const uint2*>(&bins[k]);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const unsigned b = ((u < 4 ? w.x : w.y) >> (8 * (u & 3))) & 0xFFu;
+                        if (b == 254u) break;           // padding past the last observation
+                        if (scale) m = __dmul_rn(m, decay);
+                        const double a = __dadd_rn(m, 1.0);
+                        m = (is_total || b == mine) ? a : m;
+                    }
+                }
+            } else {
+                for (int k = 0; k < cnt; ++k) {
+                    const unsigned char b = bins[k];
+                    if (b == 255) break;   // the reference throws here; state stops
+                    if (scale) m = __dmul_rn(m, decay);
+                    if (is_total || b == mine) m = __dadd_rn(m, 1.0);
+                }
             }
         }
         __syncthreads();
-        if (*bad != 0x7fffffff) break;
+        if (chunk_bad) break;
     }
     if (tid < DS_CURVE_BINS) curve->bin_mass[tid] = m;
     else if (tid == DS_CURVE_BINS) curve->total_mass = m;

@@ -17,12 +17,13 @@
 // One CTA per SM, persistent over whole images, M = 128 tokens per tile.
 //   warps 0-3   A-builder: 128-bit loads of 16 B pixel runs (thread = token,
 //               prefetched kDepth chunks ahead), u8 -> bf16 (exact), SW128
-//               stores into its own 3-stage ring (12 chunks of K=64 per tile)
+//               stores into its own 2-stage ring (12 chunks of K=64 per tile);
+//               one thread bulk-prefetches the NEXT tile's pixel rows into L2
 //   warps 4-11  epilogue: tcgen05.ld of the TMEM accumulators, activation,
 //               bf16 pack, SW128 stores of H1/H2 (next GEMM's A operand), and
 //               the head dot product + per-image mean
 //   warp 12     weight producer: 1-D bulk TMA of pre-swizzled 16 KB weight
-//               stages (256 x K=32, SW64; L2 evict-last) into a 3-stage ring
+//               stages (256 x K=32, SW64; L2 evict-last) into a 4-stage ring
 //   warp 13     TMEM allocator + the single thread issuing tcgen05.mma
 // TMEM (512 columns): [0,256) accumulates GEMM1 and each 256-wide N-chunk j
 // of GEMM2; [256,512) accumulates GEMM3. MMA issue order per tile i:
@@ -52,7 +53,7 @@ constexpr int kW1Stages = 24, kWChunkStages = 8;
 constexpr int kBlobStages = kW1Stages + 8 * kWChunkStages;   // W1 | W2_0..3 | W3_0..3 = 88
 constexpr int kAChunk = 16384;          // 128 rows x 64 bf16, SW128
 constexpr int kChunksPerTile = 12;      // K = 768 = 12 x 64
-constexpr int kAStages = 3, kBStages = 3;
+constexpr int kAStages = 2, kBStages = 4;
 constexpr int kThreads = 448;
 // dynamic shared memory map (base is 1024-aligned; no static __shared__)
 constexpr int kR1 = 0;                          // H1: 4 K-chunks x 16 KB
@@ -181,7 +182,24 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         auto piece = [&](const uint8_t* base, int q) -> const uint8_t* {
             return base + (q / 3) * row_bytes + (q % 3) * 16;
         };
+        // The pixels of a tile are one contiguous byte range (whole patch rows
+        // when px divides 128 or 128 divides px; otherwise a small superset).
+        auto prefetch_tile = [&](long long tile) {
+            const long long img = blockIdx.x + (tile / tpi) * gridDim.x;
+            const int tok0 = static_cast<int>(tile % tpi) * kM;
+            const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
+            const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
+            long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
+            for (long long off = 0; off < bytes; off += 65536) {
+                const uint32_t n = static_cast<uint32_t>(bytes - off < 65536 ? bytes - off : 65536);
+                bulk_prefetch_l2(p0 + off, n);
+            }
+        };
         const long long total_chunks = my_tiles * kChunksPerTile;
+        if (tl == 0) {
+            if (my_tiles > 0) prefetch_tile(0);
+            if (my_tiles > 1) prefetch_tile(1);
+        }
         uint4 buf[kDepth][4];
         const uint8_t* pbase = my_tiles > 0 ? token_base(0) : nullptr;   // tile of chunk g+kDepth
         long long ptile = 0;
@@ -197,7 +215,10 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             for (int d = 0; d < kDepth; ++d) {
                 const long long g = g0 + d;
                 const int c = static_cast<int>(g % kChunksPerTile);
-                if (tl == 0 && c == 0) DS_TRACE(0, g / kChunksPerTile, 0);
+                if (tl == 0 && c == 0) {
+                    DS_TRACE(0, g / kChunksPerTile, 0);
+                    if (g / kChunksPerTile + 2 < my_tiles) prefetch_tile(g / kChunksPerTile + 2);
+                }
                 mbar_wait(&B.a_empty[astage], aphase ^ 1);
                 const uint32_t st = sbase + kARing + astage * kAChunk;
 #pragma unroll

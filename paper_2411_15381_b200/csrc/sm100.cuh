@@ -67,6 +67,12 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gm
         : "memory");
 }
 
+// Bulk prefetch of a global byte range into L2 (no smem, no completion).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
