@@ -79,3 +79,61 @@ def disc_forward(images: np.ndarray, wts: dict, logits: bool = False) -> np.ndar
         lg = np.float32(s.mean(dtype=np.float64)) + np.float32(wts["head_b"])
         out[i] = lg if logits else 1.0 / (1.0 + np.exp(-np.float64(lg)))
     return out
+
+
+# ---- host restatement of the deterministic weights (disc.cu gen_weights_kernel,
+# fold_bias_kernel and ds_disc_create's head) -------------------------------------
+
+def _unif_pm1(stream: int, idx: np.ndarray) -> np.ndarray:
+    """disc.cu unif_pm1: (splitmix64(stream ^ splitmix64(idx)) >> 11) * 2^-52 - 1, as f32."""
+    with np.errstate(over="ignore"):
+        r = _splitmix64(np.uint64(stream) ^ _splitmix64(idx.astype(np.uint64)))
+    return ((r >> np.uint64(11)).astype(np.float64) * 2.0 ** -52 - 1.0).astype(np.float32)
+
+
+def _to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    return (round_bf16(x).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+
+
+def gen_weights(seed: int, calibrate: bool = True) -> dict:
+    """The PatchDisc weights ds_disc_create(seed) builds, restated on the host.
+    W1/W2/W3 bits and b1 are bit-identical to the device; the head is
+    calibrated here on the CPU forward pass (the device calibrates with its own
+    logits, so head_w/head_b agree to ~1e-6 relative, see tests)."""
+    f32 = np.float32
+    s1 = f32(1.7320508) / (f32(64.0) * np.sqrt(f32(768.0)))
+    s2 = f32(1.7320508) * np.sqrt(f32(2.0) / f32(256.0))
+    s3 = f32(1.7320508) * np.sqrt(f32(2.0) / f32(1024.0))
+    i1 = np.arange(768 * 256, dtype=np.uint64)
+    w1 = _to_bf16_bits(s1 * _unif_pm1(seed ^ 0x1111, i1)).reshape(768, 256)
+    w1[:, 255] = 0
+    n2 = 256 * 1024
+    e2 = np.arange(n2, dtype=np.uint64)
+    w2f = s2 * _unif_pm1(seed ^ 0x2222, e2)
+    w2f = w2f.reshape(256, 1024)
+    w2f[255, :] = (f32(0.05) * _unif_pm1(seed ^ 0x5555, np.arange(1024, dtype=np.uint64))) / f32(16)
+    w2f[:, 1023] = 0.0
+    w2f[255, 1023] = 1.0
+    w2 = _to_bf16_bits(w2f)
+    e3 = np.arange(1024 * 256, dtype=np.uint64)
+    w3f = (s3 * _unif_pm1(seed ^ 0x3333, e3)).reshape(1024, 256)
+    w3f[1023, :] = (f32(0.05) * _unif_pm1(seed ^ 0x6666, np.arange(256, dtype=np.uint64))) / f32(16)
+    w3 = _to_bf16_bits(w3f)
+    # b1: sequential f32 column sums (np.add.accumulate is sequential), then
+    # -128*s + 0.05*u with separate roundings
+    col = np.add.accumulate(bf16_bits_to_f32(w1), axis=0, dtype=np.float32)[-1]
+    u4 = _unif_pm1(seed ^ 0x4444, np.arange(256, dtype=np.uint64))
+    b1 = (f32(-128.0) * col + f32(0.05) * u4).astype(np.float32)
+    b1[255] = 16.0
+    hw = (_unif_pm1(seed ^ 0x7777, np.arange(256, dtype=np.uint64)) / f32(16.0)).astype(np.float32)
+    wts = dict(w1=w1, w2=w2, w3=w3, b1=b1, b2=np.zeros(1024, np.float32),
+               b3=np.zeros(256, np.float32), head_w=hw, head_b=0.0)
+    if calibrate:
+        cal = synth_images(0xCA11B8A7E, 0, 64, 512, 512)
+        lg = disc_forward(cal, wts, logits=True).astype(np.float64)
+        mean = lg.mean()
+        sd = np.sqrt(((lg - mean) ** 2).mean())
+        scale = np.float32(2.0 / sd)
+        wts["head_w"] = (hw * scale).astype(np.float32)
+        wts["head_b"] = float(np.float32(-mean * scale))
+    return wts

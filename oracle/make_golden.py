@@ -279,6 +279,43 @@ def gen_latent():
     np.savez_compressed(os.path.join(OUT, "latent.npz"), **out)
 
 
+def gen_des():
+    """Inputs + reference CSV digests for the drop-in DES run.
+    The digests come from the stock reference run_experiment (des_gpu --mode
+    cpu) on inputs re-written by oracle/des_inputs.py; they must equal the
+    digests of the reference's own files."""
+    import hashlib
+    import subprocess
+    import tempfile
+    from oracle import des_inputs
+    ref = "/root/reference/proj"
+    g = {}
+    for name, d in workloads.SHIPPED.items():
+        g[f"{name}_light"] = np.array(sorted(d["light"].items()), np.float64)
+        g[f"{name}_heavy"] = np.array(sorted(d["heavy"].items()), np.float64)
+        g[f"{name}_slo"] = np.float64(d["slo"])
+    g["prior"] = np.asarray(workloads.SHIPPED_PRIOR_SAMPLES, np.float64)
+    for t in ("trace_4to32qps", "trace_1to8qps", "trace_8to24qps"):
+        with open(f"{ref}/traces/{t}.txt") as f:
+            g[t] = np.array([float(x) for x in f.read().split()], np.float64)
+    exe = os.path.join(HERE, "_ref", "des_gpu")
+    with tempfile.TemporaryDirectory() as tmp:
+        cfgs = des_inputs.write_inputs(tmp, g)
+        for name, cfg in cfgs.items():
+            out = os.path.join(tmp, "out_" + name)
+            subprocess.run([exe, "--config", cfg, "--out", out, "--mode", "cpu"], cwd=tmp,
+                           check=True, capture_output=True)
+            outr = os.path.join(tmp, "outref_" + name)
+            subprocess.run([exe, "--config", f"configs/{name}.cfg", "--out", outr, "--mode", "cpu"],
+                           cwd=ref, check=True, capture_output=True)
+            for csv in ("intervals", "plans", "queries"):
+                a = hashlib.md5(open(os.path.join(out, csv + ".csv"), "rb").read()).hexdigest()
+                b = hashlib.md5(open(os.path.join(outr, csv + ".csv"), "rb").read()).hexdigest()
+                assert a == b, (name, csv, "rewritten inputs change the reference's output")
+                g[f"md5_{name}_{csv}"] = np.array(a)
+    np.savez_compressed(os.path.join(OUT, "des_inputs.npz"), **g)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("alloc_random_2024: feasible", gen_alloc_random(), "of 60")
@@ -287,6 +324,8 @@ def main():
     print("wide_random: feasible/total", gen_wide())
     gen_latent()
     print("latent: ok")
+    gen_des()
+    print("des: ok")
 
 
 if __name__ == "__main__":

@@ -520,18 +520,18 @@ __global__ void gen_weights_kernel(uint64_t seed, uint16_t* w1, uint16_t* w2, ui
          i += gridDim.x * blockDim.x) {
         if (i < n1) {
             const int n = i % kD1;
-            w1[i] = n == kD1 - 1 ? 0 : f2bf_bits(s1 * unif_pm1(seed ^ 0x1111, i));
+            w1[i] = n == kD1 - 1 ? 0 : f2bf_bits(__fmul_rn(s1, unif_pm1(seed ^ 0x1111, i)));
         } else if (i < n1 + n2) {
             const int e = i - n1, k = e / kD2, n = e % kD2;
             float v;
             if (n == kD2 - 1) v = k == kD1 - 1 ? 1.0f : 0.0f;          // h2[:,1023] = 16
-            else if (k == kD1 - 1) v = 0.05f * unif_pm1(seed ^ 0x5555, n) / kConst;  // b2 / 16
-            else v = s2 * unif_pm1(seed ^ 0x2222, e);
+            else if (k == kD1 - 1) v = __fmul_rn(0.05f, unif_pm1(seed ^ 0x5555, n)) / kConst;  // b2/16
+            else v = __fmul_rn(s2, unif_pm1(seed ^ 0x2222, e));
             w2[e] = f2bf_bits(v);
         } else {
             const int e = i - n1 - n2, k = e / kD3, n = e % kD3;
-            const float v = k == kD2 - 1 ? 0.05f * unif_pm1(seed ^ 0x6666, n) / kConst   // b3 / 16
-                                         : s3 * unif_pm1(seed ^ 0x3333, e);
+            const float v = k == kD2 - 1 ? __fmul_rn(0.05f, unif_pm1(seed ^ 0x6666, n)) / kConst  // b3/16
+                                         : __fmul_rn(s3, unif_pm1(seed ^ 0x3333, e));
             w3[e] = f2bf_bits(v);
         }
     }
@@ -573,9 +573,9 @@ __global__ void fold_bias_kernel(const uint16_t* w1, uint64_t seed, float* b1) {
         b1[n] = kConst;
         return;
     }
-    float s = 0.0f;
-    for (int k = 0; k < kD0; ++k) s += bf_bits2f(w1[k * kD1 + n]);
-    b1[n] = -128.0f * s + 0.05f * unif_pm1(seed ^ 0x4444, n);
+    float s = 0.0f;   // explicit _rn: no contraction, restated in oracle/disc_oracle.py
+    for (int k = 0; k < kD0; ++k) s = __fadd_rn(s, bf_bits2f(w1[k * kD1 + n]));
+    b1[n] = __fadd_rn(__fmul_rn(-128.0f, s), __fmul_rn(0.05f, unif_pm1(seed ^ 0x4444, n)));
 }
 
 } // namespace

@@ -79,3 +79,13 @@ def test_disc_rejects_bad_shapes(disc):
         disc.score(np.zeros((1, 100, 100, 3), np.uint8))
     with pytest.raises(native.InvalidArgument):
         disc.score(np.zeros((1, 128, 128, 3), np.uint8))   # 64 patches: not a 128-token tile
+
+
+def test_weights_match_host_restatement(weights):
+    """ds_disc_create's generator == oracle/disc_oracle.gen_weights bit for bit
+    (W1/W2/W3, b1); the head is calibrated on each side's own logits."""
+    ref = disc_oracle.gen_weights(2024, calibrate=True)
+    for k in ("w1", "w2", "w3", "b1"):
+        assert np.array_equal(weights[k], ref[k]), k
+    assert np.allclose(weights["head_w"], ref["head_w"], rtol=1e-4)
+    assert abs(weights["head_b"] - ref["head_b"]) <= 1e-3 * max(1.0, abs(ref["head_b"]))

@@ -155,3 +155,25 @@ def test_reference_unit_suites_pass_under_oracle_build():
     r = subprocess.run([exe], cwd=src, capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "0 failed" in r.stdout
+
+
+def test_disc_weight_restatement_matches_committed_export():
+    """oracle/disc_oracle.gen_weights vs the GPU export committed in profiles/."""
+    import os
+    from oracle import disc_oracle
+    path = os.path.join(os.path.dirname(lib.HERE), "profiles", "disc_weights_seed2024.npz")
+    if not os.path.exists(path):
+        pytest.skip("no committed export")
+    c = dict(np.load(path))
+    w = disc_oracle.gen_weights(2024, calibrate=False)
+    for k in ("w1", "w2", "w3"):
+        assert np.array_equal(w[k], c[k]), k
+    assert np.abs(w["b1"] - c["b1"]).max() <= 2e-7 * max(1.0, float(np.abs(c["b1"]).max()))
+
+
+def test_synth_images_host_restatement_is_deterministic():
+    from oracle import disc_oracle
+    a = disc_oracle.synth_images(1, 0, 2, 32, 32)
+    b = disc_oracle.synth_images(1, 0, 2, 32, 32)
+    assert np.array_equal(a, b) and a.dtype == np.uint8 and a.shape == (2, 32, 32, 3)
+    assert not np.array_equal(a[0], a[1])
