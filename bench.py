@@ -288,6 +288,7 @@ def run_gpu(args):
     import torch.distributed as dist
 
     from paper_2411_15381_b200 import abi, native, workloads
+    from paper_2411_15381_b200 import dist as ddist
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -318,7 +319,6 @@ def run_gpu(args):
     _olib.port().dso_curve_observe(abi.ptr(prior), abi.ptr(s), len(s), 1.0)
     prior_t = torch.from_numpy(prior.reshape(1).view(np.uint8).copy()).to(dev)
     curve_t = torch.empty_like(prior_t)
-    gathered = torch.empty(ws * NT, dtype=torch.int64, device=dev)
 
     def step(ev=None):
         with torch.cuda.stream(stream):
@@ -338,9 +338,9 @@ def run_gpu(args):
                                                    native.c_p(conf.data_ptr()), abi.CONF_F32,
                                                    N_IMG, DECAY, native.c_p(ctx.stream)))
             if ws > 1:
-                dist.all_gather_into_tensor(gathered, counts)
-                # exclusive scan over ranks: this rank's offset in each global heavy queue
-                offsets = gathered.view(ws, NT)[:rank].sum(0)  # noqa: F841
+                # routed-count all-gather + exclusive scan over ranks: this
+                # rank's offset inside each of the 101 global heavy queues
+                ddist.global_offsets_device(counts)
 
     # ---- warmup + timed region -------------------------------------------------
     for _ in range(args.warmup):

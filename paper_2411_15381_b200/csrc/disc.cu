@@ -736,21 +736,41 @@ extern "C" ds_status ds_disc_score_device(ds_disc* d, const uint8_t* nhwc, int64
     return launch_disc(d, nhwc, n, h, w, conf, 0, st);
 }
 
+// Host-buffer entry: the image upload is pipelined with scoring -- chunks of
+// kChunkImgs images alternate between two device buffers; chunk k+1's copy
+// (on the ctx copy stream) overlaps chunk k's kernel (on the ctx stream).
 extern "C" ds_status ds_disc_score(ds_disc* d, const uint8_t* nhwc, int64_t n, int32_t h, int32_t w,
                                    float* conf) {
     if (!d || (n > 0 && (!nhwc || !conf))) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
     if (n <= 0) return DS_OK;
     ds_ctx* ctx = d->ctx;
+    ds_status s = dsi::ensure_copy_stream(ctx);
+    if (s != DS_OK) return s;
+    constexpr int64_t kChunkImgs = 148 * 4;
     const size_t img_bytes = static_cast<size_t>(h) * w * 3;
-    const size_t bi = dsi::align_up(img_bytes * n, 256);
+    const int64_t chunk = n < kChunkImgs ? n : kChunkImgs;
+    const size_t bi = dsi::align_up(img_bytes * chunk, 256);
     char* buf = nullptr;
-    ds_status s = dsi::ensure_scratch(ctx, bi + dsi::align_up(sizeof(float) * n, 256),
-                                      reinterpret_cast<void**>(&buf));
+    s = dsi::ensure_scratch(ctx, 2 * bi + dsi::align_up(sizeof(float) * n, 256),
+                            reinterpret_cast<void**>(&buf));
     if (s != DS_OK) return s;
-    DS_CUDA_TRY(cudaMemcpyAsync(buf, nhwc, img_bytes * n, cudaMemcpyHostToDevice, ctx->stream));
-    float* dconf = reinterpret_cast<float*>(buf + bi);
-    s = launch_disc(d, reinterpret_cast<uint8_t*>(buf), n, h, w, dconf, 0, ctx->stream);
-    if (s != DS_OK) return s;
+    float* dconf = reinterpret_cast<float*>(buf + 2 * bi);
+    cudaEvent_t* copied = ctx->ev;          // ev[0], ev[1]
+    cudaEvent_t* consumed = ctx->ev + 2;    // ev[2], ev[3]
+    int k = 0;
+    for (int64_t off = 0; off < n; off += chunk, ++k) {
+        const int b = k & 1;
+        const int64_t m = n - off < chunk ? n - off : chunk;
+        uint8_t* dst = reinterpret_cast<uint8_t*>(buf + b * bi);
+        if (k >= 2) DS_CUDA_TRY(cudaStreamWaitEvent(ctx->copy_stream, consumed[b], 0));
+        DS_CUDA_TRY(cudaMemcpyAsync(dst, nhwc + static_cast<size_t>(off) * img_bytes,
+                                    img_bytes * m, cudaMemcpyHostToDevice, ctx->copy_stream));
+        DS_CUDA_TRY(cudaEventRecord(copied[b], ctx->copy_stream));
+        DS_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, copied[b], 0));
+        s = launch_disc(d, dst, m, h, w, dconf + off, 0, ctx->stream);
+        if (s != DS_OK) return s;
+        DS_CUDA_TRY(cudaEventRecord(consumed[b], ctx->stream));
+    }
     DS_CUDA_TRY(cudaMemcpyAsync(conf, dconf, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
     DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return DS_OK;

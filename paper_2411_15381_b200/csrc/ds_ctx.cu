@@ -56,6 +56,13 @@ ds_status ensure_pinned(ds_ctx* ctx, size_t bytes, void** out) {
     return DS_OK;
 }
 
+ds_status ensure_copy_stream(ds_ctx* ctx) {
+    if (ctx->copy_stream) return DS_OK;
+    DS_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev) DS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return DS_OK;
+}
+
 } // namespace dsi
 
 extern "C" {
@@ -97,6 +104,12 @@ ds_status ds_ctx_destroy(ds_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return DS_OK;

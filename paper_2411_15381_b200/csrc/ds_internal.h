@@ -20,6 +20,9 @@ struct ds_ctx {
     // pinned host staging for small results
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
+    // second stream + events for copy/compute overlap in host-buffer calls
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace dsi {
@@ -33,6 +36,7 @@ ds_status cuda_fail(cudaError_t e, const char* what);
 // ctx are serialized by the stream).
 ds_status ensure_scratch(ds_ctx* ctx, size_t bytes, void** out);
 ds_status ensure_pinned(ds_ctx* ctx, size_t bytes, void** out);
+ds_status ensure_copy_stream(ds_ctx* ctx);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -1,0 +1,50 @@
+"""Multi-GPU plumbing for the hot path: one process per GPU,
+torch.distributed for the collectives.
+
+* Queries shard by contiguous id range; each rank routes its shard with
+  index_base = its first id, so every heavy-queue id it writes is global.
+* The only data-path collective is an all-gather of the per-rank routed
+  counts ([T] int64 per rank); an exclusive scan over ranks gives each rank's
+  offset inside every global heavy queue, and concatenating the per-rank
+  lists in rank order reproduces the single-GPU (= reference) id order.
+* Planner problems shard by index; plans are independent (no collective on
+  the data path; gather only to report).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) of a contiguous, balanced split of n items over world ranks."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad world/rank")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def exclusive_offsets(gathered_counts: np.ndarray) -> np.ndarray:
+    """[world, T] routed counts -> [world, T] start offset of each rank's
+    block inside every global heavy queue (exclusive scan over ranks)."""
+    c = np.asarray(gathered_counts, np.int64)
+    out = np.zeros_like(c)
+    out[1:] = np.cumsum(c[:-1], axis=0)
+    return out
+
+
+def gather_counts(counts, group=None):
+    """All-gather of a rank's [T] int64 routed counts (torch tensor on the
+    rank's device for NCCL, CPU for gloo) -> [world, T] tensor."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = torch.empty(world * counts.numel(), dtype=counts.dtype, device=counts.device)
+    dist.all_gather_into_tensor(out, counts.contiguous(), group=group)
+    return out.view(world, counts.numel())
+
+
+def global_offsets_device(counts, group=None):
+    """Device-side version: gathered counts -> this rank's offsets [T]."""
+    import torch.distributed as dist
+    g = gather_counts(counts, group)
+    rank = dist.get_rank(group)
+    return g[:rank].sum(0) if rank > 0 else g[0] * 0

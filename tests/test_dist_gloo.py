@@ -1,0 +1,144 @@
+"""CPU suite: the multi-GPU host logic over world_size-2 gloo process groups.
+
+Each rank routes its contiguous id shard (here with the C oracle, as test
+infrastructure standing in for K2 on a GPU), all-gathers its routed counts,
+and places its ordered ids at the exclusive-scan offset; the assembled global
+heavy queues must equal single-rank routing of all queries (the reference's
+id order, cluster.cpp:290-306). Planner sharding likewise reproduces the
+single-rank plans."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import lib
+from paper_2411_15381_b200 import abi, dist as ddist, workloads
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _route_worker(rank, world, port, conf, thr, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = len(conf)
+        lo, hi = ddist.shard_range(n, world, rank)
+        mine = np.ascontiguousarray(conf[lo:hi])
+        nt = len(thr)
+        idx = np.zeros(nt * max(hi - lo, 1), np.int64)
+        cnt = np.zeros(nt, np.int64)
+        lib.port().dso_route(abi.ptr(mine), hi - lo, abi.ptr(thr), nt, lo, abi.ptr(idx),
+                             abi.ptr(cnt))
+        g = ddist.gather_counts(torch.from_numpy(cnt)).numpy()
+        offs = ddist.exclusive_offsets(g)[rank]
+        total = g.sum(0)
+        # every rank writes its block into its own copy of the global queues;
+        # a sum-reduce assembles them (blocks are disjoint)
+        glob = np.zeros((nt, n), np.int64)
+        for k in range(nt):
+            glob[k, offs[k]:offs[k] + cnt[k]] = idx[k * (hi - lo): k * (hi - lo) + cnt[k]] + 1
+        t = torch.from_numpy(glob)
+        dist.all_reduce(t)
+        if rank == 0:
+            q.put((total, t.numpy() - 1))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_routing_equals_single_rank_order(world):
+    rng = np.random.default_rng(world)
+    conf = rng.random(10_007)
+    conf[::9] = 0.5
+    thr = workloads.make_grid(0.05)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_route_worker, args=(r, world, port, conf, thr, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    total, glob = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = len(conf)
+    idx = np.zeros(len(thr) * n, np.int64)
+    cnt = np.zeros(len(thr), np.int64)
+    lib.port().dso_route(abi.ptr(conf), n, abi.ptr(thr), len(thr), 0, abi.ptr(idx), abi.ptr(cnt))
+    assert np.array_equal(total, cnt)
+    for k in range(len(thr)):
+        assert np.array_equal(glob[k, :cnt[k]], idx[k * n: k * n + cnt[k]])
+
+
+def _plan_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "config4.npz")))
+        pro = g["problems"]
+        lo, hi = ddist.shard_range(len(pro), world, rank)
+        mine = np.ascontiguousarray(pro[lo:hi])
+        out = np.zeros(hi - lo, abi.PLAN)
+        st = np.zeros(hi - lo, np.int32)
+        lib.port().dso_plan_batch(abi.ptr(mine), hi - lo, abi.ptr(g["cascades"]),
+                                  abi.ptr(g["grid_values"]), abi.ptr(g["grid_offsets"]),
+                                  abi.ptr(out), abi.ptr(st), 2)
+        parts = [None] * world
+        dist.all_gather_object(parts, out.tobytes())
+        if rank == 0:
+            q.put(b"".join(parts))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_planner_equals_reference_plans():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = np.frombuffer(q.get(timeout=120), abi.PLAN)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "config4.npz")))
+    assert got.tobytes() == g["want_solve"].tobytes()
+
+
+def test_shard_range_and_offsets():
+    assert [ddist.shard_range(10, 3, r) for r in range(3)] == [(0, 3), (3, 6), (6, 10)]
+    offs = ddist.exclusive_offsets(np.array([[2, 0], [3, 1], [1, 4]]))
+    assert offs.tolist() == [[0, 0], [2, 0], [5, 1]]
+    with pytest.raises(ValueError):
+        ddist.shard_range(5, 2, 2)
+
+
+def test_curve_shards_combine_exactly_at_decay_one():
+    """S7 with decay 1: integer bin counts add across shards exactly (8(e))."""
+    rng = np.random.default_rng(0)
+    conf = rng.random(5000)
+    whole = np.zeros((), abi.CURVE)
+    lib.port().dso_curve_observe(abi.ptr(whole), abi.ptr(conf), len(conf), 1.0)
+    parts = []
+    for r in range(2):
+        lo, hi = ddist.shard_range(len(conf), 2, r)
+        c = np.zeros((), abi.CURVE)
+        s = np.ascontiguousarray(conf[lo:hi])
+        lib.port().dso_curve_observe(abi.ptr(c), abi.ptr(s), len(s), 1.0)
+        parts.append(c)
+    assert np.array_equal(parts[0]["bin_mass"] + parts[1]["bin_mass"], whole["bin_mass"])

@@ -89,3 +89,19 @@ def test_weights_match_host_restatement(weights):
         assert np.array_equal(weights[k], ref[k]), k
     assert np.allclose(weights["head_w"], ref["head_w"], rtol=1e-4)
     assert abs(weights["head_b"] - ref["head_b"]) <= 1e-3 * max(1.0, abs(ref["head_b"]))
+
+
+def test_pipelined_host_path_equals_device_path(disc):
+    """ds_disc_score (chunked H2D overlapped with scoring, 592-image chunks)
+    returns exactly what ds_disc_score_device returns on the same images."""
+    import torch
+    ctx = default_context()
+    n = 700
+    dev = torch.empty(n * 256 * 512 * 3, dtype=torch.uint8, device="cuda")
+    native.check(native.lib().ds_synth_images_device(ctx.handle, 11, 0, n, 256, 512,
+                                                     native.c_p(dev.data_ptr()), native.c_p(0)))
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    disc.score_device(dev.data_ptr(), n, 256, 512, out.data_ptr(), 0)
+    torch.cuda.synchronize()
+    host = dev.cpu().numpy().reshape(n, 256, 512, 3)
+    assert np.array_equal(disc.score(host), out.cpu().numpy())
