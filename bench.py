@@ -148,7 +148,7 @@ def cpu_images_leg(n_img: int):
             r.dsref_curve_from_samples(abi.ptr(s), len(s), abi.ptr(curve))
             r.dsref_route_loop(abi.ptr(conf), n_img, float(t), 1 if k == 0 else 0, DECAY,
                                abi.ptr(curve), abi.ptr(idx), abi.ptr(cnt))
-        kind = "reference+port"
+        kind = "port"   # discriminator is this repo's port; route loop is the reference's
     else:
         p = lib.port()
         for k, t in enumerate(grid):

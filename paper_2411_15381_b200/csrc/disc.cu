@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -46,38 +47,46 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kM = 128;
+constexpr int kM = 128;                 // tokens per CTA per tile
 constexpr int kD0 = DS_DISC_D0, kD1 = DS_DISC_D1, kD2 = DS_DISC_D2, kD3 = DS_DISC_D3;
-constexpr int kBStage = 16384;          // 256 rows (N) x 32 bf16 (K), SW64
+constexpr int kBStage = 16384;          // one blob stage: 256 rows (N) x 32 bf16 (K), SW64
 constexpr int kW1Stages = 24, kWChunkStages = 8;
 constexpr int kBlobStages = kW1Stages + 8 * kWChunkStages;   // W1 | W2_0..3 | W3_0..3 = 88
 constexpr int kAChunk = 16384;          // 128 rows x 64 bf16, SW128
 constexpr int kChunksPerTile = 12;      // K = 768 = 12 x 64
-constexpr int kAStages = 2, kBStages = 4;
 constexpr int kThreads = 448;
-// dynamic shared memory map (base is 1024-aligned; no static __shared__)
-constexpr int kR1 = 0;                          // H1: 4 K-chunks x 16 KB
-constexpr int kR2 = kR1 + 65536;                // H2_j: 4 K-chunks x 16 KB
-constexpr int kARing = kR2 + 65536;
-constexpr int kBRing = kARing + kAStages * kAChunk;
-constexpr int kB1 = kBRing + kBStages * kBStage;   // float b1[256]
-constexpr int kHW = kB1 + 1024;                     // float head_w[256]
-constexpr int kBar = kHW + 1024;                    // mbarriers + misc
-constexpr int kSmemBytes = kBar + 256;
-constexpr uint32_t kIdesc = idesc_bf16_f32(128, 256);
-constexpr float kConst = 16.0f;                     // value of the constant features
-constexpr int kDepth = 4;                           // A-builder prefetch depth (chunks)
+constexpr float kConst = 16.0f;         // value of the constant features
+constexpr int kDepth = 4;               // A-builder prefetch depth (chunks)
 static_assert(kChunksPerTile % kDepth == 0, "slot = chunk % kDepth must be static");
-static_assert(kSmemBytes <= 232448, "shared memory budget");
+
+// Per-mode geometry. kPair: an SM pair (cta_group::2) computes M = 256, each
+// CTA holds its own 128 token rows and HALF of every weight stage (N = 128
+// rows, 8 KB), so per-SM B traffic halves and the weight ring deepens.
+template <bool kPair>
+struct Geo {
+    static constexpr int kCtas = kPair ? 2 : 1;
+    static constexpr int kTokPerTile = kM * kCtas;
+    static constexpr int kBHalf = kBStage / kCtas;            // bytes of a stage per CTA
+    static constexpr int kAStages = kPair ? 3 : 2;
+    static constexpr int kBStages = kPair ? 6 : 4;
+    static constexpr int kR1 = 0;                             // H1: 4 K-chunks x 16 KB
+    static constexpr int kR2 = kR1 + 65536;                   // H2_j: 4 K-chunks x 16 KB
+    static constexpr int kARing = kR2 + 65536;
+    static constexpr int kBRing = kARing + kAStages * kAChunk;
+    static constexpr int kB1 = kBRing + kBStages * kBHalf;    // float b1[256]
+    static constexpr int kHW = kB1 + 1024;                    // float head_w[256]
+    static constexpr int kBar = kHW + 1024;                   // mbarriers + misc
+    static constexpr int kSmemBytes = kBar + 512;
+    static constexpr uint32_t kIdesc = idesc_bf16_f32(128 * kCtas, 256);
+    static_assert(kSmemBytes <= 232448, "shared memory budget");
+};
 
 struct DiscParams {
     float b1[kD1];
     float hw[kD3];
-    float hb;
-    int out_logit;
     const uint8_t* images;
     const uint8_t* wblob;
-    float* out;
+    float* part;        // per (image, CTA of the pair) sum of head scores
     long long n_img;
     int h, w, px, tokens, tiles_per_img;
     long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr = off)
@@ -122,20 +131,26 @@ __device__ __forceinline__ void u8x16_to_bf16(const uint4 v, uint32_t (&o)[8]) {
 }
 
 struct Bars {
-    uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
+    uint64_t a_full[3], a_empty[3], b_full[6], b_empty[6];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
     uint32_t tmem_base;
     float warp_part[2][8];
 };
-static_assert(sizeof(Bars) <= 256, "barrier block");
+static_assert(sizeof(Bars) <= 512, "barrier block");
 
+template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant__ DiscParams P) {
+    using G = Geo<kPair>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    Bars& B = *reinterpret_cast<Bars*>(smem + kBar);
-    float* s_b1 = reinterpret_cast<float*>(smem + kB1);
-    float* s_hw = reinterpret_cast<float*>(smem + kHW);
+    Bars& B = *reinterpret_cast<Bars*>(smem + G::kBar);
+    float* s_b1 = reinterpret_cast<float*>(smem + G::kB1);
+    float* s_hw = reinterpret_cast<float*>(smem + G::kHW);
     const uint32_t sbase = smem_u32(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const long long unit = kPair ? cluster_id_x() : blockIdx.x;   // pair (or CTA) index
+    const long long nunits = kPair ? nclusters_x() : gridDim.x;
 
     if (sbase & 1023u) __trap();   // SW128 operand tiles need 1024-byte alignment
     if (threadIdx.x < kD1) {
@@ -143,56 +158,84 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         s_hw[threadIdx.x] = P.hw[threadIdx.x];
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kAStages; ++s) { mbar_init(&B.a_full[s], 128); mbar_init(&B.a_empty[s], 1); }
-        for (int s = 0; s < kBStages; ++s) { mbar_init(&B.b_full[s], 1); mbar_init(&B.b_empty[s], 1); }
+        // The leader's barriers also count the peer's single relayed arrival.
+        const uint32_t peer = (kPair && leader) ? 1u : 0u;
+        for (int s = 0; s < G::kAStages; ++s) {
+            mbar_init(&B.a_full[s], 128 + peer);
+            mbar_init(&B.a_empty[s], 1);
+        }
+        for (int s = 0; s < G::kBStages; ++s) {
+            mbar_init(&B.b_full[s], 1 + peer);
+            mbar_init(&B.b_empty[s], 1);
+        }
         mbar_init(&B.acc12_full, 1);
-        mbar_init(&B.drained, 256);
-        mbar_init(&B.h2_ready, 256);
+        mbar_init(&B.drained, 256 + peer);
+        mbar_init(&B.h2_ready, 256 + peer);
         mbar_init(&B.h2_free, 1);
         mbar_init(&B.acc3_full, 1);
-        mbar_init(&B.acc3_empty, 256);
+        mbar_init(&B.acc3_empty, 256 + peer);
         fence_mbar_init();
     }
-    if (warp == 13) tmem_alloc<512>(&B.tmem_base);
+    if (warp == 13) {
+        if constexpr (kPair) tmem_alloc2<512>(&B.tmem_base);
+        else tmem_alloc<512>(&B.tmem_base);
+    }
     tc_fence_before();
     __syncthreads();
+    if constexpr (kPair) cluster_sync();   // peer barriers initialised before remote arrives
     tc_fence_after();
     const uint32_t tmem = B.tmem_base;
 
+    // Signal helpers: a role's arrival on the LEADER's barrier. The leader's
+    // threads arrive locally; the peer's group syncs on a named barrier and one
+    // thread forwards a single cluster-scope arrive.
+    auto group_signal = [&](uint64_t* bar, uint32_t bar_id, uint32_t threads, bool first) {
+        if (!kPair || leader) {
+            mbar_arrive(bar);
+        } else {
+            named_bar_sync(bar_id, threads);
+            if (first) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+        }
+    };
+    auto commit = [&](uint64_t* bar) {
+        if constexpr (kPair) umma_commit_pair(bar, 0x3);
+        else umma_commit(bar);
+    };
+
     const long long n_img = P.n_img;
     const int tpi = P.tiles_per_img;
-    const long long my_imgs =
-        blockIdx.x < n_img ? (n_img - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long my_imgs = unit < n_img ? (n_img - 1 - unit) / nunits + 1 : 0;
     const long long my_tiles = my_imgs * tpi;
     const long long img_bytes = static_cast<long long>(P.h) * P.w * 3;
     const long long row_bytes = static_cast<long long>(P.w) * 3;
+    const int tok_off = static_cast<int>(rank) * kM;   // this CTA's rows in a tile
 
     if (warp < 4) {
         // ===================== A-builder (128 threads, thread = token) =========
         const int tl = threadIdx.x;
-        // byte offset of piece q (0..47) of a token's 768-byte patch vector:
-        // patch row dy = q / 3, 16-byte run (q % 3) of that row's 48 bytes
         auto token_base = [&](long long tile) -> const uint8_t* {
-            const long long img = blockIdx.x + (tile / tpi) * gridDim.x;
-            const int tok = static_cast<int>(tile % tpi) * kM + tl;
+            const long long img = unit + (tile / tpi) * nunits;
+            const int tok = static_cast<int>(tile % tpi) * G::kTokPerTile + tok_off + tl;
             const int py = tok / P.px, px = tok - py * P.px;
             return P.images + img * img_bytes + (static_cast<long long>(py) * 16) * row_bytes +
                    px * 48;
         };
+        // byte offset of piece q (0..47) of a token's 768-byte patch vector:
+        // patch row dy = q / 3, 16-byte run (q % 3) of that row's 48 bytes
         auto piece = [&](const uint8_t* base, int q) -> const uint8_t* {
             return base + (q / 3) * row_bytes + (q % 3) * 16;
         };
-        // The pixels of a tile are one contiguous byte range (whole patch rows
-        // when px divides 128 or 128 divides px; otherwise a small superset).
+        // The pixels of this CTA's half tile are one contiguous byte range of
+        // whole patch rows (or a small superset); bulk-prefetch it into L2.
         auto prefetch_tile = [&](long long tile) {
-            const long long img = blockIdx.x + (tile / tpi) * gridDim.x;
-            const int tok0 = static_cast<int>(tile % tpi) * kM;
+            const long long img = unit + (tile / tpi) * nunits;
+            const int tok0 = static_cast<int>(tile % tpi) * G::kTokPerTile + tok_off;
             const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
             const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
-            long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
+            const long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
             for (long long off = 0; off < bytes; off += 65536) {
-                const uint32_t n = static_cast<uint32_t>(bytes - off < 65536 ? bytes - off : 65536);
-                bulk_prefetch_l2(p0 + off, n);
+                const uint32_t nb = static_cast<uint32_t>(bytes - off < 65536 ? bytes - off : 65536);
+                bulk_prefetch_l2(p0 + off, nb);
             }
         };
         const long long total_chunks = my_tiles * kChunksPerTile;
@@ -201,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             if (my_tiles > 1) prefetch_tile(1);
         }
         uint4 buf[kDepth][4];
-        const uint8_t* pbase = my_tiles > 0 ? token_base(0) : nullptr;   // tile of chunk g+kDepth
+        const uint8_t* pbase = my_tiles > 0 ? token_base(0) : nullptr;
         long long ptile = 0;
 #pragma unroll
         for (int d = 0; d < kDepth; ++d)
@@ -220,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     if (g / kChunksPerTile + 2 < my_tiles) prefetch_tile(g / kChunksPerTile + 2);
                 }
                 mbar_wait(&B.a_empty[astage], aphase ^ 1);
-                const uint32_t st = sbase + kARing + astage * kAChunk;
+                const uint32_t st = sbase + G::kARing + astage * kAChunk;
 #pragma unroll
                 for (int s = 0; s < 4; ++s) {
                     uint32_t o[8];
@@ -229,9 +272,9 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     st_shared_v4(st + sw128(tl, 2 * s + 1), o[4], o[5], o[6], o[7]);
                 }
                 fence_proxy_async_smem();
-                mbar_arrive(&B.a_full[astage]);
+                group_signal(&B.a_full[astage], 2, 128, tl == 0);
                 if (tl == 0 && c == kChunksPerTile - 1) DS_TRACE(0, g / kChunksPerTile, 1);
-                if (++astage == kAStages) { astage = 0; aphase ^= 1; }
+                if (++astage == G::kAStages) { astage = 0; aphase ^= 1; }
                 const long long gn = g + kDepth;
                 if (gn < total_chunks) {
                     const long long tn = gn / kChunksPerTile;
@@ -249,10 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         const int half = ew >> 2;          // column half [128*half, 128*half+128)
         const uint32_t row = 32 * q + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
+        const bool first = ew == 0 && lane == 0;
         uint32_t p12 = 0, p3 = 0, pfree = 0;
         float img_acc = 0.0f;
 
-        // E3: ReLU(acc3) . w_head over this thread's 128 columns -> per-image mean
+        // E3: ReLU(acc3) . w_head over this thread's 128 columns -> per-image sum
         auto e3 = [&](long long tile) {
             mbar_wait(&B.acc3_full, p3);
             p3 ^= 1;
@@ -273,23 +317,22 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     part[e & 3] += fmaxf(__uint_as_float(v1[e]), 0.0f) * s_hw[c0 + 32 + e];
             }
             tc_fence_before();
-            mbar_arrive(&B.acc3_empty);
+            group_signal(&B.acc3_empty, 3, 256, first);
             DS_TRACE(1, tile, 11);
             float p = (part[0] + part[1]) + (part[2] + part[3]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-            const int buf = static_cast<int>(tile & 1);
-            if (lane == 0) B.warp_part[buf][ew] = p;
+            const int b = static_cast<int>(tile & 1);
+            if (lane == 0) B.warp_part[b][ew] = p;
             named_bar_sync(1, 256);
-            if (ew == 0 && lane == 0) {
+            if (first) {
                 float s = 0.0f;
 #pragma unroll
-                for (int w = 0; w < 8; ++w) s += B.warp_part[buf][w];
+                for (int w = 0; w < 8; ++w) s += B.warp_part[b][w];
                 img_acc += s;
                 if (tile % tpi == tpi - 1) {
-                    const long long img = blockIdx.x + (tile / tpi) * gridDim.x;
-                    const float logit = img_acc / static_cast<float>(P.tokens) + P.hb;
-                    P.out[img] = P.out_logit ? logit : 1.0f / (1.0f + expf(-logit));
+                    const long long img = unit + (tile / tpi) * nunits;
+                    P.part[img * G::kCtas + rank] = img_acc;
                     img_acc = 0.0f;
                 }
             }
@@ -320,14 +363,14 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                                                 gelu_tanh(__uint_as_float(v[e + 2 * u + 1]) + s_b1[c + 1]));
                         }
                         const int f = cbase + e;
-                        st_shared_v4(sbase + kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
+                        st_shared_v4(sbase + G::kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
                                      pk[0], pk[1], pk[2], pk[3]);
                     }
                 }
             }
             fence_proxy_async_smem();
             tc_fence_before();
-            mbar_arrive(&B.drained);
+            group_signal(&B.drained, 3, 256, first);
             DS_TRACE(1, tile, 1);
 
             // ---- E3 of the previous tile (its G3_3 was issued after G1(tile)) ----
@@ -351,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                                                       fmaxf(__uint_as_float(v[2 * e + 1]), 0.0f));
                 }
                 tc_fence_before();
-                mbar_arrive(&B.drained);            // MMA may overwrite acc[0,256) now
+                group_signal(&B.drained, 3, 256, first);   // MMA may overwrite acc[0,256)
                 if (tile > 0 || j > 0) {            // GEMM3 reading the previous H2 chunk done
                     mbar_wait(&B.h2_free, pfree);
                     pfree ^= 1;
@@ -361,13 +404,13 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int f = 128 * half + 32 * cb + 8 * e;
-                        st_shared_v4(sbase + kR2 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
+                        st_shared_v4(sbase + G::kR2 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
                                      pk[16 * cb + 4 * e], pk[16 * cb + 4 * e + 1],
                                      pk[16 * cb + 4 * e + 2], pk[16 * cb + 4 * e + 3]);
                     }
                 }
                 fence_proxy_async_smem();
-                mbar_arrive(&B.h2_ready);
+                group_signal(&B.h2_ready, 3, 256, first);
                 DS_TRACE(1, tile, 3 + 2 * j);
             }
         }
@@ -381,11 +424,11 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             auto put = [&](int first, int count) {
                 for (int t = first; t < first + count; ++t) {
                     mbar_wait(&B.b_empty[bs], bp ^ 1);
-                    mbar_arrive_expect_tx(&B.b_full[bs], kBStage);
-                    bulk_g2s_hint(smem + kBRing + bs * kBStage,
-                                  P.wblob + static_cast<size_t>(t) * kBStage, kBStage,
-                                  &B.b_full[bs], policy);
-                    if (++bs == kBStages) { bs = 0; bp ^= 1; }
+                    mbar_arrive_expect_tx(&B.b_full[bs], G::kBHalf);
+                    bulk_g2s_hint(smem + G::kBRing + bs * G::kBHalf,
+                                  P.wblob + static_cast<size_t>(t) * kBStage + rank * G::kBHalf,
+                                  G::kBHalf, &B.b_full[bs], policy);
+                    if (++bs == G::kBStages) { bs = 0; bp ^= 1; }
                 }
             };
             const int W1 = 0, W2 = kW1Stages, W3 = kW1Stages + 4 * kWChunkStages;
@@ -400,12 +443,29 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             }
             if (my_tiles > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
         }
+    } else if (kPair && !leader) {
+        // ===================== peer: relay weight-stage arrivals ==============
+        // (88 stages per tile; the leader's b_full counts this arrival)
+        if (lane == 0) {
+            const long long total = my_tiles * kBlobStages;
+            int bs = 0;
+            uint32_t bp = 0;
+            for (long long k = 0; k < total; ++k) {
+                mbar_wait(&B.b_full[bs], bp);
+                mbar_arrive_cluster(mapa_shared(smem_u32(&B.b_full[bs]), 0));
+                if (++bs == G::kBStages) { bs = 0; bp ^= 1; }
+            }
+        }
     } else {
-        // ===================== MMA issuer (warp 13, one thread) ==============
+        // ===================== MMA issuer (leader warp 13, one thread) ========
         if (lane == 0) {
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0, pdr = 0, prd = 0, pe3 = 0;
             const uint32_t acc12 = tmem, acc3 = tmem + 256;
+            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+                if constexpr (kPair) umma_bf16_pair(d, a, b, G::kIdesc, acc);
+                else umma_bf16(d, a, b, G::kIdesc, acc);
+            };
             // K = 64 x nk from an SW128 A region (nk chunks of 16 KB) against
             // 2*nk weight stages (K = 32 each).
             auto gemm = [&](uint32_t a_region, int nk, uint32_t acc, bool acc_in) {
@@ -415,13 +475,13 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     for (int hf = 0; hf < 2; ++hf) {
                         mbar_wait(&B.b_full[bs], bp);
                         tc_fence_after();
-                        const uint64_t bd = desc_k_sw64(sbase + kBRing + bs * kBStage);
+                        const uint64_t bd = desc_k_sw64(sbase + G::kBRing + bs * G::kBHalf);
 #pragma unroll
                         for (int k = 0; k < 2; ++k)
-                            umma_bf16(acc, ad + 2 * (2 * hf + k), bd + 2 * k, kIdesc,
-                                      (acc_in || kc > 0 || hf > 0 || k > 0) ? 1u : 0u);
-                        umma_commit(&B.b_empty[bs]);
-                        if (++bs == kBStages) { bs = 0; bp ^= 1; }
+                            mma(acc, ad + 2 * (2 * hf + k), bd + 2 * k,
+                                (acc_in || kc > 0 || hf > 0 || k > 0) ? 1u : 0u);
+                        commit(&B.b_empty[bs]);
+                        if (++bs == G::kBStages) { bs = 0; bp ^= 1; }
                     }
                 }
             };
@@ -432,32 +492,31 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             };
             for (long long tile = 0; tile < my_tiles; ++tile) {
                 DS_TRACE(2, tile, 0);
-                // G1: 12 A chunks from the ring
-                for (int c = 0; c < kChunksPerTile; ++c) {
+                for (int c = 0; c < kChunksPerTile; ++c) {       // G1: 12 A chunks
                     mbar_wait(&B.a_full[as], ap);
                     tc_fence_after();
-                    gemm(sbase + kARing + as * kAChunk, 1, acc12, c > 0);
-                    umma_commit(&B.a_empty[as]);
-                    if (++as == kAStages) { as = 0; ap ^= 1; }
+                    gemm(sbase + G::kARing + as * kAChunk, 1, acc12, c > 0);
+                    commit(&B.a_empty[as]);
+                    if (++as == G::kAStages) { as = 0; ap ^= 1; }
                 }
-                umma_commit(&B.acc12_full);
+                commit(&B.acc12_full);
                 DS_TRACE(2, tile, 1);
                 if (tile > 0) {                      // G3_3 of the previous tile
                     wait_bar(&B.h2_ready, prd);
-                    gemm(sbase + kR2, 4, acc3, true);
-                    umma_commit(&B.h2_free);
-                    umma_commit(&B.acc3_full);
+                    gemm(sbase + G::kR2, 4, acc3, true);
+                    commit(&B.h2_free);
+                    commit(&B.acc3_full);
                 }
                 DS_TRACE(2, tile, 2);
                 wait_bar(&B.drained, pdr);           // E1: acc drained, H1 stored
                 DS_TRACE(2, tile, 3);
-                gemm(sbase + kR1, 4, acc12, false);  // G2_0
-                umma_commit(&B.acc12_full);
+                gemm(sbase + G::kR1, 4, acc12, false);  // G2_0
+                commit(&B.acc12_full);
                 for (int j = 1; j < 4; ++j) {
                     wait_bar(&B.drained, pdr);       // E2_{j-1} has the values in registers
                     DS_TRACE(2, tile, 2 + 2 * j);
-                    gemm(sbase + kR1, 4, acc12, false);          // G2_j
-                    umma_commit(&B.acc12_full);
+                    gemm(sbase + G::kR1, 4, acc12, false);       // G2_j
+                    commit(&B.acc12_full);
                     wait_bar(&B.h2_ready, prd);      // H2_{j-1} stored
                     DS_TRACE(2, tile, 3 + 2 * j);
                     if (j == 1) {                    // acc3 drained by E3 of the previous tile
@@ -465,26 +524,39 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                         pe3 ^= 1;
                         tc_fence_after();
                     }
-                    gemm(sbase + kR2, 4, acc3, j > 1);           // G3_{j-1}
-                    umma_commit(&B.h2_free);
+                    gemm(sbase + G::kR2, 4, acc3, j > 1);        // G3_{j-1}
+                    commit(&B.h2_free);
                 }
                 wait_bar(&B.drained, pdr);           // E2_3 drained: acc[0,256) free
                 DS_TRACE(2, tile, 10);
             }
             if (my_tiles > 0) {
                 wait_bar(&B.h2_ready, prd);
-                gemm(sbase + kR2, 4, acc3, true);    // G3_3 of the last tile
-                umma_commit(&B.h2_free);
-                umma_commit(&B.acc3_full);
+                gemm(sbase + G::kR2, 4, acc3, true); // G3_3 of the last tile
+                commit(&B.h2_free);
+                commit(&B.acc3_full);
             }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (kPair) cluster_sync();     // both CTAs done with TMEM / remote barriers
     if (warp == 13) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem);
+        if constexpr (kPair) tmem_dealloc2<512>(tmem);
+        else tmem_dealloc<512>(tmem);
     }
+}
+
+// logit = (sum of the pair's per-image head sums) / tokens + b_head
+__global__ void finalize_kernel(const float* __restrict__ part, int ctas, long long n, int tokens,
+                                float hb, int logits, float* __restrict__ out) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float s = part[i * ctas];
+    for (int r = 1; r < ctas; ++r) s += part[i * ctas + r];
+    const float logit = s / static_cast<float>(tokens) + hb;
+    out[i] = logits ? logit : 1.0f / (1.0f + expf(-logit));
 }
 
 // ---- deterministic weights ---------------------------------------------------------
@@ -587,9 +659,38 @@ struct ds_disc {
     uint8_t* d_blob = nullptr;
     float* d_b1 = nullptr;
     DiscParams params{};       // b1 + head (device-independent part)
+    float hb = 0.0f;           // head bias
+    int force_ctas = 0;        // DS_DISC_CTAS=1|2 overrides the mode (testing)
 };
 
 namespace {
+
+template <bool kPair>
+ds_status launch_mode(ds_disc* d, const DiscParams& p, int units, cudaStream_t st) {
+    using G = Geo<kPair>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel<kPair>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         G::kSmemBytes));
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(units * G::kCtas));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = G::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = G::kCtas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, disc_kernel<kPair>, p));
+    DS_LAUNCH_CHECK(d->ctx, "disc_kernel");
+    return DS_OK;
+}
 
 ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w, float* out,
                       int logits, cudaStream_t st, long long* trace = nullptr) {
@@ -601,30 +702,34 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     if (reinterpret_cast<uintptr_t>(images) % 16)
         return dsi::fail(DS_ERR_INVALID_ARGUMENT, "image buffer must be 16-byte aligned");
     if (n <= 0) return DS_OK;
+    // SM pairs (cta_group::2) whenever a tile of 256 tokens divides the image
+    const bool pair = d->force_ctas == 1 ? false : (tokens % (2 * kM) == 0);
+    const int ctas = pair ? 2 : 1;
     DiscParams p = d->params;
-    p.out_logit = logits;
     p.images = images;
     p.wblob = d->d_blob;
-    p.out = out;
     p.n_img = n;
     p.h = h;
     p.w = w;
     p.px = w / 16;
     p.tokens = tokens;
-    p.tiles_per_img = tokens / kM;
+    p.tiles_per_img = tokens / (kM * ctas);
     p.trace = trace;
-    static bool attr_set = false;
-    if (!attr_set) {
-        DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kSmemBytes));
-        attr_set = true;
-    }
+    float* part = nullptr;
+    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * ctas * n, st));
+    p.part = part;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->ctx->device);
-    const int grid = static_cast<int>(n < sms ? n : sms);
-    disc_kernel<<<grid, kThreads, kSmemBytes, st>>>(p);
-    DS_LAUNCH_CHECK(d->ctx, "disc_kernel");
-    return DS_OK;
+    const int max_units = sms / ctas;
+    const int units = static_cast<int>(n < max_units ? n : max_units);
+    ds_status s = pair ? launch_mode<true>(d, p, units, st) : launch_mode<false>(d, p, units, st);
+    if (s == DS_OK) {
+        finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+            part, ctas, n, tokens, d->hb, logits, out);
+        DS_LAUNCH_CHECK(d->ctx, "finalize_kernel");
+    }
+    cudaFreeAsync(part, st);
+    return s;
 }
 
 } // namespace
@@ -664,7 +769,8 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
         return cleanup(dsi::cuda_fail(e, "copy b1"));
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "sync"));
     for (int i = 0; i < kD3; ++i) d->params.hw[i] = unif_pm1(weight_seed ^ 0x7777, i) / 16.0f;
-    d->params.hb = 0.0f;
+    d->hb = 0.0f;
+    if (const char* e = std::getenv("DS_DISC_CTAS")) d->force_ctas = std::atoi(e);
 
     // Head calibration: logits of 64 synthetic images (fixed seed) -> affine
     // head so confidences spread over (0, 1): w *= 2/sd, b = -mean * 2/sd.
@@ -696,7 +802,7 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
         return cleanup(dsi::fail(DS_ERR_CUDA, "discriminator calibration produced degenerate logits"));
     const float scale = static_cast<float>(2.0 / sd);
     for (int i = 0; i < kD3; ++i) d->params.hw[i] *= scale;
-    d->params.hb = static_cast<float>(-mean * scale);
+    d->hb = static_cast<float>(-mean * scale);
     *out = d;
     return DS_OK;
 }
@@ -725,7 +831,7 @@ extern "C" ds_status ds_disc_export(const ds_disc* d, uint16_t* w1, uint16_t* w2
     if (b2) std::memset(b2, 0, sizeof(float) * kD2);
     if (b3) std::memset(b3, 0, sizeof(float) * kD3);
     if (head_w) std::memcpy(head_w, d->params.hw, sizeof(d->params.hw));
-    if (head_b) *head_b = d->params.hb;
+    if (head_b) *head_b = d->hb;
     return DS_OK;
 }
 

@@ -105,3 +105,22 @@ def test_pipelined_host_path_equals_device_path(disc):
     torch.cuda.synchronize()
     host = dev.cpu().numpy().reshape(n, 256, 512, 3)
     assert np.array_equal(disc.score(host), out.cpu().numpy())
+
+
+def test_single_cta_mode_matches_pair_mode(disc, monkeypatch):
+    """DS_DISC_CTAS=1 forces the 1-CTA kernel; the cta_group::2 kernel computes
+    the same per-token values (only the final per-image sum is associated
+    differently)."""
+    monkeypatch.setenv("DS_DISC_CTAS", "1")
+    single = native.Discriminator(default_context(), weight_seed=2024)
+    imgs = disc_oracle.synth_images(5, 0, 12, 512, 512)
+    a = disc.score(imgs)
+    b = single.score(imgs)
+    single.close()
+    assert np.allclose(a, b, rtol=2e-5, atol=1e-6)
+
+
+def test_disc_single_cta_fallback_shapes(disc, weights):
+    """128 tokens per image (128x256): no 256-token pair tile -> 1-CTA path."""
+    imgs = disc_oracle.synth_images(9, 3, 5, 128, 256)
+    check_conf(disc.score(imgs), disc_oracle.disc_forward(imgs, weights))
