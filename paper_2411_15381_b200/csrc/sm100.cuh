@@ -27,17 +27,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
-// Blocks until the phase with parity `parity` has completed.
+// Blocks until the phase with parity `parity` has completed. No suspend-time
+// hint: with an explicit hint the retry loop compiles to a long NANOSLEEP,
+// which oversleeps when the releasing arrive comes from the peer CTA.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     asm volatile(
         "{\n\t"
         ".reg .pred P1;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
         "@!P1 bra WAIT_%=;\n\t"
         "}" ::"r"(a),
-        "r"(parity), "r"(0x989680)
+        "r"(parity)
         : "memory");
 }
 
