@@ -208,10 +208,13 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t smem_addr, uint32_t ran
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
     return r;
 }
-// Arrive (release, cluster scope) on an mbarrier given by a shared::cluster address.
+// Arrive on an mbarrier given by a shared::cluster address (possibly the peer
+// CTA's). Default .release.cta semantics, as CUTLASS's ClusterBarrier::arrive:
+// an explicit .release.cluster compiles to MEMBAR.ALL.GPU, which drains every
+// outstanding global load of the arriving thread (the A-builder's prefetches).
+// Callers order their shared-memory writes first (fence.proxy.async + bar.sync).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 template <uint32_t kCols>
