@@ -67,8 +67,8 @@ struct Geo {
     static constexpr int kCtas = kPair ? 2 : 1;
     static constexpr int kTokPerTile = kM * kCtas;
     static constexpr int kBHalf = kBStage / kCtas;            // bytes of a stage per CTA
-    static constexpr int kAStages = kPair ? 3 : 2;
-    static constexpr int kBStages = kPair ? 6 : 4;
+    static constexpr int kAStages = 2;
+    static constexpr int kBStages = kPair ? 8 : 4;
     static constexpr int kR1 = 0;                             // H1: 4 K-chunks x 16 KB
     static constexpr int kR2 = kR1 + 65536;                   // H2_j: 4 K-chunks x 16 KB
     static constexpr int kARing = kR2 + 65536;
@@ -104,6 +104,21 @@ __device__ __forceinline__ float gelu_tanh(float x) {
     return 0.5f * x * (1.0f + tanh_approx(u));
 }
 
+// GELU_tanh of two values with ONE packed MUFU op (tanh.approx.f16x2): the
+// tanh argument is rounded to fp16 (11 significant bits; the result is stored
+// as bf16, 8 bits, right after). Returns the bf16x2 pack (lo = a, hi = b).
+__device__ __forceinline__ uint32_t gelu_tanh_pack2(float a, float b) {
+    const float ua = 0.7978845608028654f * (a + 0.044715f * a * a * a);
+    const float ub = 0.7978845608028654f * (b + 0.044715f * b * b * b);
+    uint32_t h, t;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(ub), "f"(ua));
+    asm("tanh.approx.f16x2 %0, %1;" : "=r"(t) : "r"(h));
+    float ta, tb;
+    asm("{\n\t.reg .f16 l, hh;\n\tmov.b32 {l, hh}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, hh;\n\t}"
+        : "=f"(ta), "=f"(tb) : "r"(t));
+    return pack_bf16x2(0.5f * a * (1.0f + ta), 0.5f * b * (1.0f + tb));
+}
+
 // Byte offset of (row, 16-byte chunk) inside a K-major SW128 tile (128 B rows).
 __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
     return (row >> 3) * 1024u + (row & 7u) * 128u + ((chunk ^ (row & 7u)) << 4);
@@ -131,7 +146,7 @@ __device__ __forceinline__ void u8x16_to_bf16(const uint4 v, uint32_t (&o)[8]) {
 }
 
 struct Bars {
-    uint64_t a_full[3], a_empty[3], b_full[6], b_empty[6];
+    uint64_t a_full[2], a_empty[2], b_full[8], b_empty[8];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
     uint32_t tmem_base;
     float warp_part[2][8];
@@ -263,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     if (g / kChunksPerTile + 2 < my_tiles) prefetch_tile(g / kChunksPerTile + 2);
                 }
                 mbar_wait(&B.a_empty[astage], aphase ^ 1);
+                if (tl == 0) DS_TRACE(3, g / kChunksPerTile, c);
                 const uint32_t st = sbase + G::kARing + astage * kAChunk;
 #pragma unroll
                 for (int s = 0; s < 4; ++s) {
@@ -273,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 }
                 fence_proxy_async_smem();
                 group_signal(&B.a_full[astage], 2, 128, tl == 0);
+                if (tl == 0) DS_TRACE(4, g / kChunksPerTile, c);
                 if (tl == 0 && c == kChunksPerTile - 1) DS_TRACE(0, g / kChunksPerTile, 1);
                 if (++astage == G::kAStages) { astage = 0; aphase ^= 1; }
                 const long long gn = g + kDepth;
@@ -359,8 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int c = cbase + e + 2 * u;
-                            pk[u] = pack_bf16x2(gelu_tanh(__uint_as_float(v[e + 2 * u]) + s_b1[c]),
-                                                gelu_tanh(__uint_as_float(v[e + 2 * u + 1]) + s_b1[c + 1]));
+                            pk[u] = gelu_tanh_pack2(__uint_as_float(v[e + 2 * u]) + s_b1[c],
+                                                    __uint_as_float(v[e + 2 * u + 1]) + s_b1[c + 1]);
                         }
                         const int f = cbase + e;
                         st_shared_v4(sbase + G::kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
@@ -495,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 for (int c = 0; c < kChunksPerTile; ++c) {       // G1: 12 A chunks
                     mbar_wait(&B.a_full[as], ap);
                     tc_fence_after();
+                    DS_TRACE(5, tile, c);
                     gemm(sbase + G::kARing + as * kAChunk, 1, acc12, c > 0);
                     commit(&B.a_empty[as]);
                     if (++as == G::kAStages) { as = 0; ap ^= 1; }

@@ -27,13 +27,13 @@ def main():
     native.check(L.ds_synth_images_device(ctx.handle, 1, 0, n, 512, 512,
                                           native.c_p(img.data_ptr()), native.c_p(ctx.stream)))
     conf = torch.empty(n, dtype=torch.float32, device="cuda")
-    tr = torch.zeros(3 * 8 * 16, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(6 * 8 * 16, dtype=torch.int64, device="cuda")
     for _ in range(2):
         native.check(L.ds_disc_trace_device(disc.handle, native.c_p(img.data_ptr()), n, 512, 512,
                                             native.c_p(conf.data_ptr()), native.c_p(tr.data_ptr()),
                                             native.c_p(ctx.stream)))
     ctx.synchronize()
-    t = tr.cpu().numpy().reshape(3, 8, 16)
+    t = tr.cpu().numpy().reshape(6, 8, 16)
     base = t[2, 0, 0]
     names = {0: ["c0_start", "c11_stored"],
              1: ["E1_rdy", "E1_done", "E20_rdy", "E20_done", "E21_rdy", "E21_done", "E22_rdy",
@@ -48,6 +48,11 @@ def main():
                           for i, nm in enumerate(names[role]))
             print(f"  role{role}: {s}")
     print("per-tile cycles (MMA start deltas):", np.diff(t[2, :, 0]).tolist())
+    for tile in (5, 6):
+        print(f"tile {tile} per-chunk: a_empty_ok / a_full_arrive / mma_a_full_seen")
+        for c in range(12):
+            print(f"  c{c:2d}: {int(t[3, tile, c] - base):8d} {int(t[4, tile, c] - base):8d} "
+                  f"{int(t[5, tile, c] - base):8d}")
 
 
 if __name__ == "__main__":
