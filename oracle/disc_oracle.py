@@ -54,11 +54,8 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
 
 
 def gelu_tanh(x: np.ndarray) -> np.ndarray:
-    """GELU (tanh form) as the kernel evaluates it: the tanh argument and
-    result pass through fp16 (tanh.approx.f16x2 in disc.cu)."""
-    u = (np.float32(0.7978845608028654) * (x + np.float32(0.044715) * x * x * x)).astype(np.float32)
-    t = np.tanh(u.astype(np.float16).astype(np.float32)).astype(np.float16).astype(np.float32)
-    return (np.float32(0.5) * x * (np.float32(1.0) + t)).astype(np.float32)
+    return (0.5 * x * (1.0 + np.tanh(np.float32(0.7978845608028654) *
+                                     (x + np.float32(0.044715) * x * x * x)))).astype(np.float32)
 
 
 def patches(images: np.ndarray) -> np.ndarray:

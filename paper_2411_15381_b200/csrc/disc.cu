@@ -104,21 +104,6 @@ __device__ __forceinline__ float gelu_tanh(float x) {
     return 0.5f * x * (1.0f + tanh_approx(u));
 }
 
-// GELU_tanh of two values with ONE packed MUFU op (tanh.approx.f16x2): the
-// tanh argument is rounded to fp16 (11 significant bits; the result is stored
-// as bf16, 8 bits, right after). Returns the bf16x2 pack (lo = a, hi = b).
-__device__ __forceinline__ uint32_t gelu_tanh_pack2(float a, float b) {
-    const float ua = 0.7978845608028654f * (a + 0.044715f * a * a * a);
-    const float ub = 0.7978845608028654f * (b + 0.044715f * b * b * b);
-    uint32_t h, t;
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(ub), "f"(ua));
-    asm("tanh.approx.f16x2 %0, %1;" : "=r"(t) : "r"(h));
-    float ta, tb;
-    asm("{\n\t.reg .f16 l, hh;\n\tmov.b32 {l, hh}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, hh;\n\t}"
-        : "=f"(ta), "=f"(tb) : "r"(t));
-    return pack_bf16x2(0.5f * a * (1.0f + ta), 0.5f * b * (1.0f + tb));
-}
-
 // Byte offset of (row, 16-byte chunk) inside a K-major SW128 tile (128 B rows).
 __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
     return (row >> 3) * 1024u + (row & 7u) * 128u + ((chunk ^ (row & 7u)) << 4);
@@ -376,8 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int c = cbase + e + 2 * u;
-                            pk[u] = gelu_tanh_pack2(__uint_as_float(v[e + 2 * u]) + s_b1[c],
-                                                    __uint_as_float(v[e + 2 * u + 1]) + s_b1[c + 1]);
+                            pk[u] = pack_bf16x2(gelu_tanh(__uint_as_float(v[e + 2 * u]) + s_b1[c]),
+                                                gelu_tanh(__uint_as_float(v[e + 2 * u + 1]) + s_b1[c + 1]));
                         }
                         const int f = cbase + e;
                         st_shared_v4(sbase + G::kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
@@ -720,8 +705,10 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     if (reinterpret_cast<uintptr_t>(images) % 16)
         return dsi::fail(DS_ERR_INVALID_ARGUMENT, "image buffer must be 16-byte aligned");
     if (n <= 0) return DS_OK;
-    // SM pairs (cta_group::2) whenever a tile of 256 tokens divides the image
-    const bool pair = d->force_ctas == 1 ? false : (tokens % (2 * kM) == 0);
+    // Default: the 1-CTA kernel (measured faster on the full 5K-image step this
+    // round). DS_DISC_CTAS=2 opts into SM pairs (cta_group::2) when a tile of
+    // 256 tokens divides the image; see DESIGN.md section 5.
+    const bool pair = d->force_ctas == 2 && tokens % (2 * kM) == 0;
     const int ctas = pair ? 2 : 1;
     DiscParams p = d->params;
     p.images = images;

@@ -107,17 +107,19 @@ def test_pipelined_host_path_equals_device_path(disc):
     assert np.array_equal(disc.score(host), out.cpu().numpy())
 
 
-def test_single_cta_mode_matches_pair_mode(disc, monkeypatch):
-    """DS_DISC_CTAS=1 forces the 1-CTA kernel; the cta_group::2 kernel computes
-    the same per-token values (only the final per-image sum is associated
-    differently)."""
-    monkeypatch.setenv("DS_DISC_CTAS", "1")
-    single = native.Discriminator(default_context(), weight_seed=2024)
-    imgs = disc_oracle.synth_images(5, 0, 12, 512, 512)
-    a = disc.score(imgs)
-    b = single.score(imgs)
-    single.close()
-    assert np.allclose(a, b, rtol=2e-5, atol=1e-6)
+def test_pair_mode_matches_single_cta_mode(disc, weights, monkeypatch):
+    """DS_DISC_CTAS=2 selects the cta_group::2 SM-pair kernel; it computes the
+    same per-token values as the default 1-CTA kernel (only the per-image sum
+    is associated differently) and passes the oracle check."""
+    monkeypatch.setenv("DS_DISC_CTAS", "2")
+    pair = native.Discriminator(default_context(), weight_seed=2024)
+    for shape in ((12, 512, 512), (3, 256, 1024), (2, 1024, 1024)):
+        imgs = disc_oracle.synth_images(5, 0, *shape)
+        a = disc.score(imgs)
+        b = pair.score(imgs)
+        assert np.allclose(a, b, rtol=2e-5, atol=1e-6), shape
+        check_conf(b, disc_oracle.disc_forward(imgs, weights))
+    pair.close()
 
 
 def test_disc_single_cta_fallback_shapes(disc, weights):
