@@ -671,13 +671,9 @@ namespace {
 template <bool kPair>
 ds_status launch_mode(ds_disc* d, const DiscParams& p, int units, cudaStream_t st) {
     using G = Geo<kPair>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel<kPair>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         G::kSmemBytes));
-        attr_set = true;
-    }
+    // per device (one ds_ctx per GPU in a process): cheap, so set every launch
+    DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel<kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     G::kSmemBytes));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(units * G::kCtas));
     cfg.blockDim = dim3(kThreads);
