@@ -153,6 +153,12 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     const long long nunits = kPair ? nclusters_x() : gridDim.x;
 
     if (sbase & 1023u) __trap();   // SW128 operand tiles need 1024-byte alignment
+    if (P.trace && threadIdx.x == 0) {   // debug: per-CTA start time and SM id
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        P.trace[6 * kTraceTiles * 16 + 3 * blockIdx.x] = static_cast<long long>(globaltimer());
+        P.trace[6 * kTraceTiles * 16 + 3 * blockIdx.x + 2] = smid;
+    }
     if (threadIdx.x < kD1) {
         s_b1[threadIdx.x] = P.b1[threadIdx.x];
         s_hw[threadIdx.x] = P.hw[threadIdx.x];
@@ -543,6 +549,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     }
     tc_fence_before();
     __syncthreads();
+    if (P.trace && threadIdx.x == 0)
+        P.trace[6 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
     if constexpr (kPair) cluster_sync();     // both CTAs done with TMEM / remote barriers
     if (warp == 13) {
         tc_fence_after();
