@@ -291,9 +291,26 @@ def run_gpu(args):
     from paper_2411_15381_b200 import dist as ddist
 
     ws, rank, local = dist_env()
+    # Test hooks for the multi-rank path on a 1-GPU box: BENCH_DIST_BACKEND=gloo
+    # and BENCH_SHARE_DEVICE=1 run every rank on cuda:0 (the driver uses NCCL,
+    # one rank per GPU).
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if os.environ.get("BENCH_SHARE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    def allmax(vals):
+        """Max over ranks (the contract: timings are the max over ranks)."""
+        t = torch.tensor(vals, dtype=torch.float64)
+        if ws > 1:
+            t = t if backend == "gloo" else t.to(dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t.cpu()]
+
     ctx = native.Context(local)
     L = native.lib()
     stream = torch.cuda.ExternalStream(ctx.stream)
@@ -369,10 +386,7 @@ def run_gpu(args):
     clocks = sampler.stop()
     total_ms = t_start.elapsed_time(t_end)
     disc_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    t = torch.tensor([total_ms, disc_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, disc_ms = float(t[0]), float(t[1])
+    total_ms, disc_ms = allmax([total_ms, disc_ms])
     ms_per_step = total_ms / args.steps
     value = ws * N_IMG / (ms_per_step / 1000.0)
 
@@ -404,10 +418,7 @@ def run_gpu(args):
         c, cnts = e2e_step()
         d2h = c.nbytes + int(cnts.sum()) * 8 + cnts.nbytes + abi.CURVE.itemsize
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(e, op=dist.ReduceOp.MAX)
-    e2e_value = ws * N_IMG / float(e[0])
+    e2e_value = ws * N_IMG / allmax([e2e_s])[0]
     h2d = N_IMG * H * W * 3 + grid_np.nbytes + 2 * abi.CURVE.itemsize
 
     # ---- planner leg (config 4) -------------------------------------------------
@@ -436,10 +447,7 @@ def run_gpu(args):
     p1.record(stream)
     torch.cuda.synchronize()
     plan_ms = p0.elapsed_time(p1) / args.steps
-    pt = torch.tensor([plan_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(pt, op=dist.ReduceOp.MAX)
-    plan_ms = float(pt[0])
+    plan_ms = allmax([plan_ms])[0]
     plan_value = ws * len(pro) * CANDS_PER_PROBLEM / (plan_ms / 1000.0)
     gpu_plans = d_out.cpu().numpy().view(abi.PLAN)
     # planner e2e through the host-buffer C-ABI call
@@ -447,7 +455,7 @@ def run_gpu(args):
     t0 = time.perf_counter()
     for _ in range(3):
         ctx.plan_batch(pro, cas, grid, offs)
-    plan_e2e = ws * len(pro) * CANDS_PER_PROBLEM / ((time.perf_counter() - t0) / 3)
+    plan_e2e = ws * len(pro) * CANDS_PER_PROBLEM / allmax([(time.perf_counter() - t0) / 3])[0]
 
     # ---- latent leg (config 5: 1M queries per GPU, reference-parity scorer) ------
     lconf = torch.empty(N_LATENT, dtype=torch.float64, device=dev)
@@ -485,10 +493,7 @@ def run_gpu(args):
     latent_step(ev=True)
     torch.cuda.synchronize()
     lat_ms = [levs[i].elapsed_time(levs[i + 1]) for i in range(3)]
-    lt = torch.tensor([sum(lat_ms)], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(lt, op=dist.ReduceOp.MAX)
-    latent_value = ws * N_LATENT / (float(lt[0]) / 1000.0)
+    latent_value = ws * N_LATENT / (allmax([sum(lat_ms)])[0] / 1000.0)
 
     if rank == 0:
         peaks, peak_src = load_peaks()

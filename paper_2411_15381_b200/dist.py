@@ -37,6 +37,11 @@ def gather_counts(counts, group=None):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    if dist.get_backend(group) == "gloo" and counts.is_cuda:
+        # gloo test path: gather through host memory
+        parts = [torch.empty_like(counts, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, counts.cpu(), group=group)
+        return torch.stack(parts).to(counts.device)
     out = torch.empty(world * counts.numel(), dtype=counts.dtype, device=counts.device)
     dist.all_gather_into_tensor(out, counts.contiguous(), group=group)
     return out.view(world, counts.numel())
