@@ -32,6 +32,7 @@
 // (packed bf16 values stay in registers) and stores H2_j only after the GEMM3
 // still reading the previous H2 chunk committed, so G2_{j+1} overlaps E2_j and
 // G3_3(i-1) overlaps E1(i).
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -67,8 +68,14 @@ struct Geo {
     static constexpr int kCtas = kPair ? 2 : 1;
     static constexpr int kTokPerTile = kM * kCtas;
     static constexpr int kBHalf = kBStage / kCtas;            // bytes of a stage per CTA
-    static constexpr int kAStages = 2;
-    static constexpr int kBStages = kPair ? 8 : 4;
+#ifndef DS_A_STAGES_1CTA
+#define DS_A_STAGES_1CTA 2
+#endif
+#ifndef DS_B_STAGES_1CTA
+#define DS_B_STAGES_1CTA 4
+#endif
+    static constexpr int kAStages = kPair ? 2 : DS_A_STAGES_1CTA;
+    static constexpr int kBStages = kPair ? 8 : DS_B_STAGES_1CTA;
     static constexpr int kR1 = 0;                             // H1: 4 K-chunks x 16 KB
     static constexpr int kR2 = kR1 + 65536;                   // H2_j: 4 K-chunks x 16 KB
     static constexpr int kARing = kR2 + 65536;
@@ -82,6 +89,7 @@ struct Geo {
 };
 
 struct DiscParams {
+    CUtensorMap wmap;   // the weight blob as [88*256 rows x 32 bf16] (pair mode TMA)
     float b1[kD1];
     float hw[kD3];
     const uint8_t* images;
@@ -131,7 +139,7 @@ __device__ __forceinline__ void u8x16_to_bf16(const uint4 v, uint32_t (&o)[8]) {
 }
 
 struct Bars {
-    uint64_t a_full[2], a_empty[2], b_full[8], b_empty[8];
+    uint64_t a_full[4], a_empty[4], b_full[8], b_empty[8];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
     uint32_t tmem_base;
     float warp_part[2][8];
@@ -156,8 +164,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     if (P.trace && threadIdx.x == 0) {   // debug: per-CTA start time and SM id
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        P.trace[6 * kTraceTiles * 16 + 3 * blockIdx.x] = static_cast<long long>(globaltimer());
-        P.trace[6 * kTraceTiles * 16 + 3 * blockIdx.x + 2] = smid;
+        P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x] = static_cast<long long>(globaltimer());
+        P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 2] = smid;
     }
     if (threadIdx.x < kD1) {
         s_b1[threadIdx.x] = P.b1[threadIdx.x];
@@ -170,8 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             mbar_init(&B.a_full[s], 128 + peer);
             mbar_init(&B.a_empty[s], 1);
         }
-        for (int s = 0; s < G::kBStages; ++s) {
-            mbar_init(&B.b_full[s], 1 + peer);
+        for (int s = 0; s < G::kBStages; ++s) {   // leader expects both halves' bytes
+            mbar_init(&B.b_full[s], 1);
             mbar_init(&B.b_empty[s], 1);
         }
         mbar_init(&B.acc12_full, 1);
@@ -429,18 +437,31 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             const uint64_t policy = policy_evict_last();
             int bs = 0;
             uint32_t bp = 0;
+            long long ptile = 0;   // trace only
+            if constexpr (kPair) prefetch_tmap(&P.wmap);
             auto put = [&](int first, int count) {
                 for (int t = first; t < first + count; ++t) {
                     mbar_wait(&B.b_empty[bs], bp ^ 1);
-                    mbar_arrive_expect_tx(&B.b_full[bs], G::kBHalf);
-                    bulk_g2s_hint(smem + G::kBRing + bs * G::kBHalf,
-                                  P.wblob + static_cast<size_t>(t) * kBStage + rank * G::kBHalf,
-                                  G::kBHalf, &B.b_full[bs], policy);
+                    if (t < 16) DS_TRACE(6, ptile, t);
+                    if constexpr (kPair) {
+                        // both CTAs load their N-half; completion lands on the leader's
+                        // barrier, which expects the whole 16 KB stage
+                        const uint32_t lbar = mapa_shared(smem_u32(&B.b_full[bs]), 0);
+                        if (leader) mbar_arrive_expect_tx(&B.b_full[bs], kBStage);
+                        tma_2d_pair(sbase + G::kBRing + bs * G::kBHalf, &P.wmap, 0,
+                                    t * 256 + static_cast<int>(rank) * 128, lbar, policy);
+                    } else {
+                        mbar_arrive_expect_tx(&B.b_full[bs], G::kBHalf);
+                        bulk_g2s_hint(smem + G::kBRing + bs * G::kBHalf,
+                                      P.wblob + static_cast<size_t>(t) * kBStage, G::kBHalf,
+                                      &B.b_full[bs], policy);
+                    }
                     if (++bs == G::kBStages) { bs = 0; bp ^= 1; }
                 }
             };
             const int W1 = 0, W2 = kW1Stages, W3 = kW1Stages + 4 * kWChunkStages;
             for (long long tile = 0; tile < my_tiles; ++tile) {
+                ptile = tile;
                 put(W1, kW1Stages);
                 if (tile > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
                 put(W2, kWChunkStages);
@@ -451,24 +472,13 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             }
             if (my_tiles > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
         }
-    } else if (kPair && !leader) {
-        // ===================== peer: relay weight-stage arrivals ==============
-        // (88 stages per tile; the leader's b_full counts this arrival)
-        if (lane == 0) {
-            const long long total = my_tiles * kBlobStages;
-            int bs = 0;
-            uint32_t bp = 0;
-            for (long long k = 0; k < total; ++k) {
-                mbar_wait(&B.b_full[bs], bp);
-                mbar_arrive_cluster(mapa_shared(smem_u32(&B.b_full[bs]), 0));
-                if (++bs == G::kBStages) { bs = 0; bp ^= 1; }
-            }
-        }
     } else {
         // ===================== MMA issuer (leader warp 13, one thread) ========
-        if (lane == 0) {
+        if (lane == 0 && leader) {
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0, pdr = 0, prd = 0, pe3 = 0;
+            long long trace_tile = 0;   // trace only
+            int trace_stage = 0;
             const uint32_t acc12 = tmem, acc3 = tmem + 256;
             auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
                 if constexpr (kPair) umma_bf16_pair(d, a, b, G::kIdesc, acc);
@@ -483,6 +493,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     for (int hf = 0; hf < 2; ++hf) {
                         mbar_wait(&B.b_full[bs], bp);
                         tc_fence_after();
+                        if (trace_stage < 16) DS_TRACE(7, trace_tile, trace_stage);
+                        ++trace_stage;
                         const uint64_t bd = desc_k_sw64(sbase + G::kBRing + bs * G::kBHalf);
 #pragma unroll
                         for (int k = 0; k < 2; ++k)
@@ -500,6 +512,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             };
             for (long long tile = 0; tile < my_tiles; ++tile) {
                 DS_TRACE(2, tile, 0);
+                trace_tile = tile;
+                trace_stage = 0;
                 for (int c = 0; c < kChunksPerTile; ++c) {       // G1: 12 A chunks
                     mbar_wait(&B.a_full[as], ap);
                     tc_fence_after();
@@ -550,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     tc_fence_before();
     __syncthreads();
     if (P.trace && threadIdx.x == 0)
-        P.trace[6 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
+        P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
     if constexpr (kPair) cluster_sync();     // both CTAs done with TMEM / remote barriers
     if (warp == 13) {
         tc_fence_after();
@@ -663,6 +677,32 @@ __global__ void fold_bias_kernel(const uint16_t* w1, uint64_t seed, float* b1) {
 
 } // namespace
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static ds_status make_weight_tmap(const void* blob, CUtensorMap* out) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    DS_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+        return dsi::fail(DS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    // [rows = 88 stages x 256][32 bf16] row-major (64-byte rows); a box of
+    // 128 rows x 32 copies one pre-swizzled N-half of a stage byte for byte.
+    const cuuint64_t dims[2] = {32, static_cast<cuuint64_t>(kBlobStages) * 256};
+    const cuuint64_t strides[1] = {64};
+    const cuuint32_t box[2] = {32, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = reinterpret_cast<EncodeFn>(fn)(
+        out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(blob), dims, strides, box,
+        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return dsi::fail(DS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return DS_OK;
+}
+
 struct ds_disc {
     ds_ctx* ctx = nullptr;
     uint64_t seed = 0;
@@ -773,6 +813,10 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
     fold_bias_kernel<<<1, 256, 0, st>>>(w1, weight_seed, d->d_b1);
     ctx->launches.fetch_add(3);
     if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "weight init"));
+    {
+        const ds_status ts = make_weight_tmap(d->d_blob, &d->params.wmap);
+        if (ts != DS_OK) return cleanup(ts);
+    }
     if ((e = cudaMemcpyAsync(d->params.b1, d->d_b1, sizeof(d->params.b1), cudaMemcpyDeviceToHost,
                              st)) != cudaSuccess)
         return cleanup(dsi::cuda_fail(e, "copy b1"));

@@ -260,6 +260,23 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
+// 2-D tensor TMA of one box into this CTA's smem whose completion (tx bytes)
+// is signalled on the PAIR LEADER's mbarrier (cta_group::2). `tmap` is the
+// generic address of a __grid_constant__ CUtensorMap; `leader_bar` a
+// shared::cluster address (mapa to rank 0).
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst_smem, const void* tmap, int32_t x,
+                                            int32_t y, uint32_t leader_bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst_smem),
+        "l"(tmap), "r"(leader_bar), "r"(x), "r"(y), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
 // ---- misc ---------------------------------------------------------------------------
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");

@@ -27,15 +27,15 @@ def main():
     native.check(L.ds_synth_images_device(ctx.handle, 1, 0, n, 512, 512,
                                           native.c_p(img.data_ptr()), native.c_p(ctx.stream)))
     conf = torch.empty(n, dtype=torch.float32, device="cuda")
-    tr = torch.zeros(6 * 8 * 16 + 3 * 160, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(8 * 8 * 16 + 3 * 160, dtype=torch.int64, device="cuda")
     for _ in range(2):
         native.check(L.ds_disc_trace_device(disc.handle, native.c_p(img.data_ptr()), n, 512, 512,
                                             native.c_p(conf.data_ptr()), native.c_p(tr.data_ptr()),
                                             native.c_p(ctx.stream)))
     ctx.synchronize()
     tall = tr.cpu().numpy()
-    t = tall[:6 * 8 * 16].reshape(6, 8, 16)
-    cta = tall[6 * 8 * 16:].reshape(160, 3)
+    t = tall[:8 * 8 * 16].reshape(8, 8, 16)
+    cta = tall[8 * 8 * 16:].reshape(160, 3)
     base = t[2, 0, 0]
     names = {0: ["c0_start", "c11_stored"],
              1: ["E1_rdy", "E1_done", "E20_rdy", "E20_done", "E21_rdy", "E21_done", "E22_rdy",
@@ -57,7 +57,12 @@ def main():
           f"min {dur.min():.0f} median {np.median(dur):.0f} max {dur.max():.0f}")
     order = np.argsort(-dur)[:6]
     print("slowest CTAs (bid, smid, us):", [(int(i), int(cta[i, 2]), round(float(dur[i]))) for i in order])
-    for tile in (5, 6):
+    for tile in (6,):
+        print(f"tile {tile} weight stages: producer issue / MMA b_full seen / latency")
+        for k in range(16):
+            print(f"  s{k:2d}: {int(t[6, tile, k] - base):8d} {int(t[7, tile, k] - base):8d} "
+                  f"{int(t[7, tile, k] - t[6, tile, k]):6d}")
+    for tile in (6,):
         print(f"tile {tile} per-chunk: a_empty_ok / a_full_arrive / mma_a_full_seen")
         for c in range(12):
             print(f"  c{c:2d}: {int(t[3, tile, c] - base):8d} {int(t[4, tile, c] - base):8d} "
