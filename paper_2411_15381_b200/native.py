@@ -19,7 +19,7 @@ import numpy as np
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("DS_B200_LIB") or os.path.join(HERE, "_lib", "libds_b200.so")
+LIB_PATH = os.path.join(HERE, "_lib", "libds_b200.so")
 
 
 class DsError(RuntimeError):
