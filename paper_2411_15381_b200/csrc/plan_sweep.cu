@@ -9,11 +9,13 @@
 //      deferral curve (profiles.cpp:98-106 -- built in the reference's summation
 //      order, so f(t) is bit-identical);
 //   2. thresholds walked from the top in chunks of kTChunk: x2[t][b2] for the
-//      chunk, then ONE CANDIDATE (t, b1, b2) PER THREAD ITERATION scored as a
-//      packed u64 key whose unsigned order is the reference's selection order
-//      ("first feasible t from the top", then Candidate::better_than,
+//      chunk, then each thread takes (b1, b2) pairs and decides that pair's
+//      (t, b1, b2) candidates from the top t down, scoring each as a packed
+//      u64 key whose unsigned order is the reference's selection order ("first
+//      feasible t from the top", then Candidate::better_than,
 //      allocator.cpp:57-67):
 //          (G-1-t_idx)<<40 | (x1+x2)<<28 | (255-b1_idx)<<20 | (255-b2_idx)<<12 | x1
+//      (a pair's first valid t is its minimum key, so its walk stops there);
 //   3. warp-shuffle min, then a block min over 8 warps; the first chunk with a
 //      finite key holds the global minimum, so the walk stops there (the
 //      reference's early exit, allocator.cpp:118).
@@ -133,21 +135,27 @@ __device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int
             s.x2[tl * kMaxB + j] = min_servers(s.ft[tl], s.T2[j], S);
         }
         __syncthreads();
+        // Each thread owns fixed (b1, b2) pairs -- the latency and x1 checks
+        // are per pair -- and walks the chunk's thresholds from the top; the
+        // first valid t is the pair's best (larger t = smaller key), so the
+        // walk stops there. Every (t, b1, b2) candidate of the chunk is still
+        // decided (reference semantics); only provably worse keys are skipped.
         unsigned long long mine = kNone;
-        const int total_cands = cnt * ni * nj;
-        for (int k = threadIdx.x; k < total_cands; k += kThreads) {
-            const int j = j0 + k % nj;
-            const int r = k / nj;
-            const int i = i0 + r % ni;
-            const int tl = r / ni;
+        for (int pr = threadIdx.x; pr < ni * nj; pr += kThreads) {
+            const int i = i0 + pr / nj, j = j0 + pr % nj;
             if (!((s.lat[i] >> j) & 1ull)) continue;
             const int x1 = s.x1[i];
             if (x1 > S) continue;
-            const int x2 = s.x2[tl * kMaxB + j];
-            if (x1 + x2 > S) continue;
-            const unsigned long long key =
-                (static_cast<unsigned long long>(G - 1 - (lo + tl)) << 40) | tie_key(x1, x2, i, j);
-            mine = key < mine ? key : mine;
+            const unsigned long long tie_lo = tie_key(x1, 0, i, j);   // x2 added below
+            for (int tl = cnt - 1; tl >= 0; --tl) {
+                const int x2 = s.x2[tl * kMaxB + j];
+                if (x1 + x2 > S) continue;
+                const unsigned long long key =
+                    (static_cast<unsigned long long>(G - 1 - (lo + tl)) << 40) +
+                    (static_cast<unsigned long long>(x2) << 28) + tie_lo;
+                mine = key < mine ? key : mine;
+                break;
+            }
         }
         best = block_min(mine, parity ? s.red2 : s.red);
         parity ^= 1;
