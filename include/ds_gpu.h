@@ -17,6 +17,10 @@
  *                                     proj/src/policies.cpp:37-39)
  *   curve    : ds_curve_observe*     replaces diffserve::observe_confidence
  *                                    (reference proj/src/profiles.cpp:108-120)
+ *   workload : ds_generate_arrivals* replaces diffserve::generate_arrivals
+ *                                    (reference proj/src/workload.cpp:82-106)
+ *              ds_sample_queries*    replaces the sample_query loop of
+ *                                    run_experiment (experiment.cpp:76-79)
  *
  * Functions without the _device suffix take HOST buffers and copy in/out
  * inside the call (the reference-facing drop-in). The _device variants take
@@ -190,6 +194,49 @@ ds_status ds_curve_observe(ds_ctx* ctx, ds_curve* curve, const void* conf, int32
                            int64_t n, double decay);
 ds_status ds_curve_observe_device(ds_ctx* ctx, ds_curve* curve, const void* conf,
                                   int32_t dtype, int64_t n, double decay, void* stream);
+
+/* ---- workload synthesis (K8 arrivals, K4 query records) --------------- */
+/* ArrivalMode (workload.hpp:26). */
+typedef enum {
+    DS_ARRIVALS_POISSON = 0,
+    DS_ARRIVALS_UNIFORM = 1
+} ds_arrival_mode;
+
+/* Query (workload.hpp:39-46), 48 bytes. */
+typedef struct {
+    uint64_t id;
+    double arrival;
+    double deadline;
+    double quality_light;
+    double quality_heavy;
+    double confidence;
+} ds_query;
+
+/* generate_arrivals(Trace{interval_seconds, rates[0..n_rates)}, seed, mode)
+ * (workload.cpp:82-106): bit-identical timestamps. *count receives the number
+ * of arrivals. arrivals may be NULL (count only); otherwise it must hold
+ * *count entries, else DS_ERR_CAPACITY (with *count set). Rates must be
+ * finite and >= 0 and interval_seconds > 0 (what load_trace admits,
+ * workload.cpp:21-22,44-45), else DS_ERR_DOMAIN. */
+ds_status ds_generate_arrivals(ds_ctx* ctx, const double* rates, int32_t n_rates,
+                               double interval_seconds, uint64_t seed, int32_t mode,
+                               double* arrivals, int64_t capacity, int64_t* count);
+/* Same with arrivals on the device (rates and count stay host memory). The
+ * output length is data-dependent, so this call synchronizes its stream once
+ * to read the count; the copy into arrivals is stream-ordered after it. */
+ds_status ds_generate_arrivals_device(ds_ctx* ctx, const double* rates, int32_t n_rates,
+                                      double interval_seconds, uint64_t seed, int32_t mode,
+                                      double* arrivals, int64_t capacity, int64_t* count,
+                                      void* stream);
+/* out[i] = sample_query(model, id0 + i, arrivals[i], slo_seconds)
+ * (workload.cpp:108-129): the Query records run_experiment builds
+ * (experiment.cpp:76-79) with ids id0.. in arrival order. */
+ds_status ds_sample_queries(ds_ctx* ctx, const ds_query_model* model, uint64_t id0,
+                            const double* arrivals, int64_t n, double slo_seconds,
+                            ds_query* out);
+ds_status ds_sample_queries_device(ds_ctx* ctx, const ds_query_model* model, uint64_t id0,
+                                   const double* arrivals, int64_t n, double slo_seconds,
+                                   ds_query* out, void* stream);
 
 /* ---- discriminator (K5-K7: ingest + fused tcgen05 MLP + head) --------- */
 /* PatchDisc: u8 NHWC image -> 16x16 patches -> 768->256 GELU -> 256->1024

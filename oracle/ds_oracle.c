@@ -147,6 +147,39 @@ int dso_sample_queries(const ds_query_model* m, uint64_t id0, int64_t n, double*
 }
 
 /* ---------------------------------------------------------------------- */
+/* Workload synthesis: workload.cpp:82-106                                 */
+
+/* generate_arrivals on Trace{dt, rates[0..n)}: returns the count and writes
+ * min(count, cap) timestamps. mode 0 = poisson, 1 = uniform. The Exp(1)
+ * draws are RandomStream::exponential(1.0) = -log1p(-U) / 1.0 through the
+ * host libm, as in the reference (rng.cpp:24-28). */
+int64_t dso_generate_arrivals(const double* rates, int32_t n, double dt, uint64_t seed,
+                              int32_t mode, double* out, int64_t cap) {
+    dso_mt64 g;
+    stream_init(&g, seed, "arrivals");
+    const double duration = dt * (double)n;
+    double target = mode == 1 ? 0.0 : -log1p(-stream_uniform(&g)) / 1.0;
+    double cum = 0.0, last = 0.0;
+    int64_t c = 0;
+    for (int32_t k = 0; k < n; ++k) {
+        double rate = rates[k];
+        double start = dt * (double)k;
+        double cum_end = cum + rate * dt;
+        while (rate > 0.0 && target < cum_end - 1e-12) {
+            double t = start + (target - cum) / rate;
+            if (c > 0 && t <= last) t = nextafter(last, INFINITY);
+            if (t >= duration) break;
+            if (c < cap) out[c] = t;
+            last = t;
+            ++c;
+            target += mode == 1 ? 1.0 : -log1p(-stream_uniform(&g)) / 1.0;
+        }
+        cum = cum_end;
+    }
+    return c;
+}
+
+/* ---------------------------------------------------------------------- */
 /* Deferral curve: profiles.cpp:60-71, 75-120                              */
 
 static int bin_of(double c) { /* profiles.cpp:60-65 */

@@ -65,6 +65,9 @@ def ref():
         lib.dsref_load_cascade.argtypes = [ctypes.c_char_p, ctypes.c_char_p, c_p]
         lib.dsref_splitmix64.argtypes = [u64]
         lib.dsref_splitmix64.restype = u64
+        lib.dsref_generate_arrivals.argtypes = [c_p, i32, f64, u64, i32, c_p, i64]
+        lib.dsref_generate_arrivals.restype = i64
+        lib.dsref_sample_query_records.argtypes = [c_p, u64, c_p, i64, f64, c_p]
         lib.dsref_hash_name.argtypes = [ctypes.c_char_p]
         lib.dsref_hash_name.restype = u64
         lib.dsref_stream_raw.argtypes = [u64, ctypes.c_char_p, ctypes.c_int, c_p]
@@ -88,6 +91,8 @@ def port():
         lib.dso_hash_name.restype = u64
         lib.dso_stream_raw.argtypes = [u64, ctypes.c_char_p, ctypes.c_int, c_p]
         lib.dso_sample_query.argtypes = [c_p, u64, c_p, c_p]
+        lib.dso_generate_arrivals.argtypes = [c_p, i32, f64, u64, i32, c_p, i64]
+        lib.dso_generate_arrivals.restype = i64
         lib.dso_sample_queries.argtypes = [c_p, u64, i64, c_p, c_p, ctypes.c_int]
         lib.dso_bin_of.argtypes = [f64]
         lib.dso_bins_below.argtypes = [f64]

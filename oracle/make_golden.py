@@ -316,6 +316,86 @@ def gen_des():
     np.savez_compressed(os.path.join(OUT, "des_inputs.npz"), **g)
 
 
+def arrival_cases():
+    """(name, rates, interval_seconds, seed, mode) for generate_arrivals goldens:
+    the reference's own unit/acceptance traces (test_workload.cpp:71-103,
+    acceptance_main.cpp:326-336), the shipped traces at the configs' seed, and
+    synthetic traces that stress zero-rate gaps, tiny rates, many interval
+    boundaries and ~1M arrivals."""
+    ref = "/root/reference/proj"
+    cases = [
+        ("unit_uniform_2", [2.0], 1.0, 0, 1),
+        ("unit_uniform_13", [1.0, 3.0], 1.0, 0, 1),
+        ("unit_zero", [0.0, 0.0], 1.0, 0, 1),
+        ("unit_poisson_42", [10.0] * 600, 1.0, 42, 0),
+        ("unit_poisson_43", [10.0] * 600, 1.0, 43, 0),
+    ]
+    for t, seed in (("trace_4to32qps", 1), ("trace_1to8qps", 1), ("trace_8to24qps", 1),
+                    ("trace_4to32qps", 7)):
+        with open(f"{ref}/traces/{t}.txt") as f:
+            rates = [float(x) for x in f.read().split()]
+        cases.append((f"{t}_s{seed}", rates, 1.0, seed, 0))
+        cases.append((f"{t}_s{seed}_uniform", rates, 1.0, seed, 1))
+    light = workloads.SHIPPED["cascade1"]["light"]
+    rate = 0.7 * 2 * (4 / light[4])                 # acceptance_main.cpp:329
+    cases.append(("accept_wait", [rate] * 3600, 1.0, 11, 0))
+    mixed = [0.0, 0.0, 5.0, 0.001, 0.0, 17.5, 300.0, 0.0, 1e-6, 42.0, 0.0]
+    cases.append(("mixed_poisson", mixed, 0.37, 7, 0))
+    cases.append(("mixed_uniform", mixed, 0.37, 7, 1))
+    rng = np.random.default_rng(9)
+    # rates on a 1/64 qps lattice (exact in binary, compresses well)
+    cases.append(("boundaries", list(rng.integers(0, 400 * 64, 30000) / 64.0), 0.01, 9, 0))
+    cases.append(("boundaries_uniform", list(rng.integers(0, 400 * 64, 8000) / 64.0), 0.013, 9,
+                  1))
+    cases.append(("dense_1m", [2500.0] * 400, 1.0, 3, 0))
+    cases.append(("dense_1m_uniform", [4999.5] * 200, 1.0, 3, 1))
+    return cases
+
+
+def gen_arrivals(full_limit=6000):
+    """generate_arrivals goldens from the reference (workload.cpp:82-106):
+    count, sha256 of the timestamp bytes, and the timestamps themselves for
+    small cases (head/tail/strided samples for large ones). Also the Query
+    records of the cascade-1 and cascade-3 runs (experiment.cpp:76-79)."""
+    import hashlib
+    r = lib.ref()
+    out = {}
+    names = []
+    for name, rates, dt, seed, mode in arrival_cases():
+        rates = np.asarray(rates, np.float64)
+        n = r.dsref_generate_arrivals(P(rates), len(rates), dt, seed, mode, None, 0)
+        a = np.zeros(max(n, 1), np.float64)
+        n2 = r.dsref_generate_arrivals(P(rates), len(rates), dt, seed, mode, P(a), len(a))
+        assert n == n2 >= 0, name
+        a = a[:n]
+        names.append(name)
+        out[f"{name}__rates"] = rates
+        out[f"{name}__meta"] = np.array([dt, seed, mode], np.float64)
+        out[f"{name}__count"] = np.int64(n)
+        out[f"{name}__sha256"] = np.array(hashlib.sha256(a.tobytes()).hexdigest())
+        if n <= full_limit:
+            out[f"{name}__arrivals"] = a
+        else:
+            idx = np.unique(np.concatenate([np.arange(512), np.arange(n - 512, n),
+                                            np.linspace(0, n - 1, 1024).astype(np.int64)]))
+            out[f"{name}__sample_idx"] = idx
+            out[f"{name}__sample"] = a[idx]
+    out["names"] = np.array(names)
+    for cname, tname in (("cascade3", "trace_1to8qps_s1"),):
+        m = np.zeros((), abi.QUERY_MODEL)
+        m["easy_fraction"], m["quality_gap_scale"] = 0.3, 1.0
+        m["confidence_fidelity"], m["noise_sigma"], m["seed"] = 0.35, 0.12, 1
+        slo = workloads.SHIPPED[cname]["slo"]
+        a = out.get(f"{tname}__arrivals")
+        q = np.zeros(len(a), abi.QUERY)
+        _check(r.dsref_sample_query_records(P(m.reshape(1)), 0, P(a), len(a), slo, P(q)),
+               "sample_query_records")
+        out[f"records_{cname}"] = q
+        out[f"records_{cname}_slo"] = np.float64(slo)
+    np.savez_compressed(os.path.join(OUT, "arrivals.npz"), **out)
+    return {n: int(out[f"{n}__count"]) for n in names}
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("alloc_random_2024: feasible", gen_alloc_random(), "of 60")
@@ -326,7 +406,12 @@ def main():
     print("latent: ok")
     gen_des()
     print("des: ok")
+    print("arrivals:", gen_arrivals())
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            print(name, globals()[f"gen_{name}"]())
+    else:
+        main()

@@ -358,6 +358,47 @@ void dsref_from_problem(const void* p, ds_problem* out) {
 }
 
 // RNG primitives (rng.cpp:8-36) for the oracle's own checks.
+// generate_arrivals (workload.cpp:82-106) on Trace{dt, rates}. Returns the
+// arrival count and copies min(count, cap) timestamps; -1 on an exception.
+int64_t dsref_generate_arrivals(const double* rates, int32_t n, double dt, uint64_t seed,
+                                int32_t mode, double* out, int64_t cap) {
+    try {
+        Trace t;
+        t.interval_seconds = dt;
+        t.rates.assign(rates, rates + n);
+        const auto a = generate_arrivals(t, seed, mode == 1 ? ArrivalMode::uniform
+                                                            : ArrivalMode::poisson);
+        const int64_t c = static_cast<int64_t>(a.size());
+        for (int64_t i = 0; i < c && i < cap; ++i) out[i] = a[i];
+        return c;
+    } catch (...) {
+        map_exception();
+        return -1;
+    }
+}
+
+// The run_experiment query loop (experiment.cpp:76-79) with ids id0.. :
+// full Query records.
+int dsref_sample_query_records(const ds_query_model* m, uint64_t id0, const double* arrivals,
+                               int64_t n, double slo, ds_query* out) {
+    QueryOutcomeModel qm;
+    qm.easy_fraction = m->easy_fraction;
+    qm.quality_gap_scale = m->quality_gap_scale;
+    qm.confidence_fidelity = m->confidence_fidelity;
+    qm.noise_sigma = m->noise_sigma;
+    qm.seed = m->seed;
+    try {
+        for (int64_t i = 0; i < n; ++i) {
+            const Query q = sample_query(qm, id0 + static_cast<uint64_t>(i), arrivals[i], slo);
+            out[i] = ds_query{q.id, q.arrival, q.deadline, q.quality_light, q.quality_heavy,
+                              q.confidence};
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 uint64_t dsref_splitmix64(uint64_t x) { return splitmix64(x); }
 uint64_t dsref_hash_name(const char* s) { return hash_name(s); }
 void dsref_stream_raw(uint64_t seed, const char* name, int k, uint64_t* out) {

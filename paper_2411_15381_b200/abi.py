@@ -38,6 +38,10 @@ QUEUING_TWICE_EXEC = 1
 CONF_F64 = 0
 CONF_F32 = 1
 
+# ds_arrival_mode (ArrivalMode, workload.hpp:26)
+ARRIVALS_POISSON = 0
+ARRIVALS_UNIFORM = 1
+
 MODEL_PROFILE = np.dtype(
     [("n", "<i4"), ("_pad", "<i4"), ("batch", "<i4", (MAX_BATCHES,)),
      ("latency", "<f8", (MAX_BATCHES,))], align=True)
@@ -58,12 +62,17 @@ QUERY_MODEL = np.dtype(
     [("easy_fraction", "<f8"), ("quality_gap_scale", "<f8"), ("confidence_fidelity", "<f8"),
      ("noise_sigma", "<f8"), ("seed", "<u8")], align=True)
 
+QUERY = np.dtype(
+    [("id", "<u8"), ("arrival", "<f8"), ("deadline", "<f8"), ("quality_light", "<f8"),
+     ("quality_heavy", "<f8"), ("confidence", "<f8")], align=True)
+
 assert MODEL_PROFILE.itemsize == 776
 assert CURVE.itemsize == 816
 assert CASCADE.itemsize == 2376
 assert PROBLEM.itemsize == 96
 assert PLAN.itemsize == 32
 assert QUERY_MODEL.itemsize == 40
+assert QUERY.itemsize == 48
 
 
 def ptr(a: np.ndarray | None) -> ctypes.c_void_p:

@@ -24,7 +24,8 @@ __all__ = ["ModelProfile", "DeferralCurve", "CascadeProfile", "QueueState", "All
            "solve_even_split", "solve_batch", "sample_query", "sample_queries",
            "observe_confidences", "route", "InvalidArgument", "DomainError", "InvariantError",
            "OutOfRange", "CapacityError", "default_context", "Policy", "make_policy",
-           "PolicyParams"]
+           "PolicyParams", "Trace", "POISSON", "UNIFORM", "generate_arrivals",
+           "sample_query_records"]
 
 _ctx: Context | None = None
 
@@ -222,6 +223,40 @@ def sample_query(model: QueryOutcomeModel, id: int, arrival_time: float,
         raise DomainError("slo_seconds must be positive")
     conf, ql = sample_queries(model, 1, id)
     return Query(id, arrival_time, arrival_time + slo_seconds, float(ql[0]), 1.0, float(conf[0]))
+
+
+@dataclass
+class Trace:                              # workload.hpp:10-16
+    interval_seconds: float = 1.0
+    rates: list = None
+
+    def duration(self) -> float:
+        return self.interval_seconds * float(len(self.rates or []))
+
+    def peak(self) -> float:
+        return max(self.rates) if self.rates else 0.0
+
+
+POISSON = "poisson"                       # ArrivalMode, workload.hpp:26
+UNIFORM = "uniform"
+
+
+def generate_arrivals(trace: Trace, seed: int, mode: str = POISSON,
+                      ctx: Context | None = None) -> np.ndarray:
+    """generate_arrivals (workload.cpp:82-106) on the GPU (K8), bit-identical."""
+    if mode not in (POISSON, UNIFORM):
+        raise ValueError(f"unknown arrival mode '{mode}'")
+    m = abi.ARRIVALS_UNIFORM if mode == UNIFORM else abi.ARRIVALS_POISSON
+    return (ctx or default_context()).generate_arrivals(trace.rates or [], trace.interval_seconds,
+                                                        seed, m)
+
+
+def sample_query_records(model: QueryOutcomeModel, arrivals, slo_seconds: float, id0: int = 0,
+                         ctx: Context | None = None) -> np.ndarray:
+    """The run_experiment query loop (experiment.cpp:76-79): Query records
+    (abi.QUERY) for ids id0.. at the given arrivals, on the GPU (K4)."""
+    return (ctx or default_context()).sample_query_records(model.pod(), arrivals, slo_seconds,
+                                                           id0)
 
 
 def observe_confidences(curve: DeferralCurve, conf, decay: float) -> DeferralCurve:

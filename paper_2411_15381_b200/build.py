@@ -22,11 +22,11 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
           f"-I{ROOT}/include", f"-I{CSRC}", "--expt-relaxed-constexpr"]
-EXACT_FP64 = {"plan_sweep.cu", "latent.cu", "curve.cu", "route.cu"}
+EXACT_FP64 = {"plan_sweep.cu", "latent.cu", "curve.cu", "route.cu", "arrivals.cu"}
 
 SOURCES = ["ds_ctx.cu", "plan_sweep.cu", "latent.cu", "route.cu", "curve.cu", "disc.cu",
-           "synth.cu"]
-HEADERS = ["ds_internal.h", "sm100.cuh"]
+           "synth.cu", "arrivals.cu"]
+HEADERS = ["ds_internal.h", "sm100.cuh", "fdlibm_log1p.h"]
 
 
 def _mtime(p: str) -> float:

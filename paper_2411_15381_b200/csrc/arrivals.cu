@@ -1,0 +1,561 @@
+// K8 arrivals: diffserve::generate_arrivals (reference proj/src/workload.cpp:82-106)
+// on the device, bit-identical to the reference.
+//
+// The reference walks the trace's piecewise-linear cumulative rate R(t) with a
+// running target (0, 1, 2, ... for uniform arrivals; a sum of Exp(1) draws from
+// one RandomStream(seed, "arrivals") for Poisson) and emits
+//     t = start_k + (target - cum_k) / rate_k
+// in the first positive-rate interval k with target < cum_end_k - 1e-12, nudged
+// to nextafter(previous, +inf) when it does not increase, and stops at the
+// first t >= duration. Every piece is restated as a data-parallel pass:
+//
+//   K8a mt_stream   one warp runs the single std::mt19937_64 stream. Word m of
+//                   the stream obeys x_m = x_{m-156} ^ twist(x_{m-312},
+//                   x_{m-311}); lane l owns columns 5l..5l+4 (mod 156) in
+//                   registers, so a step of 156 words needs one shuffle and no
+//                   shared memory on the dependency chain.
+//   K8b exp_draws   grid-wide: temper, U = (u64 >> 11) * 2^-53,
+//                   e = -log1p(-U) with glibc's log1p restated bit for bit
+//                   (fdlibm_log1p.h; rng.cpp:24-28).
+//   K8c target_sum  one CTA: the sequentially rounded running sum
+//                   T_i = fl(T_{i-1} + e_i) as an EXACT integer scan. While the
+//                   accumulator stays in one binade [2^p, 2^(p+1)) with ulp u,
+//                   fl(M*u + e) = (M + rint(e/u)) * u, so a tile of 8192 steps is
+//                   an int64 prefix sum. The first step that could leave the
+//                   binade (or is a rounding tie, whose direction depends on the
+//                   accumulator's parity) is done as one real fp64 add and the
+//                   tile restarts after it: ~log2(N) restarts in total.
+//   K8d place       grid-wide: interval k by binary search over the positive-rate
+//                   intervals' thresholds (targets and thresholds are both
+//                   nondecreasing, so the first k that admits target i is the
+//                   reference's k), t_i in the reference's operation order, and
+//                   key_i = ord(t_i) - i where ord() maps doubles to int64 in
+//                   order with nextafter(x, +inf) == ord(x) + 1.
+//   K8e/K8f         the nextafter fix is t'_i = max(t_i, next(t'_{i-1})), i.e.
+//                   ord(t'_i) = max_{j<=i} key_j + i: a max-scan (block maxima,
+//                   one-block carry scan, in-block scan); the first t'_i >=
+//                   duration ends the walk.
+//
+// Interval tables (cum, start, threshold) are O(#intervals) sequential fp64
+// sums and are built on the host in the reference's order.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <limits>
+#include <vector>
+
+#include "ds_internal.h"
+#include "fdlibm_log1p.h"
+
+namespace {
+
+constexpr int kSumThreads = 1024;
+constexpr int kSumPer = 8;
+constexpr int kSumTile = kSumThreads * kSumPer;
+constexpr int kPlaceThreads = 512;
+constexpr long long kNoIndex = 0x7fffffffffffffffLL;
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {   // rng.cpp:8-13
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+uint64_t fnv1a(const char* s) {                                          // rng.cpp:15-22
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (; *s; ++s) {
+        h ^= static_cast<unsigned char>(*s);
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+__device__ __forceinline__ uint64_t mt_mix(uint64_t xk, uint64_t xk1) {
+    const uint64_t y = (xk & 0xFFFFFFFF80000000ULL) | (xk1 & 0x7FFFFFFFULL);
+    return (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
+}
+
+__device__ __forceinline__ uint64_t temper(uint64_t z) {
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+    z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+    z ^= z >> 43;
+    return z;
+}
+
+// ---- K8a: the single mt19937_64 stream, untempered words x_312 .. -----------
+// raw[k] = x_{312+k}; output k of the engine is temper(raw[k]).
+__global__ void __launch_bounds__(32) mt_stream_kernel(uint64_t seed, int64_t n,
+                                                       uint64_t* __restrict__ raw) {
+    __shared__ uint64_t init[312];
+    const int lane = threadIdx.x;
+    if (lane == 0) {   // std::mt19937_64 seeding recurrence
+        uint64_t x = seed;
+        init[0] = x;
+        for (int i = 1; i < 312; ++i) {
+            x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
+            init[i] = x;
+        }
+    }
+    __syncwarp();
+    // Column c = 5*lane + q (c < 156). x2 = step s-2, x1 = step s-1.
+    uint64_t x2[5], x1[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int c = 5 * lane + q;
+        x2[q] = c < 156 ? init[c] : 0;
+        x1[q] = c < 156 ? init[156 + c] : 0;
+    }
+    const int64_t steps = (n + 155) / 156;
+    for (int64_t s = 0; s < steps; ++s) {
+        // x_{m-311} for column c is column c+1 of step s-2 (lane+1's q=0 for
+        // q=4); for c = 155 (lane 31, q = 0) it is column 0 of step s-1.
+        const uint64_t nb2 = __shfl_down_sync(0xffffffffu, x2[0], 1);
+        const uint64_t c0_1 = __shfl_sync(0xffffffffu, x1[0], 0);
+        uint64_t nx[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            uint64_t nbr;
+            if (q < 4) nbr = x2[q + 1];
+            else nbr = nb2;
+            if (lane == 31 && q == 0) nbr = c0_1;
+            nx[q] = x1[q] ^ mt_mix(x2[q], nbr);
+        }
+        const int64_t k0 = s * 156 + 5 * lane;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            if (5 * lane + q < 156 && k0 + q < n) raw[k0 + q] = nx[q];
+            x2[q] = x1[q];
+            x1[q] = nx[q];
+        }
+    }
+}
+
+// ---- K8b: Exp(1) variates -----------------------------------------------------
+// RandomStream::exponential(1.0) = -log1p(-uniform()) / 1.0 (rng.cpp:24-28); the
+// division by 1.0 is an exact identity and is dropped.
+// raw and e are the same buffer (each element is replaced in place).
+__global__ void __launch_bounds__(256) exp_draws_kernel(const uint64_t* raw, int64_t n,
+                                                        double* e) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += stride) {
+        const double u = __dmul_rn(static_cast<double>(temper(raw[i]) >> 11), 0x1.0p-53);
+        e[i] = -ds_log1p(-u);
+    }
+}
+
+// ---- K8c: exact sequentially rounded running sum -----------------------------
+__device__ __forceinline__ unsigned long long block_exclusive_sum(unsigned long long v,
+                                                                  unsigned long long* warp_tot,
+                                                                  unsigned long long* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = warp_tot[lane];
+        unsigned long long wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        warp_tot[lane] = wi - w;   // exclusive prefix of warps
+        if (lane == 31) *total = wi;
+    }
+    __syncthreads();
+    return warp_tot[warp] + inc - v;
+}
+
+__global__ void __launch_bounds__(kSumThreads) target_sum_kernel(const double* __restrict__ e,
+                                                                 int64_t n,
+                                                                 double* __restrict__ T) {
+    __shared__ unsigned long long warp_tot[32];
+    __shared__ unsigned long long s_total;
+    __shared__ long long s_first;
+    __shared__ double s_acc;
+    const int tid = threadIdx.x;
+    double acc = e[0];
+    if (tid == 0) T[0] = acc;
+    int64_t i = 1;
+    constexpr unsigned long long kLimit = (1ULL << 53) - 2;
+    while (i < n) {
+        // Binade of the accumulator: acc = M * u, M in [2^52, 2^53).
+        const bool scan_ok = acc >= 0x1.0p-60 && acc < 0x1.0p+500;
+        int p = 0;
+        double scale = 0.0, ulp = 0.0;
+        unsigned long long M = 0;
+        if (scan_ok) {
+            p = static_cast<int>((__double_as_longlong(acc) >> 52) & 0x7ff) - 1023;
+            scale = __longlong_as_double(static_cast<long long>(52 - p + 1023) << 52);
+            ulp = __longlong_as_double(static_cast<long long>(p - 52 + 1023) << 52);
+            M = static_cast<unsigned long long>(__dmul_rn(acc, scale));
+        }
+        const int64_t base = i + static_cast<int64_t>(tid) * kSumPer;
+        unsigned long long r[kSumPer];
+        unsigned long long mine = 0;
+        long long first_bad = kNoIndex;
+#pragma unroll
+        for (int q = 0; q < kSumPer; ++q) {
+            const int64_t j = base + q;
+            r[q] = 0;
+            if (j < n) {
+                const double y = __dmul_rn(e[j], scale);   // exact power-of-two scaling
+                const double fl = floor(y);
+                const double fr = __dsub_rn(y, fl);
+                const bool bad = !scan_ok || !(y < 0x1.0p53) || fr == 0.5;
+                if (bad && first_bad == kNoIndex) first_bad = j;
+                r[q] = bad ? 0 : static_cast<unsigned long long>(fl) + (fr > 0.5 ? 1 : 0);
+            }
+            mine += r[q];
+        }
+        const unsigned long long excl = block_exclusive_sum(mine, warp_tot, &s_total);
+        // First step whose result could leave the binade.
+        unsigned long long P = M + excl;
+#pragma unroll
+        for (int q = 0; q < kSumPer; ++q) {
+            const int64_t j = base + q;
+            P += r[q];
+            if (j < n && P > kLimit && j < first_bad) first_bad = j;
+        }
+        if (tid == 0) s_first = kNoIndex;
+        __syncthreads();
+        if (first_bad != kNoIndex) atomicMin(&s_first, first_bad);
+        __syncthreads();
+        const long long v = s_first;
+        const int64_t tile_end = (i + kSumTile < n) ? i + kSumTile : n;
+        P = M + excl;
+#pragma unroll
+        for (int q = 0; q < kSumPer; ++q) {
+            const int64_t j = base + q;
+            P += r[q];
+            if (j < n && j < v) T[j] = __dmul_rn(static_cast<double>(P), ulp);
+            if (j == tile_end - 1 && v >= tile_end) s_acc = __dmul_rn(static_cast<double>(P), ulp);
+        }
+        __syncthreads();   // T[v-1] (or s_acc) visible to thread 0
+        if (v < tile_end) {
+            if (tid == 0) {
+                const double prev = (v == i) ? acc : T[v - 1];
+                const double t = __dadd_rn(prev, e[v]);   // the reference's own add
+                T[v] = t;
+                s_acc = t;
+            }
+            __syncthreads();
+            acc = s_acc;
+            i = v + 1;
+        } else {
+            acc = s_acc;
+            i = tile_end;
+        }
+        __syncthreads();
+    }
+}
+
+// ---- K8d: place targets in intervals ------------------------------------------
+__device__ __forceinline__ long long ord_of(double x) {
+    const long long b = __double_as_longlong(x);
+    return b >= 0 ? b : -(b & 0x7fffffffffffffffLL);
+}
+
+__device__ __forceinline__ double double_of(long long o) {
+    return o >= 0 ? __longlong_as_double(o) : __longlong_as_double((-o) | (1LL << 63));
+}
+
+struct IntervalParams {
+    double cum;
+    double start;
+    double rate;
+    double pad;
+};
+
+__device__ __forceinline__ int first_interval(const double* thr, int P, double target) {
+    // first k with target < thr[k] (thr nondecreasing)
+    int lo = 0, hi = P;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (target < thr[mid]) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ double target_of(const double* T, int64_t i) {
+    return T ? T[i] : static_cast<double>(i);   // uniform: target += 1.0 from 0.0 is exact
+}
+
+__device__ __forceinline__ long long block_max_inclusive(long long v, long long* warp_buf) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o && t > v) v = t;
+    }
+    if (lane == 31) warp_buf[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        long long w = lane < nw ? warp_buf[lane] : LLONG_MIN;
+        long long wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o && t > wi) wi = t;
+        }
+        const long long prev = __shfl_up_sync(0xffffffffu, wi, 1);
+        if (lane < nw) warp_buf[lane] = lane == 0 ? LLONG_MIN : prev;   // exclusive
+    }
+    __syncthreads();
+    const long long pre = warp_buf[warp];
+    return pre > v ? pre : v;
+}
+
+__global__ void __launch_bounds__(kPlaceThreads)
+place_kernel(const double* __restrict__ T, int64_t n, const double* __restrict__ thr,
+             const IntervalParams* __restrict__ ip, int P, long long* __restrict__ key,
+             long long* __restrict__ block_max, long long* __restrict__ flags) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kPlaceThreads + threadIdx.x;
+    long long k_out = LLONG_MIN;
+    if (i < n) {
+        const double target = target_of(T, i);
+        const int k = first_interval(thr, P, target);
+        if (k == P) {
+            atomicMin(&flags[0], static_cast<long long>(i));   // no interval admits it
+        } else {
+            const IntervalParams q = ip[k];
+            // workload.cpp:97: start + (target - cum) / rate
+            const double t = __dadd_rn(q.start, __ddiv_rn(__dsub_rn(target, q.cum), q.rate));
+            k_out = ord_of(t) - static_cast<long long>(i);
+        }
+        key[i] = k_out;
+    }
+    __shared__ long long red[kPlaceThreads / 32];
+    long long m = k_out;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const long long t = __shfl_xor_sync(0xffffffffu, m, o);
+        m = t > m ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long b = LLONG_MIN;
+        for (int w = 0; w < kPlaceThreads / 32; ++w) b = red[w] > b ? red[w] : b;
+        block_max[blockIdx.x] = b;
+    }
+}
+
+// Exclusive max-scan of the block maxima (one block), in place.
+__global__ void __launch_bounds__(1024) carry_kernel(long long* __restrict__ block_max, int nb) {
+    __shared__ long long warp_buf[32];
+    __shared__ long long s_incl[1024];
+    long long run = LLONG_MIN;
+    for (int base = 0; base < nb; base += 1024) {
+        const int b = base + threadIdx.x;
+        const long long v = b < nb ? block_max[b] : LLONG_MIN;
+        long long incl = block_max_inclusive(v, warp_buf);
+        incl = incl > run ? incl : run;
+        s_incl[threadIdx.x] = incl;
+        __syncthreads();
+        if (b < nb) block_max[b] = threadIdx.x == 0 ? run : s_incl[threadIdx.x - 1];
+        run = s_incl[1023];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kPlaceThreads)
+finalize_kernel(const double* __restrict__ T, int64_t n, const double* __restrict__ thr, int P,
+                const long long* __restrict__ key, const long long* __restrict__ carry,
+                double duration, double* __restrict__ out, long long* __restrict__ flags) {
+    __shared__ long long warp_buf[kPlaceThreads / 32];
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kPlaceThreads + threadIdx.x;
+    const long long v = i < n ? key[i] : LLONG_MIN;
+    long long m = block_max_inclusive(v, warp_buf);
+    const long long c = carry[blockIdx.x];
+    m = c > m ? c : m;
+    if (i < n && i < flags[0]) {
+        const double t = double_of(m + static_cast<long long>(i));
+        out[i] = t;
+        if (t >= duration) {   // workload.cpp:100 ends the walk here
+            atomicMin(&flags[1], static_cast<long long>(i));
+            // Only the last positive-rate interval can end the walk this way
+            // (the reference would otherwise retry the target in later ones).
+            if (first_interval(thr, P, target_of(T, i)) != P - 1) atomicOr(
+                reinterpret_cast<unsigned long long*>(&flags[2]), 1ULL);
+        }
+    }
+}
+
+struct Walk {
+    std::vector<double> thr;
+    std::vector<IntervalParams> ip;
+    double duration = 0.0;
+};
+
+ds_status build_walk(const double* rates, int32_t n_rates, double dt, Walk* w) {
+    double cum = 0.0;   // workload.cpp:90-94
+    for (int32_t k = 0; k < n_rates; ++k) {
+        const double rate = rates[k];
+        if (!(rate >= 0.0) || !std::isfinite(rate))
+            return dsi::fail(DS_ERR_DOMAIN, "rate must be a non-negative finite number");
+        const double start = dt * static_cast<double>(k);
+        const double cum_end = cum + rate * dt;
+        if (!std::isfinite(cum_end))
+            return dsi::fail(DS_ERR_DOMAIN, "cumulative rate overflows");
+        if (rate > 0.0) {
+            w->thr.push_back(cum_end - 1e-12);
+            w->ip.push_back({cum, start, rate, 0.0});
+        }
+        cum = cum_end;
+    }
+    w->duration = dt * static_cast<double>(n_rates);
+    return DS_OK;
+}
+
+ds_status generate(ds_ctx* ctx, const double* rates, int32_t n_rates, double dt, uint64_t seed,
+                   int32_t mode, double* dev_out, double* host_out, int64_t capacity,
+                   int64_t* count, cudaStream_t st) {
+    if (!ctx || !count || n_rates < 0 || (n_rates > 0 && !rates))
+        return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (mode != DS_ARRIVALS_POISSON && mode != DS_ARRIVALS_UNIFORM)
+        return dsi::fail(DS_ERR_INVALID_ARGUMENT, "unknown arrival mode");
+    if (!(dt > 0.0) || !std::isfinite(dt))
+        return dsi::fail(DS_ERR_DOMAIN, "trace interval must be positive");
+    *count = 0;
+    Walk w;
+    ds_status s = build_walk(rates, n_rates, dt, &w);
+    if (s != DS_OK) return s;
+    const int P = static_cast<int>(w.thr.size());
+    if (P == 0) return DS_OK;
+    const double last = w.thr.back();   // no target at or above this is placed
+    const bool poisson = mode == DS_ARRIVALS_POISSON;
+    double want;
+    if (poisson) {
+        want = std::ceil(last + 8.0 * std::sqrt(last > 0.0 ? last : 0.0) + 64.0);
+        if (const char* env = std::getenv("DS_ARRIVALS_INITIAL_DRAWS")) {   // test hook
+            const double v = std::atof(env);
+            if (v >= 2.0) want = v;
+        }
+    } else {
+        want = std::floor(last > 0.0 ? last : 0.0) + 2.0;   // target floor(last)+1 fails
+    }
+    constexpr double kMaxDraws = 1ULL << 33;
+    for (;;) {
+        if (!(want <= kMaxDraws))
+            return dsi::fail(DS_ERR_CAPACITY, "trace implies more arrivals than supported");
+        const int64_t D = static_cast<int64_t>(want);
+        const int64_t nb = (D + kPlaceThreads - 1) / kPlaceThreads;
+        const size_t b8 = dsi::align_up(sizeof(double) * D, 256);
+        const size_t bt = dsi::align_up(sizeof(double) * P, 256);
+        const size_t bi = dsi::align_up(sizeof(IntervalParams) * P, 256);
+        const size_t bb = dsi::align_up(sizeof(long long) * nb, 256);
+        const size_t total = (poisson ? 2 * b8 : 0) + 2 * b8 + bt + bi + bb + 256;
+        char* base = nullptr;
+        s = dsi::ensure_scratch(ctx, total, reinterpret_cast<void**>(&base));
+        if (s != DS_OK) return s;
+        char* p = base;
+        double* e = nullptr;
+        double* T = nullptr;
+        if (poisson) {
+            e = reinterpret_cast<double*>(p);
+            p += b8;
+            T = reinterpret_cast<double*>(p);
+            p += b8;
+        }
+        long long* key = reinterpret_cast<long long*>(p);
+        p += b8;
+        double* out = reinterpret_cast<double*>(p);
+        p += b8;
+        double* thr = reinterpret_cast<double*>(p);
+        p += bt;
+        IntervalParams* ip = reinterpret_cast<IntervalParams*>(p);
+        p += bi;
+        long long* bmax = reinterpret_cast<long long*>(p);
+        p += bb;
+        long long* flags = reinterpret_cast<long long*>(p);
+        long long* hflags = nullptr;
+        s = dsi::ensure_pinned(ctx, 4 * sizeof(long long), reinterpret_cast<void**>(&hflags));
+        if (s != DS_OK) return s;
+        const long long init[4] = {kNoIndex, kNoIndex, 0, 0};
+        DS_CUDA_TRY(cudaMemcpyAsync(flags, init, sizeof init, cudaMemcpyHostToDevice, st));
+        DS_CUDA_TRY(cudaMemcpyAsync(thr, w.thr.data(), sizeof(double) * P,
+                                    cudaMemcpyHostToDevice, st));
+        DS_CUDA_TRY(cudaMemcpyAsync(ip, w.ip.data(), sizeof(IntervalParams) * P,
+                                    cudaMemcpyHostToDevice, st));
+        if (poisson) {
+            // RandomStream(seed, "arrivals") (rng.hpp:20-21)
+            const uint64_t eng = splitmix64(seed ^ splitmix64(fnv1a("arrivals")));
+            uint64_t* raw = reinterpret_cast<uint64_t*>(e);
+            mt_stream_kernel<<<1, 32, 0, st>>>(eng, D, raw);
+            DS_LAUNCH_CHECK(ctx, "mt_stream_kernel");
+            int64_t blocks = (D + 255) / 256;
+            if (blocks > 148 * 16) blocks = 148 * 16;
+            exp_draws_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(raw, D, e);
+            DS_LAUNCH_CHECK(ctx, "exp_draws_kernel");
+            target_sum_kernel<<<1, kSumThreads, 0, st>>>(e, D, T);
+            DS_LAUNCH_CHECK(ctx, "target_sum_kernel");
+        }
+        place_kernel<<<static_cast<unsigned>(nb), kPlaceThreads, 0, st>>>(T, D, thr, ip, P, key,
+                                                                           bmax, flags);
+        DS_LAUNCH_CHECK(ctx, "place_kernel");
+        carry_kernel<<<1, 1024, 0, st>>>(bmax, static_cast<int>(nb));
+        DS_LAUNCH_CHECK(ctx, "carry_kernel");
+        finalize_kernel<<<static_cast<unsigned>(nb), kPlaceThreads, 0, st>>>(
+            T, D, thr, P, key, bmax, w.duration, out, flags);
+        DS_LAUNCH_CHECK(ctx, "finalize_kernel");
+        DS_CUDA_TRY(cudaMemcpyAsync(hflags, flags, 3 * sizeof(long long), cudaMemcpyDeviceToHost,
+                                    st));
+        DS_CUDA_TRY(cudaStreamSynchronize(st));
+        const long long end_target = hflags[0], end_time = hflags[1];
+        if (hflags[2])
+            return dsi::fail(DS_ERR_INVARIANT,
+                             "arrival walk ended before the last positive-rate interval");
+        if (end_target >= D && end_time >= D) {   // more draws needed: rerun longer
+            want *= 2.0;
+            continue;
+        }
+        const int64_t c = end_target < end_time ? end_target : end_time;
+        *count = c;
+        if (host_out) {
+            if (capacity < c) return dsi::fail(DS_ERR_CAPACITY, "arrivals buffer too small");
+            if (c > 0)
+                DS_CUDA_TRY(cudaMemcpyAsync(host_out, out, sizeof(double) * c,
+                                            cudaMemcpyDeviceToHost, st));
+            DS_CUDA_TRY(cudaStreamSynchronize(st));
+        } else if (dev_out) {
+            if (capacity < c) return dsi::fail(DS_ERR_CAPACITY, "arrivals buffer too small");
+            if (c > 0)
+                DS_CUDA_TRY(cudaMemcpyAsync(dev_out, out, sizeof(double) * c,
+                                            cudaMemcpyDeviceToDevice, st));
+        }
+        return DS_OK;
+    }
+}
+
+} // namespace
+
+extern "C" ds_status ds_generate_arrivals(ds_ctx* ctx, const double* rates, int32_t n_rates,
+                                          double interval_seconds, uint64_t seed, int32_t mode,
+                                          double* arrivals, int64_t capacity, int64_t* count) {
+    if (!ctx) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null ctx");
+    return generate(ctx, rates, n_rates, interval_seconds, seed, mode, nullptr, arrivals,
+                    capacity, count, ctx->stream);
+}
+
+extern "C" ds_status ds_generate_arrivals_device(ds_ctx* ctx, const double* rates,
+                                                 int32_t n_rates, double interval_seconds,
+                                                 uint64_t seed, int32_t mode, double* arrivals,
+                                                 int64_t capacity, int64_t* count, void* stream) {
+    if (!ctx) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null ctx");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    return generate(ctx, rates, n_rates, interval_seconds, seed, mode, arrivals, nullptr,
+                    capacity, count, st);
+}

@@ -86,10 +86,14 @@ __device__ __forceinline__ double box_muller(uint64_t r1, uint64_t r2) { // rng.
     return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
 }
 
+// kRecords: write full Query records (workload.cpp:121-128) instead of the
+// conf / quality_light columns.
+template <bool kRecords>
 __global__ void __launch_bounds__(256)
 latent_kernel(double easy_fraction, double gap_scale, double fidelity, double sigma,
               uint64_t seed_mix, uint64_t id0, int64_t n, double* __restrict__ conf,
-              double* __restrict__ quality_light) {
+              double* __restrict__ quality_light, const double* __restrict__ arrivals,
+              double slo_seconds, ds_query* __restrict__ records) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += stride) {
@@ -104,9 +108,33 @@ latent_kernel(double easy_fraction, double gap_scale, double fidelity, double si
         const double noise = __dadd_rn(0.0, __dmul_rn(sigma, box_muller(r[3], r[4])));
         double c = __dadd_rn(__dadd_rn(0.5, __dmul_rn(fidelity, dq)), noise);
         c = c < 0.0 ? 0.0 : (1.0 < c ? 1.0 : c);                        // std::clamp
-        conf[i] = c;
-        if (quality_light) quality_light[i] = __dadd_rn(1.0, dq);
+        if constexpr (kRecords) {
+            const double arrival = arrivals[i];
+            ds_query q;
+            q.id = id;
+            q.arrival = arrival;
+            q.deadline = __dadd_rn(arrival, slo_seconds);
+            q.quality_light = __dadd_rn(1.0, dq);
+            q.quality_heavy = 1.0;
+            q.confidence = c;
+            records[i] = q;
+        } else {
+            conf[i] = c;
+            if (quality_light) quality_light[i] = __dadd_rn(1.0, dq);
+        }
     }
+}
+
+int latent_blocks(int64_t n) {
+    int64_t blocks = (n + 255) / 256;
+    const int64_t cap = 148 * 16;   // grid-stride beyond 16 waves of 256
+    return static_cast<int>(blocks > cap ? cap : blocks);
+}
+
+ds_status check_model(const ds_query_model* m) {   // workload.cpp:110-111
+    if (!(m->easy_fraction >= 0.0) || !(m->easy_fraction <= 1.0))
+        return dsi::fail(DS_ERR_DOMAIN, "easy_fraction must lie in [0, 1]");
+    return DS_OK;
 }
 
 } // namespace
@@ -115,15 +143,13 @@ extern "C" ds_status ds_score_latent_device(ds_ctx* ctx, const ds_query_model* m
                                             int64_t n, double* conf, double* quality_light,
                                             void* stream) {
     if (!ctx || !m) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (ds_status s = check_model(m); s != DS_OK) return s;
     if (n <= 0) return DS_OK;
     const uint64_t seed_mix = splitmix64(m->seed) ^ splitmix64(fnv1a("query"));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    int64_t blocks = (n + 255) / 256;
-    const int64_t cap = 148 * 16;   // grid-stride beyond 16 waves of 256
-    if (blocks > cap) blocks = cap;
-    latent_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+    latent_kernel<false><<<latent_blocks(n), 256, 0, st>>>(
         m->easy_fraction, m->quality_gap_scale, m->confidence_fidelity, m->noise_sigma,
-        seed_mix, id0, n, conf, quality_light);
+        seed_mix, id0, n, conf, quality_light, nullptr, 0.0, nullptr);
     DS_LAUNCH_CHECK(ctx, "latent_kernel");
     return DS_OK;
 }
@@ -132,8 +158,7 @@ extern "C" ds_status ds_score_latent(ds_ctx* ctx, const ds_query_model* m, uint6
                                      int64_t n, double* conf, double* quality_light) {
     if (!ctx || !m || (n > 0 && !conf)) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
     // sample_query's checks (workload.cpp:110-112); slo is not an input here.
-    if (!(m->easy_fraction >= 0.0) || !(m->easy_fraction <= 1.0))
-        return dsi::fail(DS_ERR_DOMAIN, "easy_fraction must lie in [0, 1]");
+    if (ds_status s = check_model(m); s != DS_OK) return s;
     if (n <= 0) return DS_OK;
     const size_t bytes = dsi::align_up(sizeof(double) * n, 256);
     char* d = nullptr;
@@ -148,6 +173,47 @@ extern "C" ds_status ds_score_latent(ds_ctx* ctx, const ds_query_model* m, uint6
     if (quality_light)
         DS_CUDA_TRY(cudaMemcpyAsync(quality_light, dql, sizeof(double) * n,
                                     cudaMemcpyDeviceToHost, ctx->stream));
+    DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return DS_OK;
+}
+
+extern "C" ds_status ds_sample_queries_device(ds_ctx* ctx, const ds_query_model* m, uint64_t id0,
+                                             const double* arrivals, int64_t n,
+                                             double slo_seconds, ds_query* out, void* stream) {
+    if (!ctx || !m || (n > 0 && (!arrivals || !out)))
+        return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (ds_status s = check_model(m); s != DS_OK) return s;
+    if (!(slo_seconds > 0.0)) return dsi::fail(DS_ERR_DOMAIN, "slo_seconds must be positive");
+    if (n <= 0) return DS_OK;
+    const uint64_t seed_mix = splitmix64(m->seed) ^ splitmix64(fnv1a("query"));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    latent_kernel<true><<<latent_blocks(n), 256, 0, st>>>(
+        m->easy_fraction, m->quality_gap_scale, m->confidence_fidelity, m->noise_sigma,
+        seed_mix, id0, n, nullptr, nullptr, arrivals, slo_seconds, out);
+    DS_LAUNCH_CHECK(ctx, "latent_kernel<records>");
+    return DS_OK;
+}
+
+extern "C" ds_status ds_sample_queries(ds_ctx* ctx, const ds_query_model* m, uint64_t id0,
+                                      const double* arrivals, int64_t n, double slo_seconds,
+                                      ds_query* out) {
+    if (!ctx || !m || (n > 0 && (!arrivals || !out)))
+        return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (ds_status s = check_model(m); s != DS_OK) return s;
+    if (!(slo_seconds > 0.0)) return dsi::fail(DS_ERR_DOMAIN, "slo_seconds must be positive");
+    if (n <= 0) return DS_OK;
+    const size_t ba = dsi::align_up(sizeof(double) * n, 256);
+    char* d = nullptr;
+    ds_status st = dsi::ensure_scratch(ctx, ba + sizeof(ds_query) * n, reinterpret_cast<void**>(&d));
+    if (st != DS_OK) return st;
+    double* darr = reinterpret_cast<double*>(d);
+    ds_query* dq = reinterpret_cast<ds_query*>(d + ba);
+    DS_CUDA_TRY(cudaMemcpyAsync(darr, arrivals, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    st = ds_sample_queries_device(ctx, m, id0, darr, n, slo_seconds, dq, ctx->stream);
+    if (st != DS_OK) return st;
+    DS_CUDA_TRY(cudaMemcpyAsync(out, dq, sizeof(ds_query) * n, cudaMemcpyDeviceToHost,
+                                ctx->stream));
     DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return DS_OK;
 }

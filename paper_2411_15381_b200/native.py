@@ -89,6 +89,12 @@ SIGNATURES = [
     ("ds_disc_score", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p]),
     ("ds_disc_score_device", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p, c_p]),
     ("ds_synth_images_device", ctypes.c_int, [c_p, u64, u64, i64, i32, i32, c_p, c_p]),
+    ("ds_generate_arrivals", ctypes.c_int, [c_p, c_p, i32, f64, u64, i32, c_p, i64,
+                                            ctypes.POINTER(i64)]),
+    ("ds_generate_arrivals_device", ctypes.c_int, [c_p, c_p, i32, f64, u64, i32, c_p, i64,
+                                                   ctypes.POINTER(i64), c_p]),
+    ("ds_sample_queries", ctypes.c_int, [c_p, c_p, u64, c_p, i64, f64, c_p]),
+    ("ds_sample_queries_device", ctypes.c_int, [c_p, c_p, u64, c_p, i64, f64, c_p, c_p]),
 ]
 
 
@@ -166,6 +172,29 @@ class Context:
         check(lib().ds_score_latent(self.handle, abi.ptr(model), id0, n, abi.ptr(conf),
                                     abi.ptr(ql)))
         return (conf, ql) if with_quality else conf
+
+    # ---- workload synthesis ----------------------------------------------
+    def generate_arrivals(self, rates, interval_seconds: float, seed: int,
+                          mode: int = abi.ARRIVALS_POISSON) -> np.ndarray:
+        rates = np.ascontiguousarray(np.atleast_1d(np.asarray(rates, np.float64)))
+        n = i64(0)
+        check(lib().ds_generate_arrivals(self.handle, abi.ptr(rates), len(rates),
+                                         float(interval_seconds), int(seed), int(mode), None, 0,
+                                         ctypes.byref(n)))
+        out = np.zeros(max(n.value, 1), np.float64)
+        check(lib().ds_generate_arrivals(self.handle, abi.ptr(rates), len(rates),
+                                         float(interval_seconds), int(seed), int(mode),
+                                         abi.ptr(out), len(out), ctypes.byref(n)))
+        return out[:n.value]
+
+    def sample_query_records(self, model: np.ndarray, arrivals, slo_seconds: float,
+                             id0: int = 0) -> np.ndarray:
+        model = np.ascontiguousarray(model, abi.QUERY_MODEL)
+        arrivals = np.ascontiguousarray(arrivals, np.float64)
+        out = np.zeros(len(arrivals), abi.QUERY)
+        check(lib().ds_sample_queries(self.handle, abi.ptr(model), id0, abi.ptr(arrivals),
+                                      len(arrivals), float(slo_seconds), abi.ptr(out)))
+        return out
 
     # ---- router ---------------------------------------------------------
     def route(self, conf: np.ndarray, thresholds, index_base: int = 0, with_lists: bool = True):

@@ -32,3 +32,25 @@ def route_digest(idx):
         return np.uint64(0)
     return np.uint64(int(np.bitwise_xor.reduce(
         (idx * np.uint64(0x9E3779B97F4A7C15)) ^ np.arange(len(idx), dtype=np.uint64))))
+
+
+def arrival_case(g, name):
+    """(rates, interval_seconds, seed, mode) of a generate_arrivals golden."""
+    dt, seed, mode = g[f"{name}__meta"]
+    return np.ascontiguousarray(g[f"{name}__rates"]), float(dt), int(seed), int(mode)
+
+
+def assert_arrivals_match(g, name, got):
+    """Bit-exact equality with the reference's timestamps (count, sha256 of
+    the bytes, and the stored values)."""
+    import hashlib
+    got = np.ascontiguousarray(got, np.float64)
+    assert len(got) == int(g[f"{name}__count"]), (name, len(got), int(g[f"{name}__count"]))
+    if f"{name}__arrivals" in g:
+        want = g[f"{name}__arrivals"]
+        bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+        assert len(bad) == 0, (name, len(bad), bad[:5], got[bad[:5]], want[bad[:5]])
+    else:
+        idx = g[f"{name}__sample_idx"]
+        assert np.array_equal(got[idx].view(np.uint64), g[f"{name}__sample"].view(np.uint64)), name
+    assert hashlib.sha256(got.tobytes()).hexdigest() == str(g[f"{name}__sha256"]), name

@@ -177,3 +177,73 @@ def test_synth_images_host_restatement_is_deterministic():
     b = disc_oracle.synth_images(1, 0, 2, 32, 32)
     assert np.array_equal(a, b) and a.dtype == np.uint8 and a.shape == (2, 32, 32, 3)
     assert not np.array_equal(a[0], a[1])
+
+
+def test_port_arrivals_match_reference_goldens(golden):
+    """dso_generate_arrivals (the C restatement of workload.cpp:82-106)
+    reproduces the reference's timestamps on every golden trace."""
+    from tests.helpers import arrival_case, assert_arrivals_match
+    g = golden("arrivals")
+    for name in g["names"]:
+        rates, dt, seed, mode = arrival_case(g, str(name))
+        n = lib.port().dso_generate_arrivals(P(rates), len(rates), dt, seed, mode, None, 0)
+        a = np.zeros(max(n, 1))
+        assert lib.port().dso_generate_arrivals(P(rates), len(rates), dt, seed, mode, P(a),
+                                                len(a)) == n
+        assert_arrivals_match(g, str(name), a[:n])
+
+
+def test_arrival_goldens_hold_reference_known_answers(golden):
+    """test_workload.cpp:71-103 known answers, and the SURVEY A.1 arrival
+    counts of the shipped configs (cascade1 11,559; cascade3 1,986)."""
+    g = golden("arrivals")
+    assert list(g["unit_uniform_2__arrivals"]) == [0.0, 0.5]
+    np.testing.assert_allclose(g["unit_uniform_13__arrivals"], [0, 1, 1 + 1 / 3, 1 + 2 / 3])
+    assert int(g["unit_zero__count"]) == 0
+    a = g["unit_poisson_42__arrivals"]
+    assert 5700 < len(a) < 6300 and np.all(np.diff(a) > 0) and a[0] >= 0 and a[-1] < 600
+    assert int(g["trace_4to32qps_s1__count"]) == 11559
+    assert int(g["trace_1to8qps_s1__count"]) == 1986
+
+
+def test_log1p_restatement_matches_host_libm(tmp_path):
+    """paper_2411_15381_b200/csrc/fdlibm_log1p.h (the device's log1p, used for
+    every Exp(1) arrival draw) compiled for the host equals the host libm's
+    log1p bit for bit on 2^24 inputs: the reference's own U in [0, 1) draws,
+    tiny and near -1 arguments, and random doubles."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "t.c"
+    src.write_text(r'''
+#include <math.h>
+#include <stdio.h>
+#include "fdlibm_log1p.h"
+static uint64_t rs = 88172645463325252ull;
+static uint64_t xr(void) { rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17; return rs; }
+int main(void) {
+    long bad = 0, n = 1L << 24;
+    for (long i = 0; i < n; i++) {
+        double x;
+        switch (i & 3) {
+        case 0: x = -(double)(xr() >> 11) * 0x1.0p-53; break;          /* -U */
+        case 1: x = -ldexp((double)(xr() >> 11), -(int)(53 + xr() % 60)); break; /* tiny */
+        case 2: x = -1.0 + ldexp((double)(xr() >> 11), -(int)(53 + xr() % 8)); break;
+        default: x = ds_bitsd(xr()); if (isnan(x)) continue;
+        }
+        double a = log1p(x), b = ds_log1p(x);
+        if (ds_dbits(a) != ds_dbits(b) && !(isnan(a) && isnan(b))) {
+            if (bad < 5) printf("x=%a libm=%a restated=%a\n", x, a, b);
+            bad++;
+        }
+    }
+    printf("bad=%ld\n", bad);
+    return bad != 0;
+}
+''')
+    exe = tmp_path / "t"
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off",
+                    f"-I{root}/paper_2411_15381_b200/csrc", str(src), "-o", str(exe), "-lm"],
+                   check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout
