@@ -17,6 +17,8 @@ Secondary legs in the same JSON line:
             S in {16,32,64,128}); unit = one (problem, t, b1, b2) candidate.
   latent  : the reference's own scorer (sample_query, bit-parity mode, K4) +
             route at t = 0.5 + curve replay over 1M queries per GPU (config 5).
+  workload: generate_arrivals over a 1M-arrival Poisson trace (K8, bit-exact)
+            + the Query records at those arrivals (K4 records); replicas per GPU.
 CPU baselines run on this box's host cores on bounded samples (rank 0, N=1).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
@@ -50,6 +52,8 @@ DECAY = 0.999
 CPU_DISC_SAMPLE = 96          # images for the CPU port of the discriminator
 CPU_PLAN_SAMPLE = 256         # problems for the CPU reference planner
 CPU_LATENT_SAMPLE = 200_000   # queries for the CPU reference scorer
+WL_RATES = [2500.0] * 400     # 400 s at 2,500 qps: 1,000,811 arrivals at seed 3
+WL_SEED = 3
 
 
 def load_peaks():
@@ -201,6 +205,31 @@ def cpu_latent_leg(n, threads):
                                   abi.ptr(cnt))
         kind = "port"
     return n / (time.perf_counter() - t0), kind
+
+
+def cpu_workload_leg(threads):
+    """The reference's generate_arrivals (sequential by construction) + the
+    run_experiment sample_query loop, here on all cores."""
+    from oracle import lib
+    from paper_2411_15381_b200 import abi, workloads
+    rates = np.asarray(WL_RATES, np.float64)
+    m = workloads.query_model()
+    use_ref = lib.ref_available()
+    gen = lib.ref().dsref_generate_arrivals if use_ref else lib.port().dso_generate_arrivals
+    t0 = time.perf_counter()
+    n = gen(abi.ptr(rates), len(rates), 1.0, WL_SEED, 0, None, 0)
+    a = np.zeros(n)
+    t0 = time.perf_counter()
+    gen(abi.ptr(rates), len(rates), 1.0, WL_SEED, 0, abi.ptr(a), n)
+    t_arr = time.perf_counter() - t0
+    conf = np.zeros(n)
+    t0 = time.perf_counter()
+    if use_ref:
+        lib.ref().dsref_sample_queries(abi.ptr(m), 0, n, 5.0, abi.ptr(conf), None, threads)
+    else:
+        lib.port().dso_sample_queries(abi.ptr(m), 0, n, abi.ptr(conf), None, threads)
+    t_q = time.perf_counter() - t0
+    return n / (t_arr + t_q), n / t_arr, ("reference" if use_ref else "port"), a
 
 
 def host_weights():
@@ -495,6 +524,42 @@ def run_gpu(args):
     lat_ms = [levs[i].elapsed_time(levs[i + 1]) for i in range(3)]
     latent_value = ws * N_LATENT / (allmax([sum(lat_ms)])[0] / 1000.0)
 
+    # ---- workload leg: arrivals (K8) + Query records (K4) --------------------
+    wl_rates = np.asarray(WL_RATES, np.float64)
+    wl_cap = 1_100_000
+    wl_arr = torch.empty(wl_cap, dtype=torch.float64, device=dev)
+    wl_rec = torch.empty(wl_cap * 6, dtype=torch.float64, device=dev)   # ds_query = 48 B
+    wl_n = native.i64(0)
+    wevs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+    def workload_step(ev=False):
+        with torch.cuda.stream(stream):
+            if ev:
+                wevs[0].record(stream)
+            native.check(L.ds_generate_arrivals_device(
+                ctx.handle, abi.ptr(wl_rates), len(wl_rates), 1.0, WL_SEED, abi.ARRIVALS_POISSON,
+                native.c_p(wl_arr.data_ptr()), wl_cap, native.ctypes.byref(wl_n),
+                native.c_p(ctx.stream)))
+            if ev:
+                wevs[1].record(stream)
+            native.check(L.ds_sample_queries_device(
+                ctx.handle, abi.ptr(qm), 0, native.c_p(wl_arr.data_ptr()), wl_n.value, 5.0,
+                native.c_p(wl_rec.data_ptr()), native.c_p(ctx.stream)))
+            if ev:
+                wevs[2].record(stream)
+    for _ in range(2):
+        workload_step()
+    torch.cuda.synchronize()
+    wl_ms = [0.0, 0.0]
+    for _ in range(5):
+        workload_step(ev=True)
+        torch.cuda.synchronize()
+        wl_ms[0] += wevs[0].elapsed_time(wevs[1]) / 5
+        wl_ms[1] += wevs[1].elapsed_time(wevs[2]) / 5
+    wl_count = wl_n.value
+    wl_value = ws * wl_count / (allmax([sum(wl_ms)])[0] / 1000.0)
+    wl_arr_value = ws * wl_count / (allmax([wl_ms[0]])[0] / 1000.0)
+
     if rank == 0:
         peaks, peak_src = load_peaks()
         achieved_tflops = N_IMG * DISC_FLOP_PER_IMG / (disc_ms / 1000.0) / 1e12
@@ -532,6 +597,10 @@ def run_gpu(args):
             "latent": {"value": latent_value, "unit": "queries/s", "queries_per_gpu": N_LATENT,
                        "ms_score_route_curve": lat_ms,
                        "roofline": {"bound": "int/fp64 issue (no tensor/HBM bound)"}},
+            "workload": {"value": wl_value, "unit": "queries/s",
+                         "arrivals_per_s": wl_arr_value, "arrivals_per_gpu": wl_count,
+                         "ms_arrivals_records": wl_ms,
+                         "trace": "400 intervals x 2500 qps, Poisson, seed 3 (replica per GPU)"},
         }
         if ws == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
@@ -555,6 +624,14 @@ def run_gpu(args):
                 "value": lv, "unit": "queries/s", "cores": threads, "kind": lk,
                 "sample": f"{CPU_LATENT_SAMPLE} queries: sample_query on {threads} threads + "
                           "sequential observe/defers loop"}
+            wv, wav, wk, wa = cpu_workload_leg(threads)
+            line["workload"]["cpu_baseline"] = {
+                "value": wv, "unit": "queries/s", "arrivals_per_s": wav, "cores": threads,
+                "kind": wk, "sample": f"the full {len(wa)}-arrival trace: generate_arrivals "
+                                      f"(sequential) + sample_query on {threads} threads"}
+            got = wl_arr[:wl_count].cpu().numpy()
+            line["workload"]["parity_vs_cpu"] = bool(
+                len(wa) == wl_count and got.tobytes() == wa.tobytes())
         print(json.dumps(line), flush=True)
         try:
             np.savez(os.path.join(ROOT, "gpurun_out", f"disc_weights_seed{WEIGHT_SEED}.npz"),

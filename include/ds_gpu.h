@@ -21,6 +21,8 @@
  *                                    (reference proj/src/workload.cpp:82-106)
  *              ds_sample_queries*    replaces the sample_query loop of
  *                                    run_experiment (experiment.cpp:76-79)
+ *   output   : ds_format_*_csv*      replaces diffserve::write_csv's row
+ *                                    formatting (metrics.cpp:67-127)
  *
  * Functions without the _device suffix take HOST buffers and copy in/out
  * inside the call (the reference-facing drop-in). The _device variants take
@@ -237,6 +239,87 @@ ds_status ds_sample_queries(ds_ctx* ctx, const ds_query_model* model, uint64_t i
 ds_status ds_sample_queries_device(ds_ctx* ctx, const ds_query_model* model, uint64_t id0,
                                    const double* arrivals, int64_t n, double slo_seconds,
                                    ds_query* out, void* stream);
+
+/* ---- CSV output (K9 csv_format) ---------------------------------------- */
+/* Outcome (metrics.hpp:12-17). */
+typedef enum {
+    DS_OUTCOME_SERVED_LIGHT = 0,
+    DS_OUTCOME_SERVED_HEAVY = 1,
+    DS_OUTCOME_DROPPED = 2,
+    DS_OUTCOME_LATE = 3
+} ds_outcome;
+
+/* QueryRecord (metrics.hpp:22-36); std::optional fields are engaged when the
+ * matching DS_REC_* bit of `present` is set. */
+#define DS_REC_LIGHT_START 0x01u
+#define DS_REC_LIGHT_END 0x02u
+#define DS_REC_HEAVY_START 0x04u
+#define DS_REC_HEAVY_END 0x08u
+#define DS_REC_COMPLETION 0x10u
+#define DS_REC_OUTCOME 0x20u
+#define DS_REC_DELIVERED_QUALITY 0x40u
+typedef struct {
+    uint64_t id;
+    double arrival;
+    double deadline;
+    double confidence;
+    double quality_light;
+    double quality_heavy;
+    double light_start;
+    double light_end;
+    double heavy_start;
+    double heavy_end;
+    double completion;
+    double delivered_quality;
+    uint32_t present;
+    int32_t outcome; /* ds_outcome */
+} ds_query_record;
+
+/* IntervalSnapshot (metrics.hpp:42-54). */
+typedef struct {
+    double interval_start;
+    double demand_observed;
+    double demand_estimated;
+    ds_plan plan;
+    uint64_t arrived;
+    uint64_t served_light;
+    uint64_t served_heavy;
+    uint64_t dropped;
+    uint64_t late;
+    double threshold;
+    double mean_delivered_quality;
+    int32_t has_mean_delivered_quality;
+    int32_t _pad;
+} ds_interval_snapshot;
+
+/* PlanLogEntry (metrics.hpp:57-62). */
+typedef struct {
+    int32_t tick;
+    int32_t _pad;
+    double time;
+    double demand_estimated;
+    ds_plan plan;
+} ds_plan_log_entry;
+
+/* The bytes write_csv puts in queries.csv / intervals.csv / plans.csv
+ * (metrics.cpp:91-127, header line included), byte-identical: every real goes
+ * through an exact "%.6g" (fmt6, metrics.cpp:67-71). *bytes receives the file
+ * size; out may be NULL (size only), else it must hold *bytes bytes, else
+ * DS_ERR_CAPACITY. Host buffers in and out. */
+ds_status ds_format_queries_csv(ds_ctx* ctx, const ds_query_record* records, int64_t n,
+                                char* out, int64_t capacity, int64_t* bytes);
+ds_status ds_format_intervals_csv(ds_ctx* ctx, const ds_interval_snapshot* rows, int64_t n,
+                                  char* out, int64_t capacity, int64_t* bytes);
+ds_status ds_format_plans_csv(ds_ctx* ctx, const ds_plan_log_entry* rows, int64_t n, char* out,
+                              int64_t capacity, int64_t* bytes);
+/* Same for queries.csv with device records and a device output buffer; reads
+ * the size back once (one stream synchronization). */
+ds_status ds_format_queries_csv_device(ds_ctx* ctx, const ds_query_record* records, int64_t n,
+                                       char* out, int64_t capacity, int64_t* bytes,
+                                       void* stream);
+/* fmt6 of n doubles into 16-byte slots (NUL-padded), for tests and callers
+ * that assemble their own rows. */
+ds_status ds_format_g6(ds_ctx* ctx, const double* values, int64_t n, char* out16);
 
 /* ---- discriminator (K5-K7: ingest + fused tcgen05 MLP + head) --------- */
 /* PatchDisc: u8 NHWC image -> 16x16 patches -> 768->256 GELU -> 256->1024

@@ -1,9 +1,11 @@
 // The reference simulator run end to end with the B200 hot path plugged in
-// (SURVEY.md 8(f) row 1): run_experiment (experiment.cpp:60-159) restated
-// with (a) one K4 launch scoring every query instead of the sample_query loop
-// and (b) ds_b200::GpuPlannerPolicy as the Policy, everything else -- config,
-// trace, arrivals, the DES (Simulation), CSV writer -- the reference's own
-// code. --mode cpu runs the stock reference run_experiment for comparison.
+// (SURVEY.md 8(f) rows 1, 3, 4): run_experiment (experiment.cpp:60-159)
+// restated with (a) the arrival timestamps generated on the GPU (K8) instead
+// of generate_arrivals, (b) one K4 launch writing every Query record instead
+// of the sample_query loop, (c) ds_b200::GpuPlannerPolicy as the Policy and
+// (d) the three CSV files formatted on the GPU (K9) instead of write_csv;
+// everything else -- config, trace, the DES (Simulation) -- the reference's
+// own code. --mode cpu runs the stock reference run_experiment for comparison.
 //
 //   des_gpu --config cfg --out dir [--mode gpu|cpu] [--policy name] [--seed s]
 //
@@ -56,8 +58,10 @@ int main(int argc, char** argv) {
         CascadeProfile cascade = load_cascade(cfg.profiles_path, cfg.cascade);
         Trace trace = load_trace(cfg.trace_path);
         if (cfg.trace_scale_min) trace = scale_trace(trace, *cfg.trace_scale_min, *cfg.trace_scale_max);
-        const std::vector<double> arrivals =
-            generate_arrivals(trace, cfg.seed, parse_arrival_mode(cfg.arrival_mode));
+        ds_ctx* ctx = nullptr;
+        ds_b200::throw_status(ds_ctx_create(0, &ctx));
+        const std::vector<double> arrivals = ds_b200::generate_arrivals(
+            ctx, trace, cfg.seed, parse_arrival_mode(cfg.arrival_mode));
         QueryOutcomeModel qmodel;
         qmodel.easy_fraction = cfg.easy_fraction;
         qmodel.quality_gap_scale = cfg.quality_gap_scale;
@@ -65,8 +69,6 @@ int main(int argc, char** argv) {
         qmodel.noise_sigma = cfg.noise_sigma;
         qmodel.seed = cfg.seed;
 
-        ds_ctx* ctx = nullptr;
-        ds_b200::throw_status(ds_ctx_create(0, &ctx));
         std::vector<Query> queries =
             ds_b200::score_queries(ctx, qmodel, arrivals, cascade.slo_seconds);
 
@@ -94,7 +96,7 @@ int main(int argc, char** argv) {
         const auto t0 = std::chrono::steady_clock::now();
         RunOutput out = sim.run();
         const auto t1 = std::chrono::steady_clock::now();
-        write_csv(cfg.out_dir, out.intervals, out.records, out.plans);
+        ds_b200::write_csv(ctx, cfg.out_dir, out.intervals, out.records, out.plans);
         uint64_t arrived = 0, light = 0, heavy = 0, dropped = 0, late = 0;
         for (const QueryRecord& r : out.records) {
             ++arrived;

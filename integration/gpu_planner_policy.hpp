@@ -12,14 +12,19 @@
 // Header-only; compiles against the reference headers and links libds_b200.so.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "diffserve/allocator.hpp"
 #include "diffserve/errors.hpp"
+#include "diffserve/metrics.hpp"
 #include "diffserve/policies.hpp"
 #include "diffserve/profiles.hpp"
 #include "diffserve/workload.hpp"
@@ -198,29 +203,130 @@ private:
     int b1_ = 0, b2_ = 0;
 };
 
-// run_experiment's query construction (experiment.cpp:70-79) with one K4
-// launch instead of a sample_query call per query.
+// generate_arrivals (workload.cpp:82-106) on the GPU (K8), bit-identical.
+inline std::vector<double> generate_arrivals(ds_ctx* ctx, const diffserve::Trace& trace,
+                                             uint64_t seed, diffserve::ArrivalMode mode) {
+    const int32_t m = mode == diffserve::ArrivalMode::uniform ? DS_ARRIVALS_UNIFORM
+                                                              : DS_ARRIVALS_POISSON;
+    const int32_t nr = static_cast<int32_t>(trace.rates.size());
+    int64_t n = 0;
+    throw_status(ds_generate_arrivals(ctx, trace.rates.data(), nr, trace.interval_seconds, seed,
+                                      m, nullptr, 0, &n));
+    std::vector<double> out(static_cast<size_t>(n));
+    throw_status(ds_generate_arrivals(ctx, trace.rates.data(), nr, trace.interval_seconds, seed,
+                                      m, out.data(), n, &n));
+    return out;
+}
+
+// run_experiment's query construction (experiment.cpp:70-79): one K4 launch
+// writes the Query records instead of a sample_query call per query.
 inline std::vector<diffserve::Query> score_queries(ds_ctx* ctx,
                                                    const diffserve::QueryOutcomeModel& m,
                                                    const std::vector<double>& arrivals,
                                                    double slo_seconds) {
-    if (!(slo_seconds > 0.0)) throw std::domain_error("slo_seconds must be positive");
+    static_assert(sizeof(diffserve::Query) == sizeof(ds_query), "Query layout");
+    static_assert(offsetof(diffserve::Query, arrival) == offsetof(ds_query, arrival), "layout");
+    static_assert(offsetof(diffserve::Query, deadline) == offsetof(ds_query, deadline), "");
+    static_assert(offsetof(diffserve::Query, quality_light) == offsetof(ds_query, quality_light),
+                  "");
+    static_assert(offsetof(diffserve::Query, quality_heavy) == offsetof(ds_query, quality_heavy),
+                  "");
+    static_assert(offsetof(diffserve::Query, confidence) == offsetof(ds_query, confidence), "");
     ds_query_model qm{m.easy_fraction, m.quality_gap_scale, m.confidence_fidelity,
                       m.noise_sigma, m.seed};
     const int64_t n = static_cast<int64_t>(arrivals.size());
-    std::vector<double> conf(static_cast<size_t>(n)), ql(static_cast<size_t>(n));
-    throw_status(ds_score_latent(ctx, &qm, 0, n, conf.data(), ql.data()));
     std::vector<diffserve::Query> out(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i) {
-        diffserve::Query& q = out[static_cast<size_t>(i)];
-        q.id = static_cast<uint64_t>(i);
-        q.arrival = arrivals[static_cast<size_t>(i)];
-        q.deadline = q.arrival + slo_seconds;
-        q.quality_light = ql[static_cast<size_t>(i)];
-        q.quality_heavy = 1.0;
-        q.confidence = conf[static_cast<size_t>(i)];
-    }
+    throw_status(ds_sample_queries(ctx, &qm, 0, arrivals.data(), n, slo_seconds,
+                                   reinterpret_cast<ds_query*>(out.data())));
     return out;
+}
+
+inline ds_plan to_plan_pod(const diffserve::AllocationPlan& p) {
+    ds_plan out{};
+    out.x1 = p.x1;
+    out.x2 = p.x2;
+    out.b1 = p.b1;
+    out.b2 = p.b2;
+    out.threshold = p.threshold;
+    out.feasible = p.feasible ? 1 : 0;
+    return out;
+}
+
+// write_csv (metrics.cpp:91-127) with the rows formatted on the GPU (K9);
+// byte-identical files.
+inline void write_csv(ds_ctx* ctx, const std::string& out_dir,
+                      const std::vector<diffserve::IntervalSnapshot>& intervals,
+                      const std::vector<diffserve::QueryRecord>& records,
+                      const std::vector<diffserve::PlanLogEntry>& plans) {
+    std::vector<ds_interval_snapshot> iv(intervals.size());
+    for (size_t i = 0; i < intervals.size(); ++i) {
+        const auto& s = intervals[i];
+        ds_interval_snapshot& o = iv[i];
+        o = ds_interval_snapshot{};
+        o.interval_start = s.interval_start;
+        o.demand_observed = s.demand_observed;
+        o.demand_estimated = s.demand_estimated;
+        o.plan = to_plan_pod(s.plan);
+        o.arrived = s.arrived;
+        o.served_light = s.served_light;
+        o.served_heavy = s.served_heavy;
+        o.dropped = s.dropped;
+        o.late = s.late;
+        o.threshold = s.threshold;
+        o.has_mean_delivered_quality = s.mean_delivered_quality.has_value();
+        o.mean_delivered_quality = s.mean_delivered_quality.value_or(0.0);
+    }
+    std::vector<ds_query_record> qr(records.size());
+    for (size_t i = 0; i < records.size(); ++i) {
+        const auto& r = records[i];
+        ds_query_record& o = qr[i];
+        o = ds_query_record{};
+        o.id = r.id;
+        o.arrival = r.arrival;
+        o.deadline = r.deadline;
+        o.confidence = r.confidence;
+        o.quality_light = r.quality_light;
+        o.quality_heavy = r.quality_heavy;
+        auto opt = [&o](const std::optional<double>& v, double* dst, uint32_t bit) {
+            if (v) {
+                *dst = *v;
+                o.present |= bit;
+            }
+        };
+        opt(r.light_start, &o.light_start, DS_REC_LIGHT_START);
+        opt(r.light_end, &o.light_end, DS_REC_LIGHT_END);
+        opt(r.heavy_start, &o.heavy_start, DS_REC_HEAVY_START);
+        opt(r.heavy_end, &o.heavy_end, DS_REC_HEAVY_END);
+        opt(r.completion, &o.completion, DS_REC_COMPLETION);
+        opt(r.delivered_quality, &o.delivered_quality, DS_REC_DELIVERED_QUALITY);
+        if (r.outcome) {
+            o.outcome = static_cast<int32_t>(*r.outcome);
+            o.present |= DS_REC_OUTCOME;
+        }
+    }
+    std::vector<ds_plan_log_entry> pl(plans.size());
+    for (size_t i = 0; i < plans.size(); ++i) {
+        pl[i] = ds_plan_log_entry{};
+        pl[i].tick = plans[i].tick;
+        pl[i].time = plans[i].time;
+        pl[i].demand_estimated = plans[i].demand_estimated;
+        pl[i].plan = to_plan_pod(plans[i].plan);
+    }
+    std::filesystem::create_directories(out_dir);
+    auto emit = [&](const char* name, auto fn, const auto& rows) {
+        int64_t bytes = 0;
+        const int64_t n = static_cast<int64_t>(rows.size());
+        throw_status(fn(ctx, rows.data(), n, nullptr, 0, &bytes));
+        std::string buf(static_cast<size_t>(bytes), '\0');
+        throw_status(fn(ctx, rows.data(), n, buf.data(), bytes, &bytes));
+        const std::string path = out_dir + "/" + name;
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw std::runtime_error("cannot write " + path);
+        out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
+    };
+    emit("intervals.csv", ds_format_intervals_csv, iv);
+    emit("queries.csv", ds_format_queries_csv, qr);
+    emit("plans.csv", ds_format_plans_csv, pl);
 }
 
 } // namespace ds_b200

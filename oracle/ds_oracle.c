@@ -17,6 +17,7 @@
 #include <math.h>
 #include <pthread.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -177,6 +178,125 @@ int64_t dso_generate_arrivals(const double* rates, int32_t n, double dt, uint64_
         cum = cum_end;
     }
     return c;
+}
+
+/* ---------------------------------------------------------------------- */
+/* CSV rows: metrics.cpp:67-127 (write_csv), fmt6 = snprintf("%.6g")       */
+
+/* fmt6 of n doubles into 16-byte NUL-padded slots (metrics.cpp:67-71). */
+void dso_fmt6(const double* v, int64_t n, char* out16) {
+    for (int64_t i = 0; i < n; ++i) {
+        char buf[40];
+        memset(out16 + 16 * i, 0, 16);
+        snprintf(buf, sizeof buf, "%.6g", v[i]);
+        memcpy(out16 + 16 * i, buf, strlen(buf));
+    }
+}
+
+typedef struct {
+    char* p;
+    int64_t n, cap;
+} sbuf;
+
+static void sb_put(sbuf* b, const char* s, size_t k) {
+    if (b->p && b->n + (int64_t)k <= b->cap) memcpy(b->p + b->n, s, k);
+    b->n += (int64_t)k;
+}
+static void sb_str(sbuf* b, const char* s) { sb_put(b, s, strlen(s)); }
+static void sb_g6(sbuf* b, double v) {
+    char t[40];
+    snprintf(t, sizeof t, "%.6g", v);
+    sb_str(b, t);
+}
+static void sb_opt6(sbuf* b, int present, double v) { /* metrics.cpp:75 */
+    if (present) sb_g6(b, v);
+}
+static void sb_i64(sbuf* b, long long v) {
+    char t[32];
+    snprintf(t, sizeof t, "%lld", v);
+    sb_str(b, t);
+}
+static void sb_u64(sbuf* b, unsigned long long v) {
+    char t[32];
+    snprintf(t, sizeof t, "%llu", v);
+    sb_str(b, t);
+}
+
+/* queries.csv bytes (metrics.cpp:104-115); returns the size, writes at most cap. */
+int64_t dso_format_queries_csv(const ds_query_record* r, int64_t n, char* out, int64_t cap) {
+    static const char* outcome[] = {"served_light", "served_heavy", "dropped", "late"};
+    sbuf b = {out, 0, cap};
+    sb_str(&b, "id,arrival,confidence,quality_light,quality_heavy,deadline,light_start,"
+               "light_end,heavy_start,heavy_end,completion,outcome,delivered_quality\n");
+    for (int64_t i = 0; i < n; ++i) {
+        const ds_query_record* q = &r[i];
+        sb_u64(&b, q->id); sb_str(&b, ",");
+        sb_g6(&b, q->arrival); sb_str(&b, ",");
+        sb_g6(&b, q->confidence); sb_str(&b, ",");
+        sb_g6(&b, q->quality_light); sb_str(&b, ",");
+        sb_g6(&b, q->quality_heavy); sb_str(&b, ",");
+        sb_g6(&b, q->deadline); sb_str(&b, ",");
+        sb_opt6(&b, q->present & DS_REC_LIGHT_START, q->light_start); sb_str(&b, ",");
+        sb_opt6(&b, q->present & DS_REC_LIGHT_END, q->light_end); sb_str(&b, ",");
+        sb_opt6(&b, q->present & DS_REC_HEAVY_START, q->heavy_start); sb_str(&b, ",");
+        sb_opt6(&b, q->present & DS_REC_HEAVY_END, q->heavy_end); sb_str(&b, ",");
+        sb_opt6(&b, q->present & DS_REC_COMPLETION, q->completion); sb_str(&b, ",");
+        if (q->present & DS_REC_OUTCOME)
+            sb_str(&b, (q->outcome >= 0 && q->outcome < 4) ? outcome[q->outcome] : "?");
+        sb_str(&b, ",");
+        sb_opt6(&b, q->present & DS_REC_DELIVERED_QUALITY, q->delivered_quality);
+        sb_str(&b, "\n");
+    }
+    return b.n;
+}
+
+/* intervals.csv bytes (metrics.cpp:92-103). */
+int64_t dso_format_intervals_csv(const ds_interval_snapshot* s, int64_t n, char* out,
+                                 int64_t cap) {
+    sbuf b = {out, 0, cap};
+    sb_str(&b, "interval_start,demand_observed,demand_estimated,threshold,x1,x2,b1,b2,"
+               "feasible,arrived,served_light,served_heavy,dropped,late,"
+               "mean_delivered_quality\n");
+    for (int64_t i = 0; i < n; ++i) {
+        const ds_interval_snapshot* r = &s[i];
+        sb_g6(&b, r->interval_start); sb_str(&b, ",");
+        sb_g6(&b, r->demand_observed); sb_str(&b, ",");
+        sb_g6(&b, r->demand_estimated); sb_str(&b, ",");
+        sb_g6(&b, r->threshold); sb_str(&b, ",");
+        sb_i64(&b, r->plan.x1); sb_str(&b, ",");
+        sb_i64(&b, r->plan.x2); sb_str(&b, ",");
+        sb_i64(&b, r->plan.b1); sb_str(&b, ",");
+        sb_i64(&b, r->plan.b2); sb_str(&b, ",");
+        sb_str(&b, r->plan.feasible ? "1" : "0"); sb_str(&b, ",");
+        sb_u64(&b, r->arrived); sb_str(&b, ",");
+        sb_u64(&b, r->served_light); sb_str(&b, ",");
+        sb_u64(&b, r->served_heavy); sb_str(&b, ",");
+        sb_u64(&b, r->dropped); sb_str(&b, ",");
+        sb_u64(&b, r->late); sb_str(&b, ",");
+        sb_opt6(&b, r->has_mean_delivered_quality, r->mean_delivered_quality);
+        sb_str(&b, "\n");
+    }
+    return b.n;
+}
+
+/* plans.csv bytes (metrics.cpp:117-126). */
+int64_t dso_format_plans_csv(const ds_plan_log_entry* e, int64_t n, char* out, int64_t cap) {
+    sbuf b = {out, 0, cap};
+    sb_str(&b, "tick,time,demand_estimated,threshold,x1,x2,b1,b2,feasible\n");
+    for (int64_t i = 0; i < n; ++i) {
+        const ds_plan_log_entry* r = &e[i];
+        sb_i64(&b, r->tick); sb_str(&b, ",");
+        sb_g6(&b, r->time); sb_str(&b, ",");
+        sb_g6(&b, r->demand_estimated); sb_str(&b, ",");
+        sb_g6(&b, r->plan.threshold); sb_str(&b, ",");
+        sb_i64(&b, r->plan.x1); sb_str(&b, ",");
+        sb_i64(&b, r->plan.x2); sb_str(&b, ",");
+        sb_i64(&b, r->plan.b1); sb_str(&b, ",");
+        sb_i64(&b, r->plan.b2); sb_str(&b, ",");
+        sb_str(&b, r->plan.feasible ? "1" : "0");
+        sb_str(&b, "\n");
+    }
+    return b.n;
 }
 
 /* ---------------------------------------------------------------------- */

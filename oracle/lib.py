@@ -68,6 +68,7 @@ def ref():
         lib.dsref_generate_arrivals.argtypes = [c_p, i32, f64, u64, i32, c_p, i64]
         lib.dsref_generate_arrivals.restype = i64
         lib.dsref_sample_query_records.argtypes = [c_p, u64, c_p, i64, f64, c_p]
+        lib.dsref_write_csv.argtypes = [ctypes.c_char_p, c_p, i64, c_p, i64, c_p, i64]
         lib.dsref_hash_name.argtypes = [ctypes.c_char_p]
         lib.dsref_hash_name.restype = u64
         lib.dsref_stream_raw.argtypes = [u64, ctypes.c_char_p, ctypes.c_int, c_p]
@@ -93,6 +94,12 @@ def port():
         lib.dso_sample_query.argtypes = [c_p, u64, c_p, c_p]
         lib.dso_generate_arrivals.argtypes = [c_p, i32, f64, u64, i32, c_p, i64]
         lib.dso_generate_arrivals.restype = i64
+        lib.dso_fmt6.argtypes = [c_p, i64, c_p]
+        lib.dso_fmt6.restype = None
+        for name in ("dso_format_queries_csv", "dso_format_intervals_csv",
+                     "dso_format_plans_csv"):
+            getattr(lib, name).argtypes = [c_p, i64, c_p, i64]
+            getattr(lib, name).restype = i64
         lib.dso_sample_queries.argtypes = [c_p, u64, i64, c_p, c_p, ctypes.c_int]
         lib.dso_bin_of.argtypes = [f64]
         lib.dso_bins_below.argtypes = [f64]

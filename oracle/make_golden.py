@@ -396,6 +396,32 @@ def gen_arrivals(full_limit=6000):
     return {n: int(out[f"{n}__count"]) for n in names}
 
 
+def gen_csv():
+    """write_csv goldens (metrics.cpp:91-127): random QueryRecord /
+    IntervalSnapshot / PlanLogEntry rows (with the "%.6g" stress values of
+    tests/helpers.special_doubles) and the bytes the reference's own
+    write_csv produced for them."""
+    import tempfile
+    from tests import helpers
+    rng = np.random.default_rng(6)
+    q = helpers.random_query_records(rng, 3000)
+    iv = helpers.random_intervals(rng, 300)
+    pl = helpers.random_plan_log(rng, 200)
+    out = {"records": q, "intervals": iv, "plans": pl}
+    with tempfile.TemporaryDirectory() as tmp:
+        _check(lib.ref().dsref_write_csv(tmp.encode(), P(iv), len(iv), P(q), len(q), P(pl),
+                                         len(pl)), "write_csv")
+        for name in ("queries", "intervals", "plans"):
+            with open(os.path.join(tmp, name + ".csv"), "rb") as f:
+                out[f"{name}_csv"] = np.frombuffer(f.read(), np.uint8)
+    vals = np.concatenate([helpers.special_doubles(), helpers.random_doubles(rng, 6000)])
+    g6 = np.zeros(len(vals), "S16")
+    lib.port().dso_fmt6(P(vals), len(vals), P(g6))
+    out["g6_values"], out["g6_text"] = vals, g6
+    np.savez_compressed(os.path.join(OUT, "csv.npz"), **out)
+    return {k: len(v) for k, v in out.items()}
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     print("alloc_random_2024: feasible", gen_alloc_random(), "of 60")
@@ -407,6 +433,7 @@ def main():
     gen_des()
     print("des: ok")
     print("arrivals:", gen_arrivals())
+    print("csv:", gen_csv())
 
 
 if __name__ == "__main__":

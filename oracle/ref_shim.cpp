@@ -16,6 +16,7 @@
 
 #include "diffserve/allocator.hpp"
 #include "diffserve/errors.hpp"
+#include "diffserve/metrics.hpp"
 #include "diffserve/policies.hpp"
 #include "diffserve/profiles.hpp"
 #include "diffserve/rng.hpp"
@@ -393,6 +394,69 @@ int dsref_sample_query_records(const ds_query_model* m, uint64_t id0, const doub
             out[i] = ds_query{q.id, q.arrival, q.deadline, q.quality_light, q.quality_heavy,
                               q.confidence};
         }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
+// The reference's write_csv (metrics.cpp:91-127) on POD rows, into dir.
+static AllocationPlan to_plan(const ds_plan& p) {
+    AllocationPlan a;
+    a.x1 = p.x1;
+    a.x2 = p.x2;
+    a.b1 = p.b1;
+    a.b2 = p.b2;
+    a.threshold = p.threshold;
+    a.feasible = p.feasible != 0;
+    return a;
+}
+
+int dsref_write_csv(const char* dir, const ds_interval_snapshot* iv, int64_t ni,
+                    const ds_query_record* qr, int64_t nq, const ds_plan_log_entry* pl,
+                    int64_t np) {
+    try {
+        std::vector<IntervalSnapshot> ivs(static_cast<size_t>(ni));
+        for (int64_t i = 0; i < ni; ++i) {
+            IntervalSnapshot& s = ivs[static_cast<size_t>(i)];
+            s.interval_start = iv[i].interval_start;
+            s.demand_observed = iv[i].demand_observed;
+            s.demand_estimated = iv[i].demand_estimated;
+            s.plan = to_plan(iv[i].plan);
+            s.arrived = iv[i].arrived;
+            s.served_light = iv[i].served_light;
+            s.served_heavy = iv[i].served_heavy;
+            s.dropped = iv[i].dropped;
+            s.late = iv[i].late;
+            s.threshold = iv[i].threshold;
+            if (iv[i].has_mean_delivered_quality) s.mean_delivered_quality = iv[i].mean_delivered_quality;
+        }
+        std::vector<QueryRecord> rs(static_cast<size_t>(nq));
+        for (int64_t i = 0; i < nq; ++i) {
+            const ds_query_record& q = qr[i];
+            QueryRecord& r = rs[static_cast<size_t>(i)];
+            r.id = q.id;
+            r.arrival = q.arrival;
+            r.deadline = q.deadline;
+            r.confidence = q.confidence;
+            r.quality_light = q.quality_light;
+            r.quality_heavy = q.quality_heavy;
+            if (q.present & DS_REC_LIGHT_START) r.light_start = q.light_start;
+            if (q.present & DS_REC_LIGHT_END) r.light_end = q.light_end;
+            if (q.present & DS_REC_HEAVY_START) r.heavy_start = q.heavy_start;
+            if (q.present & DS_REC_HEAVY_END) r.heavy_end = q.heavy_end;
+            if (q.present & DS_REC_COMPLETION) r.completion = q.completion;
+            if (q.present & DS_REC_OUTCOME) r.outcome = static_cast<Outcome>(q.outcome);
+            if (q.present & DS_REC_DELIVERED_QUALITY) r.delivered_quality = q.delivered_quality;
+        }
+        std::vector<PlanLogEntry> ps(static_cast<size_t>(np));
+        for (int64_t i = 0; i < np; ++i) {
+            ps[static_cast<size_t>(i)].tick = pl[i].tick;
+            ps[static_cast<size_t>(i)].time = pl[i].time;
+            ps[static_cast<size_t>(i)].demand_estimated = pl[i].demand_estimated;
+            ps[static_cast<size_t>(i)].plan = to_plan(pl[i].plan);
+        }
+        write_csv(dir, ivs, rs, ps);
         return 0;
     } catch (...) {
         return map_exception();

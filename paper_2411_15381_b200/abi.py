@@ -66,6 +66,25 @@ QUERY = np.dtype(
     [("id", "<u8"), ("arrival", "<f8"), ("deadline", "<f8"), ("quality_light", "<f8"),
      ("quality_heavy", "<f8"), ("confidence", "<f8")], align=True)
 
+# ds_outcome / DS_REC_* (QueryRecord optionals, metrics.hpp:12-36)
+OUTCOMES = ("served_light", "served_heavy", "dropped", "late")
+REC_LIGHT_START, REC_LIGHT_END, REC_HEAVY_START, REC_HEAVY_END = 0x01, 0x02, 0x04, 0x08
+REC_COMPLETION, REC_OUTCOME, REC_DELIVERED_QUALITY = 0x10, 0x20, 0x40
+QUERY_RECORD = np.dtype(
+    [("id", "<u8"), ("arrival", "<f8"), ("deadline", "<f8"), ("confidence", "<f8"),
+     ("quality_light", "<f8"), ("quality_heavy", "<f8"), ("light_start", "<f8"),
+     ("light_end", "<f8"), ("heavy_start", "<f8"), ("heavy_end", "<f8"), ("completion", "<f8"),
+     ("delivered_quality", "<f8"), ("present", "<u4"), ("outcome", "<i4")], align=True)
+INTERVAL_SNAPSHOT = np.dtype(
+    [("interval_start", "<f8"), ("demand_observed", "<f8"), ("demand_estimated", "<f8"),
+     ("plan", PLAN), ("arrived", "<u8"), ("served_light", "<u8"), ("served_heavy", "<u8"),
+     ("dropped", "<u8"), ("late", "<u8"), ("threshold", "<f8"),
+     ("mean_delivered_quality", "<f8"), ("has_mean_delivered_quality", "<i4"),
+     ("_pad", "<i4")], align=True)
+PLAN_LOG_ENTRY = np.dtype(
+    [("tick", "<i4"), ("_pad", "<i4"), ("time", "<f8"), ("demand_estimated", "<f8"),
+     ("plan", PLAN)], align=True)
+
 assert MODEL_PROFILE.itemsize == 776
 assert CURVE.itemsize == 816
 assert CASCADE.itemsize == 2376
@@ -73,6 +92,9 @@ assert PROBLEM.itemsize == 96
 assert PLAN.itemsize == 32
 assert QUERY_MODEL.itemsize == 40
 assert QUERY.itemsize == 48
+assert QUERY_RECORD.itemsize == 104
+assert INTERVAL_SNAPSHOT.itemsize == 120
+assert PLAN_LOG_ENTRY.itemsize == 56
 
 
 def ptr(a: np.ndarray | None) -> ctypes.c_void_p:

@@ -25,7 +25,7 @@ __all__ = ["ModelProfile", "DeferralCurve", "CascadeProfile", "QueueState", "All
            "observe_confidences", "route", "InvalidArgument", "DomainError", "InvariantError",
            "OutOfRange", "CapacityError", "default_context", "Policy", "make_policy",
            "PolicyParams", "Trace", "POISSON", "UNIFORM", "generate_arrivals",
-           "sample_query_records"]
+           "sample_query_records", "fmt6", "write_csv"]
 
 _ctx: Context | None = None
 
@@ -257,6 +257,26 @@ def sample_query_records(model: QueryOutcomeModel, arrivals, slo_seconds: float,
     (abi.QUERY) for ids id0.. at the given arrivals, on the GPU (K4)."""
     return (ctx or default_context()).sample_query_records(model.pod(), arrivals, slo_seconds,
                                                            id0)
+
+
+def fmt6(v: float) -> str:
+    """metrics.cpp:67-71 ("%.6g"), computed on the GPU (K9)."""
+    return default_context().format_g6([v])[0].decode()
+
+
+def write_csv(out_dir: str, intervals: np.ndarray, records: np.ndarray, plans: np.ndarray,
+              ctx: Context | None = None) -> None:
+    """write_csv (metrics.cpp:91-127): intervals.csv, queries.csv, plans.csv in
+    out_dir, rows formatted on the GPU (K9) from abi.INTERVAL_SNAPSHOT /
+    abi.QUERY_RECORD / abi.PLAN_LOG_ENTRY arrays; byte-identical files."""
+    import os
+    c = ctx or default_context()
+    os.makedirs(out_dir, exist_ok=True)
+    for name, data in (("intervals.csv", c.format_intervals_csv(intervals)),
+                       ("queries.csv", c.format_queries_csv(records)),
+                       ("plans.csv", c.format_plans_csv(plans))):
+        with open(os.path.join(out_dir, name), "wb") as f:
+            f.write(data)
 
 
 def observe_confidences(curve: DeferralCurve, conf, decay: float) -> DeferralCurve:

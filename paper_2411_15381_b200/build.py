@@ -25,8 +25,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-Xptxas"
 EXACT_FP64 = {"plan_sweep.cu", "latent.cu", "curve.cu", "route.cu", "arrivals.cu"}
 
 SOURCES = ["ds_ctx.cu", "plan_sweep.cu", "latent.cu", "route.cu", "curve.cu", "disc.cu",
-           "synth.cu", "arrivals.cu"]
-HEADERS = ["ds_internal.h", "sm100.cuh", "fdlibm_log1p.h"]
+           "synth.cu", "arrivals.cu", "csv.cu"]
+HEADERS = ["ds_internal.h", "sm100.cuh", "fdlibm_log1p.h", "fmt6.h"]
 
 
 def _mtime(p: str) -> float:

@@ -95,6 +95,12 @@ SIGNATURES = [
                                                    ctypes.POINTER(i64), c_p]),
     ("ds_sample_queries", ctypes.c_int, [c_p, c_p, u64, c_p, i64, f64, c_p]),
     ("ds_sample_queries_device", ctypes.c_int, [c_p, c_p, u64, c_p, i64, f64, c_p, c_p]),
+    ("ds_format_queries_csv", ctypes.c_int, [c_p, c_p, i64, c_p, i64, ctypes.POINTER(i64)]),
+    ("ds_format_intervals_csv", ctypes.c_int, [c_p, c_p, i64, c_p, i64, ctypes.POINTER(i64)]),
+    ("ds_format_plans_csv", ctypes.c_int, [c_p, c_p, i64, c_p, i64, ctypes.POINTER(i64)]),
+    ("ds_format_queries_csv_device", ctypes.c_int, [c_p, c_p, i64, c_p, i64,
+                                                    ctypes.POINTER(i64), c_p]),
+    ("ds_format_g6", ctypes.c_int, [c_p, c_p, i64, c_p]),
 ]
 
 
@@ -194,6 +200,32 @@ class Context:
         out = np.zeros(len(arrivals), abi.QUERY)
         check(lib().ds_sample_queries(self.handle, abi.ptr(model), id0, abi.ptr(arrivals),
                                       len(arrivals), float(slo_seconds), abi.ptr(out)))
+        return out
+
+    # ---- CSV output ------------------------------------------------------
+    def _format_csv(self, fn: str, rows: np.ndarray, dtype) -> bytes:
+        rows = np.ascontiguousarray(rows, dtype)
+        n = i64(0)
+        f = getattr(lib(), fn)
+        check(f(self.handle, abi.ptr(rows), len(rows), None, 0, ctypes.byref(n)))
+        out = np.zeros(max(n.value, 1), np.uint8)
+        check(f(self.handle, abi.ptr(rows), len(rows), abi.ptr(out), len(out), ctypes.byref(n)))
+        return out[:n.value].tobytes()
+
+    def format_queries_csv(self, records: np.ndarray) -> bytes:
+        return self._format_csv("ds_format_queries_csv", records, abi.QUERY_RECORD)
+
+    def format_intervals_csv(self, rows: np.ndarray) -> bytes:
+        return self._format_csv("ds_format_intervals_csv", rows, abi.INTERVAL_SNAPSHOT)
+
+    def format_plans_csv(self, rows: np.ndarray) -> bytes:
+        return self._format_csv("ds_format_plans_csv", rows, abi.PLAN_LOG_ENTRY)
+
+    def format_g6(self, values) -> np.ndarray:
+        """fmt6 of each value as 16-byte NUL-padded slots (np.dtype('S16'))."""
+        values = np.ascontiguousarray(values, np.float64)
+        out = np.zeros(len(values), "S16")
+        check(lib().ds_format_g6(self.handle, abi.ptr(values), len(values), abi.ptr(out)))
         return out
 
     # ---- router ---------------------------------------------------------

@@ -247,3 +247,98 @@ int main(void) {
                    check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout
+
+
+def _compile_and_run(tmp_path, name, source, defines=()):
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / f"{name}.c"
+    src.write_text(source)
+    exe = tmp_path / name
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", *[f"-D{d}" for d in defines],
+                    f"-I{root}/paper_2411_15381_b200/csrc", str(src), "-o", str(exe), "-lm"],
+                   check=True)
+    return subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+
+
+FMT6_PROGRAM = r'''
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+#include "fmt6.h"
+static uint64_t rs = 88172645463325252ull;
+static uint64_t xr(void) { rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17; return rs; }
+static double pick(long i) {
+    double x; uint64_t b;
+    switch (i % 8) {
+    case 0: b = xr(); memcpy(&x, &b, 8); return x;
+    case 1: return ldexp((double)(xr() >> 11), -53) * pow(10.0, (double)(xr() % 16) - 8);
+    case 2: return (double)(xr() % 100000000) / (double)ds_pow10_u64(xr() % 12);
+    case 3: return (double)(xr() % 20000000);
+    case 4: { double p = pow(10.0, (double)((int)(xr() % 40) - 20)); memcpy(&b, &p, 8);
+              b += (int)(xr() % 7) - 3; memcpy(&x, &b, 8); return x; }
+    case 5: return ldexp((double)(xr() >> 11), (int)(xr() % 2200) - 1127);
+    case 6: return -((double)(xr() % 1000000) + 0.5) * pow(10.0, (double)((int)(xr() % 14) - 10));
+    default: return (double)(xr() >> 11) * 0x1.0p-53 * 3600.0;
+    }
+}
+int main(void) {
+    long n = N, bad = 0;
+    char a[64], b[64];
+    for (long i = 0; i < n; i++) {
+        double x = pick(i);
+        snprintf(a, sizeof a, "%.6g", x);
+        int k = ds_fmt_g6(x, b);
+        b[k] = 0;
+        if (strcmp(a, b)) { if (bad < 5) printf("%a: libc=%s restated=%s\n", x, a, b); bad++; }
+    }
+    printf("bad=%ld\n", bad);
+    return bad != 0;
+}
+'''
+
+
+@pytest.mark.parametrize("path", ["fast", "big"])
+def test_fmt6_restatement_matches_host_printf(tmp_path, path):
+    """paper_2411_15381_b200/csrc/fmt6.h (the device's "%.6g", metrics.cpp:67-71)
+    compiled for the host equals the host snprintf byte for byte: 4M doubles
+    through the 128-bit fast path, 1M with the 1280-bit path forced."""
+    defines = ["N=4000000"] if path == "fast" else ["N=1000000", "DS_FMT_FORCE_BIG"]
+    r = _compile_and_run(tmp_path, "fmt6", FMT6_PROGRAM, defines)
+    assert r.returncode == 0, r.stdout
+
+
+def test_port_csv_matches_reference_goldens(golden):
+    """dso_format_*_csv (C restatement of write_csv, metrics.cpp:91-127) and
+    dso_fmt6 reproduce the bytes the reference wrote."""
+    g = golden("csv")
+    port = lib.port()
+    for name, key in (("queries", "records"), ("intervals", "intervals"), ("plans", "plans")):
+        rows = np.ascontiguousarray(g[key])
+        fn = getattr(port, f"dso_format_{name}_csv")
+        n = fn(P(rows), len(rows), None, 0)
+        out = np.zeros(n, np.uint8)
+        assert fn(P(rows), len(rows), P(out), n) == n
+        assert out.tobytes() == g[f"{name}_csv"].tobytes(), name
+    vals = np.ascontiguousarray(g["g6_values"])
+    txt = np.zeros(len(vals), "S16")
+    port.dso_fmt6(P(vals), len(vals), P(txt))
+    assert np.array_equal(txt, g["g6_text"])
+
+
+@needs_ref
+def test_port_csv_vs_reference_fresh(tmp_path):
+    from tests import helpers
+    rng = np.random.default_rng(77)
+    q = helpers.random_query_records(rng, 20000)
+    iv = helpers.random_intervals(rng, 500)
+    pl = helpers.random_plan_log(rng, 500)
+    assert lib.ref().dsref_write_csv(str(tmp_path).encode(), P(iv), len(iv), P(q), len(q), P(pl),
+                                     len(pl)) == 0
+    for name, rows in (("queries", q), ("intervals", iv), ("plans", pl)):
+        fn = getattr(lib.port(), f"dso_format_{name}_csv")
+        n = fn(P(rows), len(rows), None, 0)
+        out = np.zeros(n, np.uint8)
+        fn(P(rows), len(rows), P(out), n)
+        assert out.tobytes() == (tmp_path / f"{name}.csv").read_bytes(), name
