@@ -19,6 +19,7 @@ Secondary legs in the same JSON line:
             route at t = 0.5 + curve replay over 1M queries per GPU (config 5).
   workload: generate_arrivals over a 1M-arrival Poisson trace (K8, bit-exact)
             + the Query records at those arrivals (K4 records); replicas per GPU.
+  csv     : queries.csv bytes of 1M QueryRecords (K9, byte-identical to write_csv).
 CPU baselines run on this box's host cores on bounded samples (rank 0, N=1).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
@@ -54,6 +55,8 @@ CPU_PLAN_SAMPLE = 256         # problems for the CPU reference planner
 CPU_LATENT_SAMPLE = 200_000   # queries for the CPU reference scorer
 WL_RATES = [2500.0] * 400     # 400 s at 2,500 qps: 1,000,811 arrivals at seed 3
 WL_SEED = 3
+N_CSV = 1_000_000
+CPU_CSV_SAMPLE = 200_000      # records through the reference's write_csv
 
 
 def load_peaks():
@@ -230,6 +233,32 @@ def cpu_workload_leg(threads):
         lib.port().dso_sample_queries(abi.ptr(m), 0, n, abi.ptr(conf), None, threads)
     t_q = time.perf_counter() - t0
     return n / (t_arr + t_q), n / t_arr, ("reference" if use_ref else "port"), a
+
+
+def csv_records(n):
+    from tests import helpers
+    return helpers.random_query_records(np.random.default_rng(12), n)
+
+
+def cpu_csv_leg(records):
+    """The reference's write_csv (metrics.cpp:91-127) on the records, into a
+    temporary directory (the port's snprintf formatter where it is absent)."""
+    import tempfile
+    from oracle import lib
+    from paper_2411_15381_b200 import abi
+    iv = np.zeros(0, abi.INTERVAL_SNAPSHOT)
+    pl = np.zeros(0, abi.PLAN_LOG_ENTRY)
+    if lib.ref_available():
+        with tempfile.TemporaryDirectory() as tmp:
+            t0 = time.perf_counter()
+            lib.ref().dsref_write_csv(tmp.encode(), abi.ptr(iv), 0, abi.ptr(records),
+                                      len(records), abi.ptr(pl), 0)
+            return len(records) / (time.perf_counter() - t0), "reference"
+    n = lib.port().dso_format_queries_csv(abi.ptr(records), len(records), None, 0)
+    out = np.zeros(n, np.uint8)
+    t0 = time.perf_counter()
+    lib.port().dso_format_queries_csv(abi.ptr(records), len(records), abi.ptr(out), n)
+    return len(records) / (time.perf_counter() - t0), "port"
 
 
 def host_weights():
@@ -560,6 +589,35 @@ def run_gpu(args):
     wl_value = ws * wl_count / (allmax([sum(wl_ms)])[0] / 1000.0)
     wl_arr_value = ws * wl_count / (allmax([wl_ms[0]])[0] / 1000.0)
 
+    # ---- csv leg: queries.csv of 1M records (K9) ------------------------------
+    crec = csv_records(N_CSV)
+    drec = torch.from_numpy(crec.view(np.uint8).copy()).to(dev)
+    csv_cap = N_CSV * 256 + 4096
+    dcsv = torch.empty(csv_cap, dtype=torch.uint8, device=dev)
+    csv_n = native.i64(0)
+    cevs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def csv_step(ev=False):
+        with torch.cuda.stream(stream):
+            if ev:
+                cevs[0].record(stream)
+            native.check(L.ds_format_queries_csv_device(
+                ctx.handle, native.c_p(drec.data_ptr()), N_CSV, native.c_p(dcsv.data_ptr()),
+                csv_cap, native.ctypes.byref(csv_n), native.c_p(ctx.stream)))
+            if ev:
+                cevs[1].record(stream)
+    csv_step()
+    torch.cuda.synchronize()
+    csv_ms = 0.0
+    for _ in range(3):
+        csv_step(ev=True)
+        torch.cuda.synchronize()
+        csv_ms += cevs[0].elapsed_time(cevs[1]) / 3
+    csv_value = ws * N_CSV / (allmax([csv_ms])[0] / 1000.0)
+    t0 = time.perf_counter()
+    csv_bytes = ctx.format_queries_csv(crec)
+    csv_e2e = ws * N_CSV / allmax([time.perf_counter() - t0])[0]
+
     if rank == 0:
         peaks, peak_src = load_peaks()
         achieved_tflops = N_IMG * DISC_FLOP_PER_IMG / (disc_ms / 1000.0) / 1e12
@@ -601,6 +659,12 @@ def run_gpu(args):
                          "arrivals_per_s": wl_arr_value, "arrivals_per_gpu": wl_count,
                          "ms_arrivals_records": wl_ms,
                          "trace": "400 intervals x 2500 qps, Poisson, seed 3 (replica per GPU)"},
+            "csv": {"value": csv_value, "unit": "rows/s", "rows_per_gpu": N_CSV,
+                    "bytes": csv_n.value, "ms": csv_ms,
+                    "e2e": {"value": csv_e2e, "unit": "rows/s",
+                            "note": "host records in, host bytes out (ds_format_queries_csv)"},
+                    "parity_device_vs_host": bool(
+                        dcsv[:csv_n.value].cpu().numpy().tobytes() == csv_bytes)},
         }
         if ws == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
@@ -629,6 +693,10 @@ def run_gpu(args):
                 "value": wv, "unit": "queries/s", "arrivals_per_s": wav, "cores": threads,
                 "kind": wk, "sample": f"the full {len(wa)}-arrival trace: generate_arrivals "
                                       f"(sequential) + sample_query on {threads} threads"}
+            cv2, ck2 = cpu_csv_leg(np.ascontiguousarray(crec[:CPU_CSV_SAMPLE]))
+            line["csv"]["cpu_baseline"] = {
+                "value": cv2, "unit": "rows/s", "cores": 1, "kind": ck2,
+                "sample": f"{CPU_CSV_SAMPLE} QueryRecords through write_csv (file in a tmp dir)"}
             got = wl_arr[:wl_count].cpu().numpy()
             line["workload"]["parity_vs_cpu"] = bool(
                 len(wa) == wl_count and got.tobytes() == wa.tobytes())
