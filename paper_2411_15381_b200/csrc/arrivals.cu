@@ -9,11 +9,10 @@
 // to nextafter(previous, +inf) when it does not increase, and stops at the
 // first t >= duration. Every piece is restated as a data-parallel pass:
 //
-//   K8a mt_stream   one warp runs the single std::mt19937_64 stream. Word m of
+//   K8a mt_stream   one CTA runs the single std::mt19937_64 stream. Word m of
 //                   the stream obeys x_m = x_{m-156} ^ twist(x_{m-312},
-//                   x_{m-311}); lane l owns columns 5l..5l+4 (mod 156) in
-//                   registers, so a step of 156 words needs one shuffle and no
-//                   shared memory on the dependency chain.
+//                   x_{m-311}); thread c owns column c (mod 156), two steps
+//                   of 156 words per barrier.
 //   K8b exp_draws   grid-wide: temper, U = (u64 >> 11) * 2^-53,
 //                   e = -log1p(-U) with glibc's log1p restated bit for bit
 //                   (fdlibm_log1p.h; rng.cpp:24-28).
@@ -21,7 +20,8 @@
 //                   T_i = fl(T_{i-1} + e_i) as an EXACT integer scan. While the
 //                   accumulator stays in one binade [2^p, 2^(p+1)) with ulp u,
 //                   fl(M*u + e) = (M + rint(e/u)) * u, so a tile of 8192 steps is
-//                   an int64 prefix sum. The first step that could leave the
+//                   an int64 prefix sum (no int<->double conversions: M and
+//                   the results are the accumulator's own bit patterns). The first step that could leave the
 //                   binade (or is a rounding tie, whose direction depends on the
 //                   accumulator's parity) is done as one real fp64 add and the
 //                   tile restarts after it: ~log2(N) restarts in total.
@@ -51,9 +51,6 @@
 
 namespace {
 
-constexpr int kSumThreads = 1024;
-constexpr int kSumPer = 8;
-constexpr int kSumTile = kSumThreads * kSumPer;
 constexpr int kPlaceThreads = 512;
 constexpr long long kNoIndex = 0x7fffffffffffffffLL;
 
@@ -87,50 +84,53 @@ __device__ __forceinline__ uint64_t temper(uint64_t z) {
 }
 
 // ---- K8a: the single mt19937_64 stream, untempered words x_312 .. -----------
-// raw[k] = x_{312+k}; output k of the engine is temper(raw[k]).
-__global__ void __launch_bounds__(32) mt_stream_kernel(uint64_t seed, int64_t n,
-                                                       uint64_t* __restrict__ raw) {
-    __shared__ uint64_t init[312];
-    const int lane = threadIdx.x;
-    if (lane == 0) {   // std::mt19937_64 seeding recurrence
+// raw[k] = x_{312+k}; output k of the engine is temper(raw[k]). Thread c owns
+// column c (mod 156) and keeps its last two words in registers; the only
+// cross-thread input, x_{m-311} (column c+1 two steps back; column 0 one step
+// back for c = 155), comes from a 4-step shared ring. Two steps per barrier:
+// the second step's neighbour for c = 155 (column 0 of the first new step) is
+// recomputed by that thread from words already in the ring.
+constexpr int kMtThreads = 160;
+__global__ void __launch_bounds__(kMtThreads) mt_stream_kernel(uint64_t seed, int64_t n,
+                                                               uint64_t* __restrict__ raw) {
+    __shared__ uint64_t ring[4][156];   // ring[step & 3][column]
+    const int c = threadIdx.x;
+    if (c == 0) {   // std::mt19937_64 seeding recurrence: steps 0 and 1
         uint64_t x = seed;
-        init[0] = x;
+        ring[0][0] = x;
         for (int i = 1; i < 312; ++i) {
             x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
-            init[i] = x;
+            ring[i / 156][i % 156] = x;
         }
     }
-    __syncwarp();
-    // Column c = 5*lane + q (c < 156). x2 = step s-2, x1 = step s-1.
-    uint64_t x2[5], x1[5];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-        const int c = 5 * lane + q;
-        x2[q] = c < 156 ? init[c] : 0;
-        x1[q] = c < 156 ? init[156 + c] : 0;
-    }
+    __syncthreads();
+    const bool active = c < 156;
+    uint64_t x2 = active ? ring[0][c] : 0;   // step s
+    uint64_t x1 = active ? ring[1][c] : 0;   // step s+1
     const int64_t steps = (n + 155) / 156;
-    for (int64_t s = 0; s < steps; ++s) {
-        // x_{m-311} for column c is column c+1 of step s-2 (lane+1's q=0 for
-        // q=4); for c = 155 (lane 31, q = 0) it is column 0 of step s-1.
-        const uint64_t nb2 = __shfl_down_sync(0xffffffffu, x2[0], 1);
-        const uint64_t c0_1 = __shfl_sync(0xffffffffu, x1[0], 0);
-        uint64_t nx[5];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            uint64_t nbr;
-            if (q < 4) nbr = x2[q + 1];
-            else nbr = nb2;
-            if (lane == 31 && q == 0) nbr = c0_1;
-            nx[q] = x1[q] ^ mt_mix(x2[q], nbr);
+    for (int64_t s = 0; s < steps; s += 2) {
+        const int a = static_cast<int>(s & 3), b = (a + 1) & 3, w0 = (a + 2) & 3, w1 = (a + 3) & 3;
+        if (active) {
+            uint64_t nb_a, nb_b;
+            if (c < 155) {
+                nb_a = ring[a][c + 1];   // column c+1, step s
+                nb_b = ring[b][c + 1];   // column c+1, step s+1
+            } else {
+                nb_a = ring[b][0];       // column 0, step s+1
+                // column 0 of step s+2, recomputed: x_{m-156} ^ twist(x_{m-312}, x_{m-311})
+                nb_b = ring[b][0] ^ mt_mix(ring[a][0], ring[a][1]);
+            }
+            const uint64_t y0 = x1 ^ mt_mix(x2, nb_a);   // step s+2
+            const uint64_t y1 = y0 ^ mt_mix(x1, nb_b);   // step s+3
+            ring[w0][c] = y0;
+            ring[w1][c] = y1;
+            const int64_t k0 = s * 156 + c;
+            if (k0 < n) raw[k0] = y0;
+            if (k0 + 156 < n) raw[k0 + 156] = y1;
+            x2 = y0;
+            x1 = y1;
         }
-        const int64_t k0 = s * 156 + 5 * lane;
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            if (5 * lane + q < 156 && k0 + q < n) raw[k0 + q] = nx[q];
-            x2[q] = x1[q];
-            x1[q] = nx[q];
-        }
+        __syncthreads();
     }
 }
 
@@ -149,114 +149,151 @@ __global__ void __launch_bounds__(256) exp_draws_kernel(const uint64_t* raw, int
 }
 
 // ---- K8c: exact sequentially rounded running sum -----------------------------
-__device__ __forceinline__ unsigned long long block_exclusive_sum(unsigned long long v,
-                                                                  unsigned long long* warp_tot,
-                                                                  unsigned long long* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned long long inc = v;
+// The accumulator acc = M * 2^(p-52), M in [2^52, 2^53), is kept as its bit
+// pattern: M is the mantissa with the hidden bit and any P in [2^52, 2^53)
+// maps back to the double with the same exponent field, so the scan never
+// converts between integers and doubles. Each thread scans 16 consecutive
+// steps; tiles move through shared memory (padded, double-buffered) so global
+// loads and stores stay coalesced.
+constexpr int kSumThreads = 512;
+constexpr int kSumPer = 16;
+constexpr int kSumTile = kSumThreads * kSumPer;
+constexpr int kSumPad = kSumTile + kSumTile / kSumPer;   // one pad slot per 16
+constexpr size_t kSumSmem = 2 * kSumPad * sizeof(double);
+
+__device__ __forceinline__ int pad_idx(int x) { return x + x / kSumPer; }
+
+__device__ __forceinline__ double from_binade(unsigned long long P, unsigned long long ebits) {
+    return __longlong_as_double(static_cast<long long>(ebits + (P - (1ULL << 52))));
+}
+
+// striped (coalesced) global loads of the tile starting at `start`
+__device__ __forceinline__ void load_striped(const double* __restrict__ e, int64_t n,
+                                             int64_t start, double (&v)[kSumPer]) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
+    for (int q = 0; q < kSumPer; ++q) {
+        const int64_t j = start + q * kSumThreads + threadIdx.x;
+        v[q] = j < n ? __ldcg(e + j) : 0.0;
     }
-    if (lane == 31) warp_tot[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        unsigned long long w = warp_tot[lane];
-        unsigned long long wi = w;
+}
+
+__global__ void __launch_bounds__(kSumThreads, 1)
+target_sum_kernel(const double* __restrict__ e, int64_t n, double* __restrict__ T) {
+    extern __shared__ double sbuf_all[];
+    __shared__ unsigned long long s_wsum[2][kSumThreads / 32];
+    __shared__ unsigned s_wmin[2][kSumThreads / 32];
+    __shared__ double s_acc;
+    constexpr int kWarps = kSumThreads / 32;
+    constexpr unsigned long long kLimit = (1ULL << 53) - 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double acc = __ldcg(e);
+    if (tid == 0) T[0] = acc;
+    int64_t i = 1;
+    int par = 0;
+    double st[kSumPer];   // striped values of the tile at i
+    load_striped(e, n, i, st);
+    while (i < n) {
+        double* sbuf = sbuf_all + par * kSumPad;
+        const int tile_len = (n - i < kSumTile) ? static_cast<int>(n - i) : kSumTile;
+#pragma unroll
+        for (int q = 0; q < kSumPer; ++q) sbuf[pad_idx(q * kSumThreads + tid)] = st[q];
+        // speculative prefetch of the next tile (correct unless a restart happens)
+        load_striped(e, n, i + kSumTile, st);
+        __syncthreads();
+        double ev[kSumPer];
+#pragma unroll
+        for (int q = 0; q < kSumPer; ++q) ev[q] = sbuf[pad_idx(tid * kSumPer + q)];
+
+        const unsigned long long ab = static_cast<unsigned long long>(__double_as_longlong(acc));
+        const int bexp = static_cast<int>(ab >> 52);             // acc >= 0
+        const bool scan_ok = bexp >= 1023 - 60 && bexp <= 1023 + 500;
+        const unsigned long long ebits = static_cast<unsigned long long>(bexp) << 52;
+        const unsigned long long M = (ab & ((1ULL << 52) - 1)) | (1ULL << 52);
+        // 2^(52-p), p = bexp - 1023
+        const double scale =
+            __longlong_as_double(static_cast<long long>(scan_ok ? 2098 - bexp : 1023) << 52);
+        unsigned long long r[kSumPer];
+        unsigned long long mine = 0;
+        int bad_q = kSumPer;
+#pragma unroll
+        for (int q = 0; q < kSumPer; ++q) {
+            const double y = __dmul_rn(ev[q], scale);           // exact power-of-two scaling
+            const double t = __dadd_rn(y, 0x1.0p52);            // rint(y), ties to even
+            const unsigned long long rr = static_cast<unsigned long long>(__double_as_longlong(t)) -
+                                          0x4330000000000000ULL;
+            const double d = __dsub_rn(__dsub_rn(t, 0x1.0p52), y);   // exact
+            const bool bad = !scan_ok || !(y < 0x1.0p52) || d == 0.5 || d == -0.5;
+            const bool in = tid * kSumPer + q < tile_len;
+            if (in && bad && bad_q == kSumPer) bad_q = q;
+            r[q] = (in && !bad) ? rr : 0;
+            mine += r[q];
+        }
+        // block exclusive scan of the per-thread sums
+        unsigned long long inc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) s_wsum[par][warp] = inc;
+        __syncthreads();
+        const unsigned long long wv = lane < kWarps ? s_wsum[par][lane] : 0;
+        unsigned long long wi = wv;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
             if (lane >= o) wi += t;
         }
-        warp_tot[lane] = wi - w;   // exclusive prefix of warps
-        if (lane == 31) *total = wi;
-    }
-    __syncthreads();
-    return warp_tot[warp] + inc - v;
-}
-
-__global__ void __launch_bounds__(kSumThreads) target_sum_kernel(const double* __restrict__ e,
-                                                                 int64_t n,
-                                                                 double* __restrict__ T) {
-    __shared__ unsigned long long warp_tot[32];
-    __shared__ unsigned long long s_total;
-    __shared__ long long s_first;
-    __shared__ double s_acc;
-    const int tid = threadIdx.x;
-    double acc = e[0];
-    if (tid == 0) T[0] = acc;
-    int64_t i = 1;
-    constexpr unsigned long long kLimit = (1ULL << 53) - 2;
-    while (i < n) {
-        // Binade of the accumulator: acc = M * u, M in [2^52, 2^53).
-        const bool scan_ok = acc >= 0x1.0p-60 && acc < 0x1.0p+500;
-        int p = 0;
-        double scale = 0.0, ulp = 0.0;
-        unsigned long long M = 0;
-        if (scan_ok) {
-            p = static_cast<int>((__double_as_longlong(acc) >> 52) & 0x7ff) - 1023;
-            scale = __longlong_as_double(static_cast<long long>(52 - p + 1023) << 52);
-            ulp = __longlong_as_double(static_cast<long long>(p - 52 + 1023) << 52);
-            M = static_cast<unsigned long long>(__dmul_rn(acc, scale));
-        }
-        const int64_t base = i + static_cast<int64_t>(tid) * kSumPer;
-        unsigned long long r[kSumPer];
-        unsigned long long mine = 0;
-        long long first_bad = kNoIndex;
-#pragma unroll
-        for (int q = 0; q < kSumPer; ++q) {
-            const int64_t j = base + q;
-            r[q] = 0;
-            if (j < n) {
-                const double y = __dmul_rn(e[j], scale);   // exact power-of-two scaling
-                const double fl = floor(y);
-                const double fr = __dsub_rn(y, fl);
-                const bool bad = !scan_ok || !(y < 0x1.0p53) || fr == 0.5;
-                if (bad && first_bad == kNoIndex) first_bad = j;
-                r[q] = bad ? 0 : static_cast<unsigned long long>(fl) + (fr > 0.5 ? 1 : 0);
-            }
-            mine += r[q];
-        }
-        const unsigned long long excl = block_exclusive_sum(mine, warp_tot, &s_total);
-        // First step whose result could leave the binade.
+        const unsigned long long wex = __shfl_sync(0xffffffffu, wi - wv, warp);
+        const unsigned long long tot = __shfl_sync(0xffffffffu, wi, 31);
+        const unsigned long long excl = wex + inc - mine;
+        // first step that is a tie, out of range, or could leave the binade
+        unsigned vloc = 0xffffffffu;
         unsigned long long P = M + excl;
 #pragma unroll
         for (int q = 0; q < kSumPer; ++q) {
-            const int64_t j = base + q;
             P += r[q];
-            if (j < n && P > kLimit && j < first_bad) first_bad = j;
+            const bool in = tid * kSumPer + q < tile_len;
+            if (in && (q == bad_q || P > kLimit) && vloc == 0xffffffffu)
+                vloc = static_cast<unsigned>(tid * kSumPer + q);
         }
-        if (tid == 0) s_first = kNoIndex;
+        const unsigned wmin = __reduce_min_sync(0xffffffffu, vloc);
+        if (lane == 0) s_wmin[par][warp] = wmin;
         __syncthreads();
-        if (first_bad != kNoIndex) atomicMin(&s_first, first_bad);
-        __syncthreads();
-        const long long v = s_first;
-        const int64_t tile_end = (i + kSumTile < n) ? i + kSumTile : n;
+        const unsigned v = __reduce_min_sync(0xffffffffu,
+                                             lane < kWarps ? s_wmin[par][lane] : 0xffffffffu);
+        // T for the steps before v back into shared memory (blocked), the one
+        // real add fl(T_{v-1} + e_v) by v's owner
         P = M + excl;
+        double prev = tid == 0 ? acc : from_binade(P, ebits);
 #pragma unroll
         for (int q = 0; q < kSumPer; ++q) {
-            const int64_t j = base + q;
-            P += r[q];
-            if (j < n && j < v) T[j] = __dmul_rn(static_cast<double>(P), ulp);
-            if (j == tile_end - 1 && v >= tile_end) s_acc = __dmul_rn(static_cast<double>(P), ulp);
-        }
-        __syncthreads();   // T[v-1] (or s_acc) visible to thread 0
-        if (v < tile_end) {
-            if (tid == 0) {
-                const double prev = (v == i) ? acc : T[v - 1];
-                const double t = __dadd_rn(prev, e[v]);   // the reference's own add
-                T[v] = t;
+            const unsigned rel = static_cast<unsigned>(tid * kSumPer + q);
+            if (rel == v) {
+                const double t = __dadd_rn(rel == 0 ? acc : prev, ev[q]);
+                sbuf[pad_idx(rel)] = t;
                 s_acc = t;
             }
-            __syncthreads();
-            acc = s_acc;
-            i = v + 1;
-        } else {
-            acc = s_acc;
-            i = tile_end;
+            P += r[q];
+            prev = from_binade(P, ebits);
+            if (rel < v) sbuf[pad_idx(rel)] = prev;
         }
         __syncthreads();
+        const int nout = v < static_cast<unsigned>(tile_len) ? static_cast<int>(v) + 1 : tile_len;
+#pragma unroll
+        for (int q = 0; q < kSumPer; ++q) {
+            const int rel = q * kSumThreads + tid;
+            if (rel < nout) T[i + rel] = sbuf[pad_idx(rel)];
+        }
+        par ^= 1;
+        if (v < static_cast<unsigned>(tile_len)) {
+            acc = s_acc;
+            i += static_cast<int64_t>(v) + 1;
+            load_striped(e, n, i, st);
+        } else {
+            acc = from_binade(M + tot, ebits);
+            i += tile_len;
+        }
     }
 }
 
@@ -494,13 +531,16 @@ ds_status generate(ds_ctx* ctx, const double* rates, int32_t n_rates, double dt,
             // RandomStream(seed, "arrivals") (rng.hpp:20-21)
             const uint64_t eng = splitmix64(seed ^ splitmix64(fnv1a("arrivals")));
             uint64_t* raw = reinterpret_cast<uint64_t*>(e);
-            mt_stream_kernel<<<1, 32, 0, st>>>(eng, D, raw);
+            mt_stream_kernel<<<1, kMtThreads, 0, st>>>(eng, D, raw);
             DS_LAUNCH_CHECK(ctx, "mt_stream_kernel");
             int64_t blocks = (D + 255) / 256;
             if (blocks > 148 * 16) blocks = 148 * 16;
             exp_draws_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(raw, D, e);
             DS_LAUNCH_CHECK(ctx, "exp_draws_kernel");
-            target_sum_kernel<<<1, kSumThreads, 0, st>>>(e, D, T);
+            DS_CUDA_TRY(cudaFuncSetAttribute(target_sum_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kSumSmem)));
+            target_sum_kernel<<<1, kSumThreads, kSumSmem, st>>>(e, D, T);
             DS_LAUNCH_CHECK(ctx, "target_sum_kernel");
         }
         place_kernel<<<static_cast<unsigned>(nb), kPlaceThreads, 0, st>>>(T, D, thr, ip, P, key,
