@@ -18,7 +18,18 @@ namespace {
 constexpr int kThreads = 128;   // 101 bins + total, padded to 4 warps
 constexpr int kChunk = 4096;
 
-template <typename T>
+// m + 1 on a hit, else m. A real (divergent) branch rather than an
+// add-and-select: a bin's thread hits on ~1% of observations, and only the
+// warp holding the hit bin waits for the add.
+__device__ __forceinline__ double add_one_if(double m, bool hit) {
+    if (hit) {
+        asm volatile("" ::: "memory");   // keep the branch (no if-conversion)
+        m = __dadd_rn(m, 1.0);
+    }
+    return m;
+}
+
+template <typename T, bool kScale>
 __global__ void __launch_bounds__(kThreads)
 curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int64_t n,
                      double decay, int* __restrict__ bad) {
@@ -28,7 +39,7 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
     double m = 0.0;
     if (tid < DS_CURVE_BINS) m = curve->bin_mass[tid];
     else if (tid == DS_CURVE_BINS) m = curve->total_mass;
-    const bool scale = decay != 1.0;
+    bool settled = false;
     // the total-mass thread matches every observation; bin threads their own bin
     const unsigned mine = tid < DS_CURVE_BINS ? static_cast<unsigned>(tid) : 0xFFu;
     const bool is_total = tid == DS_CURVE_BINS;
@@ -49,28 +60,47 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
             b = b < 0 ? 0 : (b > DS_CURVE_BINS - 1 ? DS_CURVE_BINS - 1 : b);
             bins[k] = static_cast<unsigned char>(b);
         }
-        for (int k = cnt + tid; k < ((cnt + 7) & ~7); k += kThreads) bins[k] = 254;  // pad
         __syncthreads();
         if (tid <= DS_CURVE_BINS) {
             if (!chunk_bad) {
-                // replay, 8 observations per 64-bit shared load; the hit add is
-                // predicated (a miss must leave m untouched, including -0.0)
-                for (int k = 0; k < cnt; k += 8) {
-                    const uint2 w = *reinterpret_cast<const uint2*>(&bins[k]);
+                if (is_total) {
+                    // every observation hits the total: t <- fl(fl(t*d) + 1). The map is
+                    // deterministic, so once a step leaves t unchanged (t reaches the
+                    // rounded fixed point, ~1/(1-d) after ~40K steps at d = 0.999) every
+                    // later step does too and the replay of the total can stop.
+                    if (!settled) {
+                        for (int k = 0; k < cnt; ++k) {
+                            const double nt = __dadd_rn(kScale ? __dmul_rn(m, decay) : m, 1.0);
+                            if (nt == m) {
+                                settled = true;
+                                break;
+                            }
+                            m = nt;
+                        }
+                    }
+                } else {
+                    // 8 observations per 64-bit shared load; the add on a hit is a
+                    // predicated instruction so a miss costs only the multiply
+                    const int full8 = cnt & ~7;
+                    for (int k = 0; k < full8; k += 8) {
+                        const uint2 w = *reinterpret_cast<const uint2*>(&bins[k]);
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const unsigned b = ((u < 4 ? w.x : w.y) >> (8 * (u & 3))) & 0xFFu;
-                        if (b == 254u) break;           // padding past the last observation
-                        if (scale) m = __dmul_rn(m, decay);
-                        const double a = __dadd_rn(m, 1.0);
-                        m = (is_total || b == mine) ? a : m;
+                        for (int u = 0; u < 8; ++u) {
+                            const unsigned b = ((u < 4 ? w.x : w.y) >> (8 * (u & 3))) & 0xFFu;
+                            if (kScale) m = __dmul_rn(m, decay);
+                            m = add_one_if(m, b == mine);
+                        }
+                    }
+                    for (int k = full8; k < cnt; ++k) {
+                        if (kScale) m = __dmul_rn(m, decay);
+                        m = add_one_if(m, bins[k] == mine);
                     }
                 }
             } else {
                 for (int k = 0; k < cnt; ++k) {
                     const unsigned char b = bins[k];
                     if (b == 255) break;   // the reference throws here; state stops
-                    if (scale) m = __dmul_rn(m, decay);
+                    if (kScale) m = __dmul_rn(m, decay);
                     if (is_total || b == mine) m = __dadd_rn(m, 1.0);
                 }
             }
@@ -88,12 +118,16 @@ ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype,
                  double decay, int* dbad, cudaStream_t st) {
     init_bad<<<1, 1, 0, st>>>(dbad);
     DS_LAUNCH_CHECK(ctx, "init_bad");
-    if (dtype == DS_CONF_F64)
-        curve_observe_kernel<double><<<1, kThreads, 0, st>>>(
-            dcurve, static_cast<const double*>(conf), n, decay, dbad);
-    else
-        curve_observe_kernel<float><<<1, kThreads, 0, st>>>(
-            dcurve, static_cast<const float*>(conf), n, decay, dbad);
+    const bool scale = decay != 1.0;
+    if (dtype == DS_CONF_F64) {
+        const double* c = static_cast<const double*>(conf);
+        if (scale) curve_observe_kernel<double, true><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);
+        else curve_observe_kernel<double, false><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);
+    } else {
+        const float* c = static_cast<const float*>(conf);
+        if (scale) curve_observe_kernel<float, true><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);
+        else curve_observe_kernel<float, false><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);
+    }
     DS_LAUNCH_CHECK(ctx, "curve_observe_kernel");
     return DS_OK;
 }

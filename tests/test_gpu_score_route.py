@@ -157,12 +157,31 @@ def test_curve_replay_large_and_f32_vs_port(ctx):
     want = curve.copy()
     lib.port().dso_curve_observe(abi.ptr(want), abi.ptr(conf), len(conf), 0.999)
     assert np.array_equal(got["bin_mass"].view(np.uint64), want["bin_mass"].view(np.uint64))
+    assert got["total_mass"] == want["total_mass"]
     c32 = conf.astype(np.float32)
     got32 = ctx.curve_observe(curve, c32, 0.999)
     want32 = curve.copy()
     c32d = c32.astype(np.float64)
     lib.port().dso_curve_observe(abi.ptr(want32), abi.ptr(c32d), len(c32d), 0.999)
     assert np.array_equal(got32["bin_mass"].view(np.uint64), want32["bin_mass"].view(np.uint64))
+
+
+@pytest.mark.parametrize("decay", [0.999, 0.9, 0.5, 1.0])
+def test_curve_replay_long_vs_port(ctx, decay):
+    """400K observations: the total-mass replay reaches its rounded fixed point
+    and stops early (curve.cu); bins and total stay bit-identical, including
+    bins that start at -0.0 and never get a hit."""
+    rng = np.random.default_rng(17)
+    conf = rng.random(400_000) * 0.9                  # bins 91..100 get no hits
+    conf[::7] = np.round(conf[::7] * 100) / 100
+    curve = workloads.uniform_prior()
+    curve["bin_mass"][95] = -0.0
+    curve["bin_mass"][100] = 5e-324                   # subnormal decay fixed point
+    got = ctx.curve_observe(curve, conf, decay)
+    want = curve.copy()
+    lib.port().dso_curve_observe(abi.ptr(want), abi.ptr(conf), len(conf), decay)
+    assert np.array_equal(got["bin_mass"].view(np.uint64), want["bin_mass"].view(np.uint64))
+    assert np.float64(got["total_mass"]).view(np.uint64) == np.float64(want["total_mass"]).view(np.uint64)
 
 
 def test_curve_domain_errors(ctx):
