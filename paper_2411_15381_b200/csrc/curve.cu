@@ -68,15 +68,21 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
                     // deterministic, so once a step leaves t unchanged (t reaches the
                     // rounded fixed point, ~1/(1-d) after ~40K steps at d = 0.999) every
                     // later step does too and the replay of the total can stop.
+                    // The fixed-point test runs once per 32 steps (one extra step,
+                    // discarded unless it proves the fixed point), off the chain.
                     if (!settled) {
-                        for (int k = 0; k < cnt; ++k) {
-                            const double nt = __dadd_rn(kScale ? __dmul_rn(m, decay) : m, 1.0);
-                            if (nt == m) {
+                        int k = 0;
+                        for (; k + 32 <= cnt; k += 32) {
+                            if (kScale && __dadd_rn(__dmul_rn(m, decay), 1.0) == m) {
                                 settled = true;
                                 break;
                             }
-                            m = nt;
+#pragma unroll
+                            for (int u = 0; u < 32; ++u)
+                                m = __dadd_rn(kScale ? __dmul_rn(m, decay) : m, 1.0);
                         }
+                        if (!settled)
+                            for (; k < cnt; ++k) m = __dadd_rn(kScale ? __dmul_rn(m, decay) : m, 1.0);
                     }
                 } else {
                     // 8 observations per 64-bit shared load; the add on a hit is a
