@@ -112,6 +112,22 @@ __device__ __forceinline__ float gelu_tanh(float x) {
     return 0.5f * x * (1.0f + tanh_approx(u));
 }
 
+// GELU_tanh(acc + b) of two adjacent columns with paired fp32 ops:
+// u = x (k + k c x^2), gelu = h + h tanh(u) with h = x / 2. (b = {b[c], b[c+1]})
+__device__ __forceinline__ uint32_t gelu2_bf16x2(uint32_t a0, uint32_t a1, uint64_t b) {
+    const uint64_t x = f2_add(f2_pack(__uint_as_float(a0), __uint_as_float(a1)), b);
+    const uint64_t kk = f2_pack(0.7978845608028654f, 0.7978845608028654f);
+    const uint64_t kc = f2_pack(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
+    const uint64_t u = f2_mul(x, f2_fma(f2_mul(x, x), kc, kk));
+    float u0, u1;
+    f2_unpack(u, u0, u1);
+    const uint64_t h = f2_mul(x, f2_pack(0.5f, 0.5f));
+    const uint64_t g = f2_fma(f2_pack(tanh_approx(u0), tanh_approx(u1)), h, h);
+    float g0, g1;
+    f2_unpack(g, g0, g1);
+    return pack_bf16x2(g0, g1);
+}
+
 // Byte offset of (row, 16-byte chunk) inside a K-major SW128 tile (128 B rows).
 __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
     return (row >> 3) * 1024u + (row & 7u) * 128u + ((chunk ^ (row & 7u)) << 4);
@@ -375,8 +391,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int c = cbase + e + 2 * u;
-                            pk[u] = pack_bf16x2(gelu_tanh(__uint_as_float(v[e + 2 * u]) + s_b1[c]),
-                                                gelu_tanh(__uint_as_float(v[e + 2 * u + 1]) + s_b1[c + 1]));
+                            pk[u] = gelu2_bf16x2(v[e + 2 * u], v[e + 2 * u + 1],
+                                                 *reinterpret_cast<const uint64_t*>(s_b1 + c));
                         }
                         const int f = cbase + e;
                         st_shared_v4(sbase + G::kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
@@ -406,8 +422,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     tmem_ld_x32_sync(tmem + lane_addr + c0, v);
 #pragma unroll
                     for (int e = 0; e < 16; ++e)
-                        pk[16 * cb + e] = pack_bf16x2(fmaxf(__uint_as_float(v[2 * e]), 0.0f),
-                                                      fmaxf(__uint_as_float(v[2 * e + 1]), 0.0f));
+                        pk[16 * cb + e] = pack_relu_bf16x2(__uint_as_float(v[2 * e]),
+                                                           __uint_as_float(v[2 * e + 1]));
                 }
                 tc_fence_before();
                 group_signal(&B.drained, 3, 256, first);   // MMA may overwrite acc[0,256)
