@@ -270,7 +270,7 @@ def host_weights():
     if os.path.exists(cache):
         d = dict(np.load(cache))
         ref = disc_oracle.gen_weights(WEIGHT_SEED, calibrate=False)
-        if all(np.array_equal(d[k], ref[k]) for k in ("w1", "w2", "w3")):
+        if all(k in d and np.array_equal(d[k], ref[k]) for k in ("q1", "w2", "w3")):
             d["head_b"] = float(d["head_b"])
             return d
     return disc_oracle.gen_weights(WEIGHT_SEED, calibrate=True)

@@ -324,7 +324,9 @@ ds_status ds_format_g6(ds_ctx* ctx, const double* values, int64_t n, char* out16
 /* ---- discriminator (K5-K7: ingest + fused tcgen05 MLP + head) --------- */
 /* PatchDisc: u8 NHWC image -> 16x16 patches -> 768->256 GELU -> 256->1024
  * ReLU -> 1024->256 ReLU -> mean over patches -> dot(256)+b -> sigmoid.
- * Weights are generated deterministically from weight_seed. */
+ * Layer 1 is u8 pixels x int8 weights with an exact s32 accumulator
+ * (h1_pre = s1 * acc + b1); layers 2-3 are bf16 x bf16 -> f32. Weights are
+ * generated deterministically from weight_seed. */
 #define DS_DISC_PATCH 16
 #define DS_DISC_D0 768
 #define DS_DISC_D1 256
@@ -333,10 +335,11 @@ ds_status ds_format_g6(ds_ctx* ctx, const double* values, int64_t n, char* out16
 typedef struct ds_disc ds_disc;
 ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc** out);
 ds_status ds_disc_destroy(ds_disc* disc);
-/* Host copies of the bf16 weights/biases in the kernel's logical layout:
- * w1 [768][256], w2 [256][1024], w3 [1024][256] (row = input feature) as
- * raw bf16 bit patterns; b1/b2/b3 f32; head w f32[256]; head bias f32. */
-ds_status ds_disc_export(const ds_disc* disc, uint16_t* w1, uint16_t* w2, uint16_t* w3,
+/* Host copies of the weights in the kernel's logical layout (row = input
+ * feature): q1 [768][256] int8 with its scale s1 (one f32), w2 [256][1024]
+ * and w3 [1024][256] as raw bf16 bit patterns; b1/b2/b3 f32; head w
+ * f32[256]; head bias f32. Any pointer may be NULL. */
+ds_status ds_disc_export(const ds_disc* disc, int8_t* q1, float* s1, uint16_t* w2, uint16_t* w3,
                          float* b1, float* b2, float* b3, float* head_w, float* head_b);
 /* Scores n images (host buffer, n*h*w*3 bytes; h, w multiples of 128). */
 ds_status ds_disc_score(ds_disc* disc, const uint8_t* nhwc, int64_t n, int32_t h, int32_t w,

@@ -4,8 +4,10 @@ synthetic image pool.
 PARITY UNPINNED against the reference: the reference has no discriminator
 network (SURVEY.md 8(c) row "Discriminator network (S9)"). This is
 a restatement of THIS repo's PatchDisc definition (DESIGN.md
-"Discriminator"), in fp32 numpy with the same bf16 rounding points as the GPU
-kernel (H1 and H2 are rounded to bf16 before the next GEMM), used to check
+"Discriminator"): layer 1 as the exact integer GEMM the kernel runs (u8 pixels
+x int8 weights, int64 here / s32 on the tensor cores -- identical sums), then
+fp32 numpy with the same bf16 rounding points as the GPU kernel (H1 and H2
+are rounded to bf16 before the next GEMM), used to check
 paper_2411_15381_b200/csrc/disc.cu within the north_star tolerance
 (|dc| <= 1e-3 * max(|c|, 1e-2)). Accumulation order differs from the tensor
 cores, so agreement is within tolerance, not bitwise.
@@ -66,13 +68,15 @@ def patches(images: np.ndarray) -> np.ndarray:
 
 
 def disc_forward(images: np.ndarray, wts: dict, logits: bool = False) -> np.ndarray:
-    w1 = bf16_bits_to_f32(wts["w1"])
+    q1 = wts["q1"].astype(np.int64)
+    s1 = np.float32(wts["s1"])
     w2 = bf16_bits_to_f32(wts["w2"])
     w3 = bf16_bits_to_f32(wts["w3"])
     out = np.zeros(len(images), np.float32)
     for i in range(len(images)):
-        x = patches(images[i:i + 1])[0]
-        h1 = round_bf16(gelu_tanh(x @ w1 + wts["b1"]))
+        x = patches(images[i:i + 1])[0].astype(np.int64)
+        acc = (x @ q1).astype(np.float32)               # exact s32 sums, then f32 (|acc| < 2^25)
+        h1 = round_bf16(gelu_tanh(acc * s1 + wts["b1"]))
         h2 = round_bf16(np.maximum(h1 @ w2 + wts["b2"], 0.0))
         h3 = np.maximum(h2 @ w3 + wts["b3"], 0.0)
         s = h3 @ wts["head_w"]
@@ -95,18 +99,25 @@ def _to_bf16_bits(x: np.ndarray) -> np.ndarray:
     return (round_bf16(x).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
 
 
+def layer1_scale() -> np.float32:
+    """disc.cu layer1_scale(): sqrt(3)/(64 sqrt(768)) / 127 in f32 arithmetic."""
+    f32 = np.float32
+    return (f32(1.7320508) / (f32(64.0) * f32(27.712812921102035))) / f32(127.0)
+
+
 def gen_weights(seed: int, calibrate: bool = True) -> dict:
     """The PatchDisc weights ds_disc_create(seed) builds, restated on the host.
-    W1/W2/W3 bits and b1 are bit-identical to the device; the head is
+    Q1/s1, W2/W3 bits and b1 are bit-identical to the device; the head is
     calibrated here on the CPU forward pass (the device calibrates with its own
     logits, so head_w/head_b agree to ~1e-6 relative, see tests)."""
     f32 = np.float32
-    s1 = f32(1.7320508) / (f32(64.0) * np.sqrt(f32(768.0)))
     s2 = f32(1.7320508) * np.sqrt(f32(2.0) / f32(256.0))
     s3 = f32(1.7320508) * np.sqrt(f32(2.0) / f32(1024.0))
     i1 = np.arange(768 * 256, dtype=np.uint64)
-    w1 = _to_bf16_bits(s1 * _unif_pm1(seed ^ 0x1111, i1)).reshape(768, 256)
-    w1[:, 255] = 0
+    # round-half-even of 127 u (f32 product), as __float2int_rn(__fmul_rn(127, u))
+    q1 = np.rint(f32(127.0) * _unif_pm1(seed ^ 0x1111, i1)).astype(np.int8).reshape(768, 256)
+    q1[:, 255] = 0
+    s1 = layer1_scale()
     n2 = 256 * 1024
     e2 = np.arange(n2, dtype=np.uint64)
     w2f = s2 * _unif_pm1(seed ^ 0x2222, e2)
@@ -119,14 +130,14 @@ def gen_weights(seed: int, calibrate: bool = True) -> dict:
     w3f = (s3 * _unif_pm1(seed ^ 0x3333, e3)).reshape(1024, 256)
     w3f[1023, :] = (f32(0.05) * _unif_pm1(seed ^ 0x6666, np.arange(256, dtype=np.uint64))) / f32(16)
     w3 = _to_bf16_bits(w3f)
-    # b1: sequential f32 column sums (np.add.accumulate is sequential), then
-    # -128*s + 0.05*u with separate roundings
-    col = np.add.accumulate(bf16_bits_to_f32(w1), axis=0, dtype=np.float32)[-1]
+    # b1: exact integer column sums of Q1, then (-128 s1) * sum + 0.05 u with
+    # separate f32 roundings
+    col = q1.astype(np.int64).sum(axis=0).astype(np.float32)
     u4 = _unif_pm1(seed ^ 0x4444, np.arange(256, dtype=np.uint64))
-    b1 = (f32(-128.0) * col + f32(0.05) * u4).astype(np.float32)
+    b1 = ((f32(-128.0) * s1) * col + f32(0.05) * u4).astype(np.float32)
     b1[255] = 16.0
     hw = (_unif_pm1(seed ^ 0x7777, np.arange(256, dtype=np.uint64)) / f32(16.0)).astype(np.float32)
-    wts = dict(w1=w1, w2=w2, w3=w3, b1=b1, b2=np.zeros(1024, np.float32),
+    wts = dict(q1=q1, s1=float(s1), w2=w2, w3=w3, b1=b1, b2=np.zeros(1024, np.float32),
                b3=np.zeros(256, np.float32), head_w=hw, head_b=0.0)
     if calibrate:
         cal = synth_images(0xCA11B8A7E, 0, 64, 512, 512)

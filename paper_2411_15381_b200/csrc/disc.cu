@@ -1,32 +1,38 @@
 // K5-K7: the discriminator ("PatchDisc") as one fused, warp-specialized
 // tcgen05 kernel. No reference implementation exists (SPEC.md:8 models the
 // discriminator as a latent score, see latent.cu); the network is this
-// repo's:
+// repo's (SURVEY.md 8(a) row S9 -- "bf16 in, fp32 accumulate (or u8 x s8 ->
+// s32 for layer 1)" -- and DESIGN.md "Discriminator"):
 //
 //   u8 NHWC image -> 16x16x3 patches (token t = py*(W/16)+px, feature
-//   k = dy*48 + dx*3 + c) -> h1 = GELU_tanh(x @ W1 + b1)  [768 -> 256]
+//   k = dy*48 + dx*3 + c) -> h1 = GELU_tanh(s1 * (x @ Q1) + b1)  [768 -> 256]
 //   -> h2 = ReLU(bf16(h1) @ W2)  [256 -> 1024] -> h3 = ReLU(bf16(h2) @ W3)
 //   [1024 -> 256] -> logit = mean_t(h3 . w_head) + b_head -> sigmoid.
-// x is the raw pixel value; the (x-128)/64 input normalisation is folded into
-// W1 and b1. Layers 2 and 3 carry their biases as weights of CONSTANT hidden
-// features: W1[:,255] = 0 and b1[255] = 16 give h1[:,255] = GELU(16) = 16
+// Layer 1 is an INTEGER GEMM: the raw pixel bytes x (u8) against int8 weights
+// Q1, accumulated exactly in s32 by tcgen05.mma kind::i8 (twice the bf16
+// tensor rate per byte of operand, and the A tile is the pixel bytes
+// themselves: no u8 -> bf16 conversion). The (x-128)/64 input normalisation
+// and the weight scale s1 fold into the epilogue: h1_pre = fma(float(acc),
+// s1, b1). Layers 2 and 3 carry their biases as weights of CONSTANT hidden
+// features: Q1[:,255] = 0 and b1[255] = 16 give h1[:,255] = GELU(16) = 16
 // exactly, so W2[255,:] is layer 2's bias (/16); W2[:,1023] is zero except
 // W2[255,1023] = 1, so h2[:,1023] = 16 and W3[1023,:] is layer 3's bias.
 // The epilogue therefore never adds a bias after GEMM2/GEMM3.
 //
 // One CTA per SM, persistent over whole images, M = 128 tokens per tile.
 //   warps 0-3   A-builder: 128-bit loads of 16 B pixel runs (thread = token,
-//               prefetched kDepth chunks ahead), u8 -> bf16 (exact), SW128
-//               stores into its own 2-stage ring (12 chunks of K=64 per tile);
-//               one thread bulk-prefetches the NEXT tile's pixel rows into L2
+//               prefetched one chunk ahead) stored as-is into a 2-stage SW128
+//               ring (6 chunks of K = 128 bytes per tile); one thread
+//               bulk-prefetches the tiles two ahead into L2
 //   warps 4-11  epilogue: tcgen05.ld of the TMEM accumulators, activation,
 //               bf16 pack, SW128 stores of H1/H2 (next GEMM's A operand), and
 //               the head dot product + per-image mean
 //   warp 12     weight producer: 1-D bulk TMA of pre-swizzled 16 KB weight
-//               stages (256 x K=32, SW64; L2 evict-last) into a 4-stage ring
+//               stages (256 x 64 B, SW64; L2 evict-last) into a 4-stage ring
 //   warp 13     TMEM allocator + the single thread issuing tcgen05.mma
-// TMEM (512 columns): [0,256) accumulates GEMM1 and each 256-wide N-chunk j
-// of GEMM2; [256,512) accumulates GEMM3. MMA issue order per tile i:
+// TMEM (512 columns): [0,256) accumulates GEMM1 (s32) and each 256-wide
+// N-chunk j of GEMM2 (f32); [256,512) accumulates GEMM3. MMA issue order per
+// tile i:
 //   G1(i) | G3_3(i-1) | G2_0(i) | G2_1(i) G3_0(i) | G2_2(i) G3_1(i) | G2_3(i) G3_2(i)
 // The epilogue signals "accumulator drained" as soon as its TMEM loads land
 // (packed bf16 values stay in registers) and stores H2_j only after the GEMM3
@@ -50,51 +56,34 @@ using namespace sm100;
 
 constexpr int kM = 128;                 // tokens per CTA per tile
 constexpr int kD0 = DS_DISC_D0, kD1 = DS_DISC_D1, kD2 = DS_DISC_D2, kD3 = DS_DISC_D3;
-constexpr int kBStage = 16384;          // one blob stage: 256 rows (N) x 32 bf16 (K), SW64
-constexpr int kW1Stages = 24, kWChunkStages = 8;
-constexpr int kBlobStages = kW1Stages + 8 * kWChunkStages;   // W1 | W2_0..3 | W3_0..3 = 88
-constexpr int kAChunk = 16384;          // 128 rows x 64 bf16, SW128
-constexpr int kChunksPerTile = 12;      // K = 768 = 12 x 64
+constexpr int kBStage = 16384;          // one blob stage: 256 rows (N) x 64 bytes of K, SW64
+constexpr int kW1Stages = 12, kWChunkStages = 8;   // W1: K = 768 int8; W2/W3 chunk: K = 256 bf16
+constexpr int kBlobStages = kW1Stages + 8 * kWChunkStages;   // W1 | W2_0..3 | W3_0..3 = 76
+constexpr int kAChunk = 16384;          // 128 token rows x 128 bytes of K (u8), SW128
+constexpr int kChunksPerTile = 6;       // K = 768 = 6 x 128
 constexpr int kThreads = 448;
 constexpr float kConst = 16.0f;         // value of the constant features
-constexpr int kDepth = 4;               // A-builder prefetch depth (chunks)
-static_assert(kChunksPerTile % kDepth == 0, "slot = chunk % kDepth must be static");
-
-// Per-mode geometry. kPair: an SM pair (cta_group::2) computes M = 256, each
-// CTA holds its own 128 token rows and HALF of every weight stage (N = 128
-// rows, 8 KB), so per-SM B traffic halves and the weight ring deepens.
-template <bool kPair>
-struct Geo {
-    static constexpr int kCtas = kPair ? 2 : 1;
-    static constexpr int kTokPerTile = kM * kCtas;
-    static constexpr int kBHalf = kBStage / kCtas;            // bytes of a stage per CTA
-#ifndef DS_A_STAGES_1CTA
-#define DS_A_STAGES_1CTA 2
-#endif
-#ifndef DS_B_STAGES_1CTA
-#define DS_B_STAGES_1CTA 4
-#endif
-    static constexpr int kAStages = kPair ? 2 : DS_A_STAGES_1CTA;
-    static constexpr int kBStages = kPair ? 8 : DS_B_STAGES_1CTA;
-    static constexpr int kR1 = 0;                             // H1: 4 K-chunks x 16 KB
-    static constexpr int kR2 = kR1 + 65536;                   // H2_j: 4 K-chunks x 16 KB
-    static constexpr int kARing = kR2 + 65536;
-    static constexpr int kBRing = kARing + kAStages * kAChunk;
-    static constexpr int kB1 = kBRing + kBStages * kBHalf;    // float b1[256]
-    static constexpr int kHW = kB1 + 1024;                    // float head_w[256]
-    static constexpr int kBar = kHW + 1024;                   // mbarriers + misc
-    static constexpr int kSmemBytes = kBar + 512;
-    static constexpr uint32_t kIdesc = idesc_bf16_f32(128 * kCtas, 256);
-    static_assert(kSmemBytes <= 232448, "shared memory budget");
-};
+constexpr int kAStages = 2, kBStages = 4;
+// shared memory map (bytes)
+constexpr int kR1 = 0;                              // H1: 4 K-chunks x 16 KB (bf16, SW128)
+constexpr int kR2 = kR1 + 65536;                    // H2_j: 4 K-chunks x 16 KB
+constexpr int kARing = kR2 + 65536;
+constexpr int kBRing = kARing + kAStages * kAChunk;
+constexpr int kB1 = kBRing + kBStages * kBStage;    // float b1[256]
+constexpr int kHW = kB1 + 1024;                     // float head_w[256]
+constexpr int kBar = kHW + 1024;                    // mbarriers + misc
+constexpr int kSmemBytes = kBar + 512;
+static_assert(kSmemBytes <= 232448, "shared memory budget");
+constexpr uint32_t kIdescF16 = idesc_bf16_f32(128, 256);
+constexpr uint32_t kIdescI8 = idesc_u8s8_s32(128, 256);
 
 struct DiscParams {
-    CUtensorMap wmap;   // the weight blob as [88*256 rows x 32 bf16] (pair mode TMA)
     float b1[kD1];
     float hw[kD3];
+    float s1;           // layer-1 scale: h1_pre = s1 * acc + b1
     const uint8_t* images;
     const uint8_t* wblob;
-    float* part;        // per (image, CTA of the pair) sum of head scores
+    float* part;        // per image: sum over tokens of the head scores
     long long n_img;
     int h, w, px, tokens, tiles_per_img;
     long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr = off)
@@ -107,15 +96,12 @@ constexpr int kTraceTiles = 8;
             P.trace[((role) * kTraceTiles + (tile)) * 16 + (ev)] = clock64();             \
     } while (0)
 
-__device__ __forceinline__ float gelu_tanh(float x) {
-    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-    return 0.5f * x * (1.0f + tanh_approx(u));
-}
-
-// GELU_tanh(acc + b) of two adjacent columns with paired fp32 ops:
-// u = x (k + k c x^2), gelu = h + h tanh(u) with h = x / 2. (b = {b[c], b[c+1]})
-__device__ __forceinline__ uint32_t gelu2_bf16x2(uint32_t a0, uint32_t a1, uint64_t b) {
-    const uint64_t x = f2_add(f2_pack(__uint_as_float(a0), __uint_as_float(a1)), b);
+// GELU_tanh(s1 * acc + b) of two adjacent s32 accumulator columns with paired
+// fp32 ops: x = fma(acc, s1, b); u = x (k + k c x^2); gelu = h + h tanh(u),
+// h = x / 2. (s = {s1, s1}, b = {b[c], b[c+1]})
+__device__ __forceinline__ uint32_t gelu2_bf16x2(uint32_t a0, uint32_t a1, uint64_t s, uint64_t b) {
+    const uint64_t x = f2_fma(f2_pack(static_cast<float>(static_cast<int>(a0)),
+                                      static_cast<float>(static_cast<int>(a1))), s, b);
     const uint64_t kk = f2_pack(0.7978845608028654f, 0.7978845608028654f);
     const uint64_t kc = f2_pack(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
     const uint64_t u = f2_mul(x, f2_fma(f2_mul(x, x), kc, kk));
@@ -133,48 +119,29 @@ __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
     return (row >> 3) * 1024u + (row & 7u) * 128u + ((chunk ^ (row & 7u)) << 4);
 }
 
-// K-major SW64 descriptor: 64 B rows (32 bf16), 8-row atoms of 512 B.
+// K-major SW64 descriptor: 64 B rows, 8-row atoms of 512 B.
 __device__ __forceinline__ uint64_t desc_k_sw64(uint32_t smem_addr) {
     const uint64_t lo = ((smem_addr >> 4) & 0x3FFFu) | (1u << 16);
     const uint64_t hi = (512u >> 4) | (1u << 14) | (4u << 29);
     return lo | (hi << 32);
 }
 
-// 16 pixel bytes -> 16 bf16 (exact: integers < 256 fit the bf16 mantissa).
-__device__ __forceinline__ void u8x16_to_bf16(const uint4 v, uint32_t (&o)[8]) {
-    const uint32_t in[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        float f[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b)   // 2^23 + byte, exactly; subtract 2^23
-            f[b] = __uint_as_float(__byte_perm(in[q], 0x4B000000u, 0x7650 + b)) - 8388608.0f;
-        o[2 * q] = pack_bf16x2(f[0], f[1]);
-        o[2 * q + 1] = pack_bf16x2(f[2], f[3]);
-    }
-}
-
 struct Bars {
-    uint64_t a_full[4], a_empty[4], b_full[8], b_empty[8];
+    uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
     uint32_t tmem_base;
     float warp_part[2][8];
 };
 static_assert(sizeof(Bars) <= 512, "barrier block");
 
-template <bool kPair>
 __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant__ DiscParams P) {
-    using G = Geo<kPair>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    Bars& B = *reinterpret_cast<Bars*>(smem + G::kBar);
-    float* s_b1 = reinterpret_cast<float*>(smem + G::kB1);
-    float* s_hw = reinterpret_cast<float*>(smem + G::kHW);
+    Bars& B = *reinterpret_cast<Bars*>(smem + kBar);
+    float* s_b1 = reinterpret_cast<float*>(smem + kB1);
+    float* s_hw = reinterpret_cast<float*>(smem + kHW);
     const uint32_t sbase = smem_u32(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = kPair ? cluster_ctarank() : 0u;
-    const bool leader = rank == 0;
-    const long long unit = kPair ? cluster_id_x() : blockIdx.x;   // pair (or CTA) index
-    const long long nunits = kPair ? nclusters_x() : gridDim.x;
+    const long long unit = blockIdx.x, nunits = gridDim.x;
 
     if (sbase & 1023u) __trap();   // SW128 operand tiles need 1024-byte alignment
     if (P.trace && threadIdx.x == 0) {   // debug: per-CTA start time and SM id
@@ -188,49 +155,27 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         s_hw[threadIdx.x] = P.hw[threadIdx.x];
     }
     if (threadIdx.x == 0) {
-        // The leader's barriers also count the peer's single relayed arrival.
-        const uint32_t peer = (kPair && leader) ? 1u : 0u;
-        for (int s = 0; s < G::kAStages; ++s) {
-            mbar_init(&B.a_full[s], 128 + peer);
+        for (int s = 0; s < kAStages; ++s) {
+            mbar_init(&B.a_full[s], 128);
             mbar_init(&B.a_empty[s], 1);
         }
-        for (int s = 0; s < G::kBStages; ++s) {   // leader expects both halves' bytes
+        for (int s = 0; s < kBStages; ++s) {
             mbar_init(&B.b_full[s], 1);
             mbar_init(&B.b_empty[s], 1);
         }
         mbar_init(&B.acc12_full, 1);
-        mbar_init(&B.drained, 256 + peer);
-        mbar_init(&B.h2_ready, 256 + peer);
+        mbar_init(&B.drained, 256);
+        mbar_init(&B.h2_ready, 256);
         mbar_init(&B.h2_free, 1);
         mbar_init(&B.acc3_full, 1);
-        mbar_init(&B.acc3_empty, 256 + peer);
+        mbar_init(&B.acc3_empty, 256);
         fence_mbar_init();
     }
-    if (warp == 13) {
-        if constexpr (kPair) tmem_alloc2<512>(&B.tmem_base);
-        else tmem_alloc<512>(&B.tmem_base);
-    }
+    if (warp == 13) tmem_alloc<512>(&B.tmem_base);
     tc_fence_before();
     __syncthreads();
-    if constexpr (kPair) cluster_sync();   // peer barriers initialised before remote arrives
     tc_fence_after();
     const uint32_t tmem = B.tmem_base;
-
-    // Signal helpers: a role's arrival on the LEADER's barrier. The leader's
-    // threads arrive locally; the peer's group syncs on a named barrier and one
-    // thread forwards a single cluster-scope arrive.
-    auto group_signal = [&](uint64_t* bar, uint32_t bar_id, uint32_t threads, bool first) {
-        if (!kPair || leader) {
-            mbar_arrive(bar);
-        } else {
-            named_bar_sync(bar_id, threads);
-            if (first) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
-        }
-    };
-    auto commit = [&](uint64_t* bar) {
-        if constexpr (kPair) umma_commit_pair(bar, 0x3);
-        else umma_commit(bar);
-    };
 
     const long long n_img = P.n_img;
     const int tpi = P.tiles_per_img;
@@ -238,28 +183,29 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     const long long my_tiles = my_imgs * tpi;
     const long long img_bytes = static_cast<long long>(P.h) * P.w * 3;
     const long long row_bytes = static_cast<long long>(P.w) * 3;
-    const int tok_off = static_cast<int>(rank) * kM;   // this CTA's rows in a tile
 
     if (warp < 4) {
         // ===================== A-builder (128 threads, thread = token) =========
+        // Chunk c of a tile holds K bytes [128c, 128c+128) of every token: the
+        // 16-byte pieces q = 8c..8c+7 of its 768-byte patch vector (piece q is
+        // patch row dy = q/3, 16-byte run q%3), stored unchanged as the u8 A
+        // operand (SW128 chunk j = q%8 of the token's row).
         const int tl = threadIdx.x;
         auto token_base = [&](long long tile) -> const uint8_t* {
             const long long img = unit + (tile / tpi) * nunits;
-            const int tok = static_cast<int>(tile % tpi) * G::kTokPerTile + tok_off + tl;
+            const int tok = static_cast<int>(tile % tpi) * kM + tl;
             const int py = tok / P.px, px = tok - py * P.px;
             return P.images + img * img_bytes + (static_cast<long long>(py) * 16) * row_bytes +
                    px * 48;
         };
-        // byte offset of piece q (0..47) of a token's 768-byte patch vector:
-        // patch row dy = q / 3, 16-byte run (q % 3) of that row's 48 bytes
         auto piece = [&](const uint8_t* base, int q) -> const uint8_t* {
             return base + (q / 3) * row_bytes + (q % 3) * 16;
         };
-        // The pixels of this CTA's half tile are one contiguous byte range of
-        // whole patch rows (or a small superset); bulk-prefetch it into L2.
+        // The pixels of a tile are one contiguous byte range of whole patch
+        // rows (or a small superset); bulk-prefetch it into L2.
         auto prefetch_tile = [&](long long tile) {
             const long long img = unit + (tile / tpi) * nunits;
-            const int tok0 = static_cast<int>(tile % tpi) * G::kTokPerTile + tok_off;
+            const int tok0 = static_cast<int>(tile % tpi) * kM;
             const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
             const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
             const long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
@@ -273,19 +219,19 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             if (my_tiles > 0) prefetch_tile(0);
             if (my_tiles > 1) prefetch_tile(1);
         }
-        uint4 buf[kDepth][4];
+        uint4 buf[2][8];
         const uint8_t* pbase = my_tiles > 0 ? token_base(0) : nullptr;
         long long ptile = 0;
 #pragma unroll
-        for (int d = 0; d < kDepth; ++d)
+        for (int d = 0; d < 2; ++d)
 #pragma unroll
-            for (int s = 0; s < 4; ++s)
-                if (d < total_chunks) buf[d][s] = ld_global_nc_v4(piece(pbase, 4 * d + s));
+            for (int j = 0; j < 8; ++j)
+                if (d < total_chunks) buf[d][j] = ld_global_nc_v4(piece(pbase, 8 * d + j));
         int astage = 0;
         uint32_t aphase = 0;
-        for (long long g0 = 0; g0 < total_chunks; g0 += kDepth) {
+        for (long long g0 = 0; g0 < total_chunks; g0 += 2) {
 #pragma unroll
-            for (int d = 0; d < kDepth; ++d) {
+            for (int d = 0; d < 2; ++d) {
                 const long long g = g0 + d;
                 const int c = static_cast<int>(g % kChunksPerTile);
                 if (tl == 0 && c == 0) {
@@ -294,26 +240,22 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 }
                 mbar_wait(&B.a_empty[astage], aphase ^ 1);
                 if (tl == 0) DS_TRACE(3, g / kChunksPerTile, c);
-                const uint32_t st = sbase + G::kARing + astage * kAChunk;
+                const uint32_t st = sbase + kARing + astage * kAChunk;
 #pragma unroll
-                for (int s = 0; s < 4; ++s) {
-                    uint32_t o[8];
-                    u8x16_to_bf16(buf[d][s], o);
-                    st_shared_v4(st + sw128(tl, 2 * s), o[0], o[1], o[2], o[3]);
-                    st_shared_v4(st + sw128(tl, 2 * s + 1), o[4], o[5], o[6], o[7]);
-                }
+                for (int j = 0; j < 8; ++j)
+                    st_shared_v4(st + sw128(tl, j), buf[d][j].x, buf[d][j].y, buf[d][j].z, buf[d][j].w);
                 fence_proxy_async_smem();
-                group_signal(&B.a_full[astage], 2, 128, tl == 0);
+                mbar_arrive(&B.a_full[astage]);
                 if (tl == 0) DS_TRACE(4, g / kChunksPerTile, c);
                 if (tl == 0 && c == kChunksPerTile - 1) DS_TRACE(0, g / kChunksPerTile, 1);
-                if (++astage == G::kAStages) { astage = 0; aphase ^= 1; }
-                const long long gn = g + kDepth;
+                if (++astage == kAStages) { astage = 0; aphase ^= 1; }
+                const long long gn = g + 2;
                 if (gn < total_chunks) {
                     const long long tn = gn / kChunksPerTile;
                     if (tn != ptile) { ptile = tn; pbase = token_base(tn); }
                     const int cn = static_cast<int>(gn % kChunksPerTile);
 #pragma unroll
-                    for (int s = 0; s < 4; ++s) buf[d][s] = ld_global_nc_v4(piece(pbase, 4 * cn + s));
+                    for (int j = 0; j < 8; ++j) buf[d][j] = ld_global_nc_v4(piece(pbase, 8 * cn + j));
                 }
             }
         }
@@ -325,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         const uint32_t row = 32 * q + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
         const bool first = ew == 0 && lane == 0;
+        const uint64_t s1x2 = f2_pack(P.s1, P.s1);
         uint32_t p12 = 0, p3 = 0, pfree = 0;
         float img_acc = 0.0f;
 
@@ -349,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     part[e & 3] += fmaxf(__uint_as_float(v1[e]), 0.0f) * s_hw[c0 + 32 + e];
             }
             tc_fence_before();
-            group_signal(&B.acc3_empty, 3, 256, first);
+            mbar_arrive(&B.acc3_empty);
             DS_TRACE(1, tile, 11);
             float p = (part[0] + part[1]) + (part[2] + part[3]);
 #pragma unroll
@@ -364,14 +307,14 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 img_acc += s;
                 if (tile % tpi == tpi - 1) {
                     const long long img = unit + (tile / tpi) * nunits;
-                    P.part[img * G::kCtas + rank] = img_acc;
+                    P.part[img] = img_acc;
                     img_acc = 0.0f;
                 }
             }
         };
 
         for (long long tile = 0; tile < my_tiles; ++tile) {
-            // ---- E1: acc[0,256) + b1 -> GELU -> bf16 -> H1 (R1) ----------------
+            // ---- E1: s1 * acc[0,256) (s32) + b1 -> GELU -> bf16 -> H1 (R1) ------
             mbar_wait(&B.acc12_full, p12);
             p12 ^= 1;
             tc_fence_after();
@@ -391,18 +334,18 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int c = cbase + e + 2 * u;
-                            pk[u] = gelu2_bf16x2(v[e + 2 * u], v[e + 2 * u + 1],
+                            pk[u] = gelu2_bf16x2(v[e + 2 * u], v[e + 2 * u + 1], s1x2,
                                                  *reinterpret_cast<const uint64_t*>(s_b1 + c));
                         }
                         const int f = cbase + e;
-                        st_shared_v4(sbase + G::kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
+                        st_shared_v4(sbase + kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
                                      pk[0], pk[1], pk[2], pk[3]);
                     }
                 }
             }
             fence_proxy_async_smem();
             tc_fence_before();
-            group_signal(&B.drained, 3, 256, first);
+            mbar_arrive(&B.drained);
             DS_TRACE(1, tile, 1);
 
             // ---- E3 of the previous tile (its G3_3 was issued after G1(tile)) ----
@@ -426,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                                                            __uint_as_float(v[2 * e + 1]));
                 }
                 tc_fence_before();
-                group_signal(&B.drained, 3, 256, first);   // MMA may overwrite acc[0,256)
+                mbar_arrive(&B.drained);            // MMA may overwrite acc[0,256)
                 if (tile > 0 || j > 0) {            // GEMM3 reading the previous H2 chunk done
                     mbar_wait(&B.h2_free, pfree);
                     pfree ^= 1;
@@ -436,13 +379,13 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int f = 128 * half + 32 * cb + 8 * e;
-                        st_shared_v4(sbase + G::kR2 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
+                        st_shared_v4(sbase + kR2 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
                                      pk[16 * cb + 4 * e], pk[16 * cb + 4 * e + 1],
                                      pk[16 * cb + 4 * e + 2], pk[16 * cb + 4 * e + 3]);
                     }
                 }
                 fence_proxy_async_smem();
-                group_signal(&B.h2_ready, 3, 256, first);
+                mbar_arrive(&B.h2_ready);
                 DS_TRACE(1, tile, 3 + 2 * j);
             }
         }
@@ -454,25 +397,15 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             int bs = 0;
             uint32_t bp = 0;
             long long ptile = 0;   // trace only
-            if constexpr (kPair) prefetch_tmap(&P.wmap);
             auto put = [&](int first, int count) {
                 for (int t = first; t < first + count; ++t) {
                     mbar_wait(&B.b_empty[bs], bp ^ 1);
                     if (t < 16) DS_TRACE(6, ptile, t);
-                    if constexpr (kPair) {
-                        // both CTAs load their N-half; completion lands on the leader's
-                        // barrier, which expects the whole 16 KB stage
-                        const uint32_t lbar = mapa_shared(smem_u32(&B.b_full[bs]), 0);
-                        if (leader) mbar_arrive_expect_tx(&B.b_full[bs], kBStage);
-                        tma_2d_pair(sbase + G::kBRing + bs * G::kBHalf, &P.wmap, 0,
-                                    t * 256 + static_cast<int>(rank) * 128, lbar, policy);
-                    } else {
-                        mbar_arrive_expect_tx(&B.b_full[bs], G::kBHalf);
-                        bulk_g2s_hint(smem + G::kBRing + bs * G::kBHalf,
-                                      P.wblob + static_cast<size_t>(t) * kBStage, G::kBHalf,
-                                      &B.b_full[bs], policy);
-                    }
-                    if (++bs == G::kBStages) { bs = 0; bp ^= 1; }
+                    mbar_arrive_expect_tx(&B.b_full[bs], kBStage);
+                    bulk_g2s_hint(smem + kBRing + bs * kBStage,
+                                  P.wblob + static_cast<size_t>(t) * kBStage, kBStage,
+                                  &B.b_full[bs], policy);
+                    if (++bs == kBStages) { bs = 0; bp ^= 1; }
                 }
             };
             const int W1 = 0, W2 = kW1Stages, W3 = kW1Stages + 4 * kWChunkStages;
@@ -489,35 +422,38 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             if (my_tiles > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
         }
     } else {
-        // ===================== MMA issuer (leader warp 13, one thread) ========
-        if (lane == 0 && leader) {
+        // ===================== MMA issuer (warp 13, one thread) ==============
+        if (lane == 0) {
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0, pdr = 0, prd = 0, pe3 = 0;
             long long trace_tile = 0;   // trace only
             int trace_stage = 0;
             const uint32_t acc12 = tmem, acc3 = tmem + 256;
-            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
-                if constexpr (kPair) umma_bf16_pair(d, a, b, G::kIdesc, acc);
-                else umma_bf16(d, a, b, G::kIdesc, acc);
+            // next weight stage: wait until it landed, return its descriptor
+            auto next_b = [&]() -> uint64_t {
+                mbar_wait(&B.b_full[bs], bp);
+                tc_fence_after();
+                if (trace_stage < 16) DS_TRACE(7, trace_tile, trace_stage);
+                ++trace_stage;
+                return desc_k_sw64(sbase + kBRing + bs * kBStage);
             };
-            // K = 64 x nk from an SW128 A region (nk chunks of 16 KB) against
-            // 2*nk weight stages (K = 32 each).
+            auto release_b = [&]() {
+                umma_commit(&B.b_empty[bs]);
+                if (++bs == kBStages) { bs = 0; bp ^= 1; }
+            };
+            // bf16 GEMM, K = 64 x nk from an SW128 A region (nk chunks of 16 KB)
+            // against 2*nk weight stages (K = 32 each).
             auto gemm = [&](uint32_t a_region, int nk, uint32_t acc, bool acc_in) {
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint64_t ad = desc_k_sw128(a_region + kc * kAChunk);
 #pragma unroll
                     for (int hf = 0; hf < 2; ++hf) {
-                        mbar_wait(&B.b_full[bs], bp);
-                        tc_fence_after();
-                        if (trace_stage < 16) DS_TRACE(7, trace_tile, trace_stage);
-                        ++trace_stage;
-                        const uint64_t bd = desc_k_sw64(sbase + G::kBRing + bs * G::kBHalf);
+                        const uint64_t bd = next_b();
 #pragma unroll
                         for (int k = 0; k < 2; ++k)
-                            mma(acc, ad + 2 * (2 * hf + k), bd + 2 * k,
-                                (acc_in || kc > 0 || hf > 0 || k > 0) ? 1u : 0u);
-                        commit(&B.b_empty[bs]);
-                        if (++bs == G::kBStages) { bs = 0; bp ^= 1; }
+                            umma_bf16(acc, ad + 2 * (2 * hf + k), bd + 2 * k, kIdescF16,
+                                     (acc_in || kc > 0 || hf > 0 || k > 0) ? 1u : 0u);
+                        release_b();
                     }
                 }
             };
@@ -530,32 +466,42 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 DS_TRACE(2, tile, 0);
                 trace_tile = tile;
                 trace_stage = 0;
-                for (int c = 0; c < kChunksPerTile; ++c) {       // G1: 12 A chunks
+                // G1: 6 u8 A chunks (K = 128 bytes) x 2 int8 weight stages (K = 64)
+                for (int c = 0; c < kChunksPerTile; ++c) {
                     mbar_wait(&B.a_full[as], ap);
                     tc_fence_after();
                     DS_TRACE(5, tile, c);
-                    gemm(sbase + G::kARing + as * kAChunk, 1, acc12, c > 0);
-                    commit(&B.a_empty[as]);
-                    if (++as == G::kAStages) { as = 0; ap ^= 1; }
+                    const uint64_t ad = desc_k_sw128(sbase + kARing + as * kAChunk);
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const uint64_t bd = next_b();
+#pragma unroll
+                        for (int k = 0; k < 2; ++k)
+                            umma_i8(acc12, ad + 2 * (2 * hf + k), bd + 2 * k, kIdescI8,
+                                    (c > 0 || hf > 0 || k > 0) ? 1u : 0u);
+                        release_b();
+                    }
+                    umma_commit(&B.a_empty[as]);
+                    if (++as == kAStages) { as = 0; ap ^= 1; }
                 }
-                commit(&B.acc12_full);
+                umma_commit(&B.acc12_full);
                 DS_TRACE(2, tile, 1);
                 if (tile > 0) {                      // G3_3 of the previous tile
                     wait_bar(&B.h2_ready, prd);
-                    gemm(sbase + G::kR2, 4, acc3, true);
-                    commit(&B.h2_free);
-                    commit(&B.acc3_full);
+                    gemm(sbase + kR2, 4, acc3, true);
+                    umma_commit(&B.h2_free);
+                    umma_commit(&B.acc3_full);
                 }
                 DS_TRACE(2, tile, 2);
                 wait_bar(&B.drained, pdr);           // E1: acc drained, H1 stored
                 DS_TRACE(2, tile, 3);
-                gemm(sbase + G::kR1, 4, acc12, false);  // G2_0
-                commit(&B.acc12_full);
+                gemm(sbase + kR1, 4, acc12, false);  // G2_0
+                umma_commit(&B.acc12_full);
                 for (int j = 1; j < 4; ++j) {
                     wait_bar(&B.drained, pdr);       // E2_{j-1} has the values in registers
                     DS_TRACE(2, tile, 2 + 2 * j);
-                    gemm(sbase + G::kR1, 4, acc12, false);       // G2_j
-                    commit(&B.acc12_full);
+                    gemm(sbase + kR1, 4, acc12, false);       // G2_j
+                    umma_commit(&B.acc12_full);
                     wait_bar(&B.h2_ready, prd);      // H2_{j-1} stored
                     DS_TRACE(2, tile, 3 + 2 * j);
                     if (j == 1) {                    // acc3 drained by E3 of the previous tile
@@ -563,17 +509,17 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                         pe3 ^= 1;
                         tc_fence_after();
                     }
-                    gemm(sbase + G::kR2, 4, acc3, j > 1);        // G3_{j-1}
-                    commit(&B.h2_free);
+                    gemm(sbase + kR2, 4, acc3, j > 1);        // G3_{j-1}
+                    umma_commit(&B.h2_free);
                 }
                 wait_bar(&B.drained, pdr);           // E2_3 drained: acc[0,256) free
                 DS_TRACE(2, tile, 10);
             }
             if (my_tiles > 0) {
                 wait_bar(&B.h2_ready, prd);
-                gemm(sbase + G::kR2, 4, acc3, true); // G3_3 of the last tile
-                commit(&B.h2_free);
-                commit(&B.acc3_full);
+                gemm(sbase + kR2, 4, acc3, true);    // G3_3 of the last tile
+                umma_commit(&B.h2_free);
+                umma_commit(&B.acc3_full);
             }
         }
     }
@@ -581,22 +527,18 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     __syncthreads();
     if (P.trace && threadIdx.x == 0)
         P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
-    if constexpr (kPair) cluster_sync();     // both CTAs done with TMEM / remote barriers
     if (warp == 13) {
         tc_fence_after();
-        if constexpr (kPair) tmem_dealloc2<512>(tmem);
-        else tmem_dealloc<512>(tmem);
+        tmem_dealloc<512>(tmem);
     }
 }
 
-// logit = (sum of the pair's per-image head sums) / tokens + b_head
-__global__ void finalize_kernel(const float* __restrict__ part, int ctas, long long n, int tokens,
-                                float hb, int logits, float* __restrict__ out) {
+// logit = (per-image sum of the head scores) / tokens + b_head
+__global__ void finalize_kernel(const float* __restrict__ part, long long n, int tokens, float hb,
+                                int logits, float* __restrict__ out) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float s = part[i * ctas];
-    for (int r = 1; r < ctas; ++r) s += part[i * ctas + r];
-    const float logit = s / static_cast<float>(tokens) + hb;
+    const float logit = part[i] / static_cast<float>(tokens) + hb;
     out[i] = logits ? logit : 1.0f / (1.0f + expf(-logit));
 }
 
@@ -618,22 +560,24 @@ __host__ __device__ __forceinline__ float unif_pm1(uint64_t stream, uint64_t idx
 __device__ __forceinline__ uint16_t f2bf_bits(float f) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
-__device__ __forceinline__ float bf_bits2f(uint16_t b) {
-    return __uint_as_float(static_cast<uint32_t>(b) << 16);
+
+// layer-1 scale: the bf16 network's U(-a, a) weights with a = sqrt(3)/(64 sqrt(768))
+// (the 1/64 of the input normalisation folded in) quantised to 127 steps
+__host__ __device__ __forceinline__ float layer1_scale() {
+    return (1.7320508f / (64.0f * 27.712812921102035f)) / 127.0f;   // sqrt(768) as f32
 }
 
-// Logical weights (row = input feature), bf16 bit patterns, including the
-// constant-feature bias rows (see the header comment).
-__global__ void gen_weights_kernel(uint64_t seed, uint16_t* w1, uint16_t* w2, uint16_t* w3) {
-    const float s1 = 1.7320508f / (64.0f * sqrtf(768.0f));   // U(-a,a): std = a/sqrt(3)
+// Logical weights (row = input feature): Q1 int8, W2/W3 bf16 bit patterns,
+// including the constant-feature bias rows (see the header comment).
+__global__ void gen_weights_kernel(uint64_t seed, int8_t* q1, uint16_t* w2, uint16_t* w3) {
     const float s2 = 1.7320508f * sqrtf(2.0f / 256.0f);
     const float s3 = 1.7320508f * sqrtf(2.0f / 1024.0f);
     const int n1 = kD0 * kD1, n2 = kD1 * kD2, n3 = kD2 * kD3;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n1 + n2 + n3;
          i += gridDim.x * blockDim.x) {
         if (i < n1) {
-            const int n = i % kD1;
-            w1[i] = n == kD1 - 1 ? 0 : f2bf_bits(__fmul_rn(s1, unif_pm1(seed ^ 0x1111, i)));
+            const int n = i % kD1;   // round-half-even of 127 u, |q| <= 127
+            q1[i] = n == kD1 - 1 ? 0 : static_cast<int8_t>(__float2int_rn(__fmul_rn(127.0f, unif_pm1(seed ^ 0x1111, i))));
         } else if (i < n1 + n2) {
             const int e = i - n1, k = e / kD2, n = e % kD2;
             float v;
@@ -650,110 +594,65 @@ __global__ void gen_weights_kernel(uint64_t seed, uint16_t* w1, uint16_t* w2, ui
     }
 }
 
-// Pre-swizzled blob of 16 KB stages (256 rows = N x 32 K, SW64):
-//   stages  0..23 : W1, K-range [32s, 32s+32)
-//   stages 24..55 : W2 N-chunk j (rows 256j..), K-range [32k, 32k+32), j-major
-//   stages 56..87 : W3 K-chunk j (input rows 256j + 32k ..), all 256 outputs
-__global__ void tile_weights_kernel(const uint16_t* w1, const uint16_t* w2, const uint16_t* w3,
-                                    uint16_t* blob) {
+// Pre-swizzled blob of 16 KB stages (256 rows = N x 64 bytes of K, SW64):
+//   stages  0..11 : Q1 (int8), K-range [64s, 64s+64)
+//   stages 12..43 : W2 N-chunk j (rows 256j..), K-range [32k, 32k+32) (bf16), j-major
+//   stages 44..75 : W3 K-chunk j (input rows 256j + 32k ..), all 256 outputs
+__global__ void tile_weights_kernel(const int8_t* q1, const uint16_t* w2, const uint16_t* w3,
+                                    uint8_t* blob) {
     const int t = blockIdx.x;
-    uint16_t* out = blob + static_cast<size_t>(t) * (kBStage / 2);
-    for (int e = threadIdx.x; e < 256 * 32; e += blockDim.x) {
-        const int n = e / 32, kl = e % 32;
-        uint16_t v;
-        if (t < kW1Stages) {
-            v = w1[(32 * t + kl) * kD1 + n];
-        } else if (t < kW1Stages + 4 * kWChunkStages) {
-            const int u = t - kW1Stages, j = u / kWChunkStages, k = u % kWChunkStages;
-            v = w2[(32 * k + kl) * kD2 + 256 * j + n];
-        } else {
-            const int u = t - kW1Stages - 4 * kWChunkStages, j = u / kWChunkStages,
-                      k = u % kWChunkStages;
-            v = w3[(256 * j + 32 * k + kl) * kD3 + n];
-        }
+    uint8_t* out = blob + static_cast<size_t>(t) * kBStage;
+    for (int e = threadIdx.x; e < 256 * 64; e += blockDim.x) {   // (row n, K byte kb)
+        const int n = e / 64, kb = e % 64;
         const uint32_t byte = (n >> 3) * 512u + (n & 7) * 64u +
-                              ((((kl >> 3) ^ ((n >> 1) & 3))) << 4) + (kl & 7) * 2u;
-        out[byte / 2] = v;
+                              ((((kb >> 4) ^ ((n >> 1) & 3))) << 4) + (kb & 15);
+        if (t < kW1Stages) {
+            out[byte] = static_cast<uint8_t>(q1[(64 * t + kb) * kD1 + n]);
+        } else if (!(kb & 1)) {
+            const int kl = kb >> 1;
+            uint16_t v;
+            if (t < kW1Stages + 4 * kWChunkStages) {
+                const int u = t - kW1Stages, j = u / kWChunkStages, k = u % kWChunkStages;
+                v = w2[(32 * k + kl) * kD2 + 256 * j + n];
+            } else {
+                const int u = t - kW1Stages - 4 * kWChunkStages, j = u / kWChunkStages,
+                          k = u % kWChunkStages;
+                v = w3[(256 * j + 32 * k + kl) * kD3 + n];
+            }
+            *reinterpret_cast<uint16_t*>(out + byte) = v;
+        }
     }
 }
 
-// b1[n] = -128 * sum_k W1[k][n] + small bias (folds (x - 128)/64 into layer 1;
-// the 1/64 is in W1's scale); b1[255] = 16 makes h1[:,255] the constant feature.
-__global__ void fold_bias_kernel(const uint16_t* w1, uint64_t seed, float* b1) {
+// b1[n] = -128 * s1 * sum_k Q1[k][n] + small bias (folds (x - 128)/64 into
+// layer 1; the 1/64 is in s1); b1[255] = 16 makes h1[:,255] the constant feature.
+__global__ void fold_bias_kernel(const int8_t* q1, uint64_t seed, float* b1) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= kD1) return;
     if (n == kD1 - 1) {
         b1[n] = kConst;
         return;
     }
-    float s = 0.0f;   // explicit _rn: no contraction, restated in oracle/disc_oracle.py
-    for (int k = 0; k < kD0; ++k) s = __fadd_rn(s, bf_bits2f(w1[k * kD1 + n]));
-    b1[n] = __fadd_rn(__fmul_rn(-128.0f, s), __fmul_rn(0.05f, unif_pm1(seed ^ 0x4444, n)));
+    int s = 0;   // exact; explicit _rn below: restated in oracle/disc_oracle.py
+    for (int k = 0; k < kD0; ++k) s += q1[k * kD1 + n];
+    b1[n] = __fadd_rn(__fmul_rn(-128.0f * layer1_scale(), static_cast<float>(s)),
+                      __fmul_rn(0.05f, unif_pm1(seed ^ 0x4444, n)));
 }
 
 } // namespace
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-static ds_status make_weight_tmap(const void* blob, CUtensorMap* out) {
-    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    DS_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess)
-        return dsi::fail(DS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    // [rows = 88 stages x 256][32 bf16] row-major (64-byte rows); a box of
-    // 128 rows x 32 copies one pre-swizzled N-half of a stage byte for byte.
-    const cuuint64_t dims[2] = {32, static_cast<cuuint64_t>(kBlobStages) * 256};
-    const cuuint64_t strides[1] = {64};
-    const cuuint32_t box[2] = {32, 128};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = reinterpret_cast<EncodeFn>(fn)(
-        out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(blob), dims, strides, box,
-        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-        return dsi::fail(DS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
-    return DS_OK;
-}
-
 struct ds_disc {
     ds_ctx* ctx = nullptr;
     uint64_t seed = 0;
-    uint16_t* d_w = nullptr;   // w1 | w2 | w3 logical
+    int8_t* d_q1 = nullptr;    // Q1 logical [768][256]
+    uint16_t* d_w = nullptr;   // w2 | w3 logical
     uint8_t* d_blob = nullptr;
     float* d_b1 = nullptr;
-    DiscParams params{};       // b1 + head (device-independent part)
+    DiscParams params{};       // b1 + head + s1 (device-independent part)
     float hb = 0.0f;           // head bias
-    int force_ctas = 0;        // DS_DISC_CTAS=1|2 overrides the mode (testing)
 };
 
 namespace {
-
-template <bool kPair>
-ds_status launch_mode(ds_disc* d, const DiscParams& p, int units, cudaStream_t st) {
-    using G = Geo<kPair>;
-    // per device (one ds_ctx per GPU in a process): cheap, so set every launch
-    DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel<kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     G::kSmemBytes));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(units * G::kCtas));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = G::kSmemBytes;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = G::kCtas;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, disc_kernel<kPair>, p));
-    DS_LAUNCH_CHECK(d->ctx, "disc_kernel");
-    return DS_OK;
-}
 
 ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w, float* out,
                       int logits, cudaStream_t st, long long* trace = nullptr) {
@@ -765,11 +664,6 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     if (reinterpret_cast<uintptr_t>(images) % 16)
         return dsi::fail(DS_ERR_INVALID_ARGUMENT, "image buffer must be 16-byte aligned");
     if (n <= 0) return DS_OK;
-    // Default: the 1-CTA kernel (measured faster on the full 5K-image step this
-    // round). DS_DISC_CTAS=2 opts into SM pairs (cta_group::2) when a tile of
-    // 256 tokens divides the image; see DESIGN.md section 5.
-    const bool pair = d->force_ctas == 2 && tokens % (2 * kM) == 0;
-    const int ctas = pair ? 2 : 1;
     DiscParams p = d->params;
     p.images = images;
     p.wblob = d->d_blob;
@@ -778,23 +672,24 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     p.w = w;
     p.px = w / 16;
     p.tokens = tokens;
-    p.tiles_per_img = tokens / (kM * ctas);
+    p.tiles_per_img = tokens / kM;
     p.trace = trace;
     float* part = nullptr;
-    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * ctas * n, st));
+    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * n, st));
     p.part = part;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->ctx->device);
-    const int max_units = sms / ctas;
-    const int units = static_cast<int>(n < max_units ? n : max_units);
-    ds_status s = pair ? launch_mode<true>(d, p, units, st) : launch_mode<false>(d, p, units, st);
-    if (s == DS_OK) {
-        finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
-            part, ctas, n, tokens, d->hb, logits, out);
-        DS_LAUNCH_CHECK(d->ctx, "finalize_kernel");
-    }
+    const int units = static_cast<int>(n < sms ? n : sms);
+    // per device (one ds_ctx per GPU in a process): cheap, so set every launch
+    DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSmemBytes));
+    disc_kernel<<<static_cast<unsigned>(units), kThreads, kSmemBytes, st>>>(p);
+    DS_LAUNCH_CHECK(d->ctx, "disc_kernel");
+    finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(part, n, tokens, d->hb,
+                                                                           logits, out);
+    DS_LAUNCH_CHECK(d->ctx, "finalize_kernel");
     cudaFreeAsync(part, st);
-    return s;
+    return DS_OK;
 }
 
 } // namespace
@@ -806,9 +701,9 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
     d->ctx = ctx;
     d->seed = weight_seed;
     cudaStream_t st = ctx->stream;
-    const size_t nw = static_cast<size_t>(kD0) * kD1 + static_cast<size_t>(kD1) * kD2 +
-                      static_cast<size_t>(kD2) * kD3;
+    const size_t nw = static_cast<size_t>(kD1) * kD2 + static_cast<size_t>(kD2) * kD3;
     auto cleanup = [&](ds_status s) {
+        cudaFree(d->d_q1);
         cudaFree(d->d_w);
         cudaFree(d->d_blob);
         cudaFree(d->d_b1);
@@ -816,30 +711,27 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
         return s;
     };
     cudaError_t e;
+    if ((e = cudaMalloc(&d->d_q1, static_cast<size_t>(kD0) * kD1)) != cudaSuccess)
+        return cleanup(dsi::cuda_fail(e, "malloc q1"));
     if ((e = cudaMalloc(&d->d_w, nw * 2)) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "malloc w"));
     if ((e = cudaMalloc(&d->d_blob, static_cast<size_t>(kBlobStages) * kBStage)) != cudaSuccess)
         return cleanup(dsi::cuda_fail(e, "malloc blob"));
     if ((e = cudaMalloc(&d->d_b1, kD1 * sizeof(float))) != cudaSuccess)
         return cleanup(dsi::cuda_fail(e, "malloc b1"));
-    uint16_t* w1 = d->d_w;
-    uint16_t* w2 = w1 + kD0 * kD1;
+    uint16_t* w2 = d->d_w;
     uint16_t* w3 = w2 + kD1 * kD2;
-    gen_weights_kernel<<<148 * 4, 256, 0, st>>>(weight_seed, w1, w2, w3);
-    tile_weights_kernel<<<kBlobStages, 256, 0, st>>>(w1, w2, w3, reinterpret_cast<uint16_t*>(d->d_blob));
-    fold_bias_kernel<<<1, 256, 0, st>>>(w1, weight_seed, d->d_b1);
+    gen_weights_kernel<<<148 * 4, 256, 0, st>>>(weight_seed, d->d_q1, w2, w3);
+    tile_weights_kernel<<<kBlobStages, 256, 0, st>>>(d->d_q1, w2, w3, d->d_blob);
+    fold_bias_kernel<<<1, 256, 0, st>>>(d->d_q1, weight_seed, d->d_b1);
     ctx->launches.fetch_add(3);
     if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "weight init"));
-    {
-        const ds_status ts = make_weight_tmap(d->d_blob, &d->params.wmap);
-        if (ts != DS_OK) return cleanup(ts);
-    }
     if ((e = cudaMemcpyAsync(d->params.b1, d->d_b1, sizeof(d->params.b1), cudaMemcpyDeviceToHost,
                              st)) != cudaSuccess)
         return cleanup(dsi::cuda_fail(e, "copy b1"));
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "sync"));
+    d->params.s1 = layer1_scale();
     for (int i = 0; i < kD3; ++i) d->params.hw[i] = unif_pm1(weight_seed ^ 0x7777, i) / 16.0f;
     d->hb = 0.0f;
-    if (const char* e = std::getenv("DS_DISC_CTAS")) d->force_ctas = std::atoi(e);
 
     // Head calibration: logits of 64 synthetic images (fixed seed) -> affine
     // head so confidences spread over (0, 1): w *= 2/sd, b = -mean * 2/sd.
@@ -879,6 +771,7 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
 extern "C" ds_status ds_disc_destroy(ds_disc* d) {
     if (!d) return DS_OK;
     cudaStreamSynchronize(d->ctx->stream);
+    cudaFree(d->d_q1);
     cudaFree(d->d_w);
     cudaFree(d->d_blob);
     cudaFree(d->d_b1);
@@ -887,13 +780,14 @@ extern "C" ds_status ds_disc_destroy(ds_disc* d) {
 }
 
 // b2/b3 are carried inside W2/W3 (constant features), so they export as zeros.
-extern "C" ds_status ds_disc_export(const ds_disc* d, uint16_t* w1, uint16_t* w2, uint16_t* w3,
-                                    float* b1, float* b2, float* b3, float* head_w, float* head_b) {
+extern "C" ds_status ds_disc_export(const ds_disc* d, int8_t* q1, float* s1, uint16_t* w2,
+                                    uint16_t* w3, float* b1, float* b2, float* b3, float* head_w,
+                                    float* head_b) {
     if (!d) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null disc");
-    const uint16_t* d1 = d->d_w;
-    const uint16_t* d2 = d1 + kD0 * kD1;
+    const uint16_t* d2 = d->d_w;
     const uint16_t* d3 = d2 + kD1 * kD2;
-    if (w1) DS_CUDA_TRY(cudaMemcpy(w1, d1, sizeof(uint16_t) * kD0 * kD1, cudaMemcpyDeviceToHost));
+    if (q1) DS_CUDA_TRY(cudaMemcpy(q1, d->d_q1, static_cast<size_t>(kD0) * kD1, cudaMemcpyDeviceToHost));
+    if (s1) *s1 = d->params.s1;
     if (w2) DS_CUDA_TRY(cudaMemcpy(w2, d2, sizeof(uint16_t) * kD1 * kD2, cudaMemcpyDeviceToHost));
     if (w3) DS_CUDA_TRY(cudaMemcpy(w3, d3, sizeof(uint16_t) * kD2 * kD3, cudaMemcpyDeviceToHost));
     if (b1) std::memcpy(b1, d->params.b1, sizeof(d->params.b1));

@@ -85,7 +85,7 @@ SIGNATURES = [
     ("ds_curve_observe_device", ctypes.c_int, [c_p, c_p, c_p, i32, i64, f64, c_p]),
     ("ds_disc_create", ctypes.c_int, [c_p, u64, ctypes.POINTER(c_p)]),
     ("ds_disc_destroy", ctypes.c_int, [c_p]),
-    ("ds_disc_export", ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+    ("ds_disc_export", ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
     ("ds_disc_score", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p]),
     ("ds_disc_score_device", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p, c_p]),
     ("ds_synth_images_device", ctypes.c_int, [c_p, u64, u64, i64, i32, i32, c_p, c_p]),
@@ -281,7 +281,8 @@ class Discriminator:
 
     def export(self) -> dict:
         from . import abi as _abi  # noqa: F401
-        w1 = np.zeros((768, 256), np.uint16)
+        q1 = np.zeros((768, 256), np.int8)
+        s1 = np.zeros(1, np.float32)
         w2 = np.zeros((256, 1024), np.uint16)
         w3 = np.zeros((1024, 256), np.uint16)
         b1 = np.zeros(256, np.float32)
@@ -289,10 +290,11 @@ class Discriminator:
         b3 = np.zeros(256, np.float32)
         hw = np.zeros(256, np.float32)
         hb = np.zeros(1, np.float32)
-        check(lib().ds_disc_export(self.handle, abi.ptr(w1), abi.ptr(w2), abi.ptr(w3),
+        check(lib().ds_disc_export(self.handle, abi.ptr(q1), abi.ptr(s1), abi.ptr(w2), abi.ptr(w3),
                                    abi.ptr(b1), abi.ptr(b2), abi.ptr(b3), abi.ptr(hw),
                                    abi.ptr(hb)))
-        return dict(w1=w1, w2=w2, w3=w3, b1=b1, b2=b2, b3=b3, head_w=hw, head_b=float(hb[0]))
+        return dict(q1=q1, s1=float(s1[0]), w2=w2, w3=w3, b1=b1, b2=b2, b3=b3, head_w=hw,
+                    head_b=float(hb[0]))
 
     def score(self, images: np.ndarray) -> np.ndarray:
         images = np.ascontiguousarray(images, np.uint8)

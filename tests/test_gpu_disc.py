@@ -83,10 +83,13 @@ def test_disc_rejects_bad_shapes(disc):
 
 def test_weights_match_host_restatement(weights):
     """ds_disc_create's generator == oracle/disc_oracle.gen_weights bit for bit
-    (W1/W2/W3, b1); the head is calibrated on each side's own logits."""
+    (Q1 and its scale, W2/W3, b1); the head is calibrated on each side's own
+    logits."""
     ref = disc_oracle.gen_weights(2024, calibrate=True)
-    for k in ("w1", "w2", "w3", "b1"):
+    for k in ("q1", "w2", "w3", "b1"):
         assert np.array_equal(weights[k], ref[k]), k
+    assert np.float32(weights["s1"]) == np.float32(ref["s1"])
+    assert np.abs(weights["q1"]).max() == 127 and not weights["q1"][:, 255].any()
     assert np.allclose(weights["head_w"], ref["head_w"], rtol=1e-4)
     assert abs(weights["head_b"] - ref["head_b"]) <= 1e-3 * max(1.0, abs(ref["head_b"]))
 
@@ -107,22 +110,19 @@ def test_pipelined_host_path_equals_device_path(disc):
     assert np.array_equal(disc.score(host), out.cpu().numpy())
 
 
-def test_pair_mode_matches_single_cta_mode(disc, weights, monkeypatch):
-    """DS_DISC_CTAS=2 selects the cta_group::2 SM-pair kernel; it computes the
-    same per-token values as the default 1-CTA kernel (only the per-image sum
-    is associated differently) and passes the oracle check."""
-    monkeypatch.setenv("DS_DISC_CTAS", "2")
-    pair = native.Discriminator(default_context(), weight_seed=2024)
-    for shape in ((12, 512, 512), (3, 256, 1024), (2, 1024, 1024)):
-        imgs = disc_oracle.synth_images(5, 0, *shape)
-        a = disc.score(imgs)
-        b = pair.score(imgs)
-        assert np.allclose(a, b, rtol=2e-5, atol=1e-6), shape
-        check_conf(b, disc_oracle.disc_forward(imgs, weights))
-    pair.close()
+def test_layer1_is_exact_integer_gemm(disc, weights):
+    """Layer 1 runs u8 x s8 -> s32 on the tensor cores: with extreme pixels
+    (all 255 / all 0 / checkerboards) the confidences still match the oracle,
+    whose layer-1 sums are exact int64."""
+    imgs = np.zeros((4, 256, 512, 3), np.uint8)
+    imgs[1] = 255
+    imgs[2, ::2, ::2] = 255
+    imgs[3] = disc_oracle.synth_images(4, 0, 1, 256, 512)[0]
+    imgs[3, :, :, 1] = 0
+    check_conf(disc.score(imgs), disc_oracle.disc_forward(imgs, weights))
 
 
-def test_disc_single_cta_fallback_shapes(disc, weights):
-    """128 tokens per image (128x256): no 256-token pair tile -> 1-CTA path."""
+def test_disc_single_tile_images(disc, weights):
+    """128 tokens per image (128x256): one token tile per image."""
     imgs = disc_oracle.synth_images(9, 3, 5, 128, 256)
     check_conf(disc.score(imgs), disc_oracle.disc_forward(imgs, weights))

@@ -165,10 +165,12 @@ def test_disc_weight_restatement_matches_committed_export():
     if not os.path.exists(path):
         pytest.skip("no committed export")
     c = dict(np.load(path))
+    if "q1" not in c:
+        pytest.skip("committed export predates the int8 layer 1")
     w = disc_oracle.gen_weights(2024, calibrate=False)
-    for k in ("w1", "w2", "w3"):
+    for k in ("q1", "w2", "w3", "b1"):
         assert np.array_equal(w[k], c[k]), k
-    assert np.abs(w["b1"] - c["b1"]).max() <= 2e-7 * max(1.0, float(np.abs(c["b1"]).max()))
+    assert np.float32(w["s1"]) == np.float32(c["s1"])
 
 
 def test_synth_images_host_restatement_is_deterministic():
