@@ -61,9 +61,11 @@ constexpr int kW1Stages = 12, kWChunkStages = 8;   // W1: K = 768 int8; W2/W3 ch
 constexpr int kBlobStages = kW1Stages + 8 * kWChunkStages;   // W1 | W2_0..3 | W3_0..3 = 76
 constexpr int kAChunk = 16384;          // 128 token rows x 128 bytes of K (u8), SW128
 constexpr int kChunksPerTile = 6;       // K = 768 = 6 x 128
-constexpr int kThreads = 448;
+constexpr int kThreads = 480;
 constexpr float kConst = 16.0f;         // value of the constant features
 constexpr int kAStages = 2, kBStages = 4;
+constexpr int kXStages = 4;            // W1 stages 0-3 land in the H1 region (free during GEMM1)
+constexpr int kE1Split = 192;           // E1 columns [0,192): epilogue warps; [192,256): A-builders
 // shared memory map (bytes)
 constexpr int kR1 = 0;                              // H1: 4 K-chunks x 16 KB (bf16, SW128)
 constexpr int kR2 = kR1 + 65536;                    // H2_j: 4 K-chunks x 16 KB
@@ -119,6 +121,42 @@ __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
     return (row >> 3) * 1024u + (row & 7u) * 128u + ((chunk ^ (row & 7u)) << 4);
 }
 
+// E1 over columns [c_lo, c_lo + 32*n32) of this thread's TMEM lane (row):
+// GELU(s1 * acc + b1) -> bf16 -> the SW128 H1 tile (4 K-chunks of 16 KB).
+template <int kN32>
+__device__ __forceinline__ void e1_columns(uint32_t tmem_lane, int c_lo, uint32_t row,
+                                           uint32_t h1, const float* s_b1, uint64_t s1x2) {
+    auto emit = [&](const uint32_t (&v)[32], int cbase) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = cbase + e + 2 * u;
+                pk[u] = gelu2_bf16x2(v[e + 2 * u], v[e + 2 * u + 1], s1x2,
+                                     *reinterpret_cast<const uint64_t*>(s_b1 + c));
+            }
+            const int f = cbase + e;
+            st_shared_v4(h1 + (f >> 6) * 16384u + sw128(row, (f & 63) >> 3), pk[0], pk[1], pk[2],
+                         pk[3]);
+        }
+    };
+#pragma unroll 1
+    for (int g = 0; g + 1 < kN32; g += 2) {
+        uint32_t v0[32], v1[32];
+        const int c0 = c_lo + 32 * g;
+        tmem_ld2_x32_sync(tmem_lane + c0, tmem_lane + c0 + 32, v0, v1);
+        emit(v0, c0);
+        emit(v1, c0 + 32);
+    }
+    if constexpr (kN32 & 1) {
+        uint32_t v[32];
+        const int c0 = c_lo + 32 * (kN32 - 1);
+        tmem_ld_x32_sync(tmem_lane + c0, v);
+        emit(v, c0);
+    }
+}
+
 // K-major SW64 descriptor: 64 B rows, 8-row atoms of 512 B.
 __device__ __forceinline__ uint64_t desc_k_sw64(uint32_t smem_addr) {
     const uint64_t lo = ((smem_addr >> 4) & 0x3FFFu) | (1u << 16);
@@ -129,6 +167,7 @@ __device__ __forceinline__ uint64_t desc_k_sw64(uint32_t smem_addr) {
 struct Bars {
     uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
+    uint64_t x_full[kXStages], r1_free, e1b_done;
     uint32_t tmem_base;
     float warp_part[2][8];
 };
@@ -169,6 +208,9 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         mbar_init(&B.h2_free, 1);
         mbar_init(&B.acc3_full, 1);
         mbar_init(&B.acc3_empty, 256);
+        for (int s = 0; s < kXStages; ++s) mbar_init(&B.x_full[s], 1);
+        mbar_init(&B.r1_free, 1);
+        mbar_init(&B.e1b_done, 128);
         fence_mbar_init();
     }
     if (warp == 13) tmem_alloc<512>(&B.tmem_base);
@@ -214,49 +256,59 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 bulk_prefetch_l2(p0 + off, nb);
             }
         };
-        const long long total_chunks = my_tiles * kChunksPerTile;
         if (tl == 0) {
             if (my_tiles > 0) prefetch_tile(0);
             if (my_tiles > 1) prefetch_tile(1);
         }
+        const uint32_t tmem_lane = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+        const uint64_t s1x2 = f2_pack(P.s1, P.s1);
         uint4 buf[2][8];
+        auto load_chunk = [&](const uint8_t* base, int c, uint4 (&b)[8]) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = ld_global_nc_v4(piece(base, 8 * c + j));
+        };
         const uint8_t* pbase = my_tiles > 0 ? token_base(0) : nullptr;
-        long long ptile = 0;
-#pragma unroll
-        for (int d = 0; d < 2; ++d)
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (d < total_chunks) buf[d][j] = ld_global_nc_v4(piece(pbase, 8 * d + j));
+        if (my_tiles > 0) {
+            load_chunk(pbase, 0, buf[0]);
+            load_chunk(pbase, 1, buf[1]);
+        }
         int astage = 0;
         uint32_t aphase = 0;
-        for (long long g0 = 0; g0 < total_chunks; g0 += 2) {
+        for (long long tile = 0; tile < my_tiles; ++tile) {
+            if (tl == 0) {
+                DS_TRACE(0, tile, 0);
+                if (tile + 2 < my_tiles) prefetch_tile(tile + 2);
+            }
 #pragma unroll
-            for (int d = 0; d < 2; ++d) {
-                const long long g = g0 + d;
-                const int c = static_cast<int>(g % kChunksPerTile);
-                if (tl == 0 && c == 0) {
-                    DS_TRACE(0, g / kChunksPerTile, 0);
-                    if (g / kChunksPerTile + 2 < my_tiles) prefetch_tile(g / kChunksPerTile + 2);
-                }
+            for (int c = 0; c < kChunksPerTile; ++c) {
                 mbar_wait(&B.a_empty[astage], aphase ^ 1);
-                if (tl == 0) DS_TRACE(3, g / kChunksPerTile, c);
+                if (tl == 0) DS_TRACE(3, tile, c);
                 const uint32_t st = sbase + kARing + astage * kAChunk;
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    st_shared_v4(st + sw128(tl, j), buf[d][j].x, buf[d][j].y, buf[d][j].z, buf[d][j].w);
+                    st_shared_v4(st + sw128(tl, j), buf[c & 1][j].x, buf[c & 1][j].y, buf[c & 1][j].z,
+                                 buf[c & 1][j].w);
                 fence_proxy_async_smem();
                 mbar_arrive(&B.a_full[astage]);
-                if (tl == 0) DS_TRACE(4, g / kChunksPerTile, c);
-                if (tl == 0 && c == kChunksPerTile - 1) DS_TRACE(0, g / kChunksPerTile, 1);
+                if (tl == 0) DS_TRACE(4, tile, c);
                 if (++astage == kAStages) { astage = 0; aphase ^= 1; }
-                const long long gn = g + 2;
-                if (gn < total_chunks) {
-                    const long long tn = gn / kChunksPerTile;
-                    if (tn != ptile) { ptile = tn; pbase = token_base(tn); }
-                    const int cn = static_cast<int>(gn % kChunksPerTile);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) buf[d][j] = ld_global_nc_v4(piece(pbase, 8 * cn + j));
-                }
+                if (c + 2 < kChunksPerTile) load_chunk(pbase, c + 2, buf[c & 1]);
+            }
+            if (tl == 0) DS_TRACE(0, tile, 1);
+            // E1 help: columns [kE1Split, 256) once GEMM1 of this tile landed. The
+            // acc12_full phase of E1(tile) has parity tile & 1; the barrier cannot
+            // be behind it (the A slots just freed were released after GEMM2_3 of
+            // the previous tile) nor past it (GEMM2_0 waits for e1b_done).
+            mbar_wait(&B.acc12_full, static_cast<uint32_t>(tile & 1));
+            tc_fence_after();
+            e1_columns<(256 - kE1Split) / 32>(tmem_lane, kE1Split, tl, sbase + kR1, s_b1, s1x2);
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(&B.e1b_done);
+            if (tile + 1 < my_tiles) {
+                pbase = token_base(tile + 1);
+                load_chunk(pbase, 0, buf[0]);
+                load_chunk(pbase, 1, buf[1]);
             }
         }
     } else if (warp < 12) {
@@ -314,35 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         };
 
         for (long long tile = 0; tile < my_tiles; ++tile) {
-            // ---- E1: s1 * acc[0,256) (s32) + b1 -> GELU -> bf16 -> H1 (R1) ------
+            // ---- E1: s1 * acc (s32) + b1 -> GELU -> bf16 -> H1 (R1), columns
+            // [96*half, 96*half + 96); the A-builders take [192, 256) -------------
             mbar_wait(&B.acc12_full, p12);
             p12 ^= 1;
             tc_fence_after();
             DS_TRACE(1, tile, 0);
-#pragma unroll 1
-            for (int cb = 0; cb < 4; cb += 2) {
-                uint32_t v0[32], v1[32];
-                const int c0 = 128 * half + 32 * cb;
-                tmem_ld2_x32_sync(tmem + lane_addr + c0, tmem + lane_addr + c0 + 32, v0, v1);
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-                    const uint32_t* v = hh ? v1 : v0;
-                    const int cbase = c0 + 32 * hh;
-#pragma unroll
-                    for (int e = 0; e < 32; e += 8) {
-                        uint32_t pk[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int c = cbase + e + 2 * u;
-                            pk[u] = gelu2_bf16x2(v[e + 2 * u], v[e + 2 * u + 1], s1x2,
-                                                 *reinterpret_cast<const uint64_t*>(s_b1 + c));
-                        }
-                        const int f = cbase + e;
-                        st_shared_v4(sbase + kR1 + (f >> 6) * kAChunk + sw128(row, (f & 63) >> 3),
-                                     pk[0], pk[1], pk[2], pk[3]);
-                    }
-                }
-            }
+            e1_columns<kE1Split / 64>(tmem + lane_addr, (kE1Split / 2) * half, row, sbase + kR1, s_b1,
+                                      s1x2);
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(&B.drained);
@@ -411,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             const int W1 = 0, W2 = kW1Stages, W3 = kW1Stages + 4 * kWChunkStages;
             for (long long tile = 0; tile < my_tiles; ++tile) {
                 ptile = tile;
-                put(W1, kW1Stages);
+                put(W1 + kXStages, kW1Stages - kXStages);
                 if (tile > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
                 put(W2, kWChunkStages);
                 for (int j = 1; j < 4; ++j) {
@@ -420,6 +451,19 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 }
             }
             if (my_tiles > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
+        }
+    } else if (warp == 14) {
+        // ===================== W1 stages 0-3 into the H1 region ================
+        if (lane == 0) {
+            const uint64_t policy = policy_evict_last();
+            for (long long tile = 0; tile < my_tiles; ++tile) {
+                if (tile > 0) mbar_wait(&B.r1_free, static_cast<uint32_t>((tile - 1) & 1));
+                for (int k = 0; k < kXStages; ++k) {
+                    mbar_arrive_expect_tx(&B.x_full[k], kBStage);
+                    bulk_g2s_hint(smem + kR1 + k * kBStage, P.wblob + static_cast<size_t>(k) * kBStage,
+                                  kBStage, &B.x_full[k], policy);
+                }
+            }
         }
     } else {
         // ===================== MMA issuer (warp 13, one thread) ==============
@@ -466,7 +510,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 DS_TRACE(2, tile, 0);
                 trace_tile = tile;
                 trace_stage = 0;
-                // G1: 6 u8 A chunks (K = 128 bytes) x 2 int8 weight stages (K = 64)
+                // G1: 6 u8 A chunks (K = 128 bytes) x 2 int8 weight stages (K = 64);
+                // stages 0-3 come from the H1 region (x_full), the rest from the ring
                 for (int c = 0; c < kChunksPerTile; ++c) {
                     mbar_wait(&B.a_full[as], ap);
                     tc_fence_after();
@@ -474,12 +519,20 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     const uint64_t ad = desc_k_sw128(sbase + kARing + as * kAChunk);
 #pragma unroll
                     for (int hf = 0; hf < 2; ++hf) {
-                        const uint64_t bd = next_b();
+                        const int ws = 2 * c + hf;
+                        uint64_t bd;
+                        if (ws < kXStages) {
+                            mbar_wait(&B.x_full[ws], static_cast<uint32_t>(tile & 1));
+                            tc_fence_after();
+                            bd = desc_k_sw64(sbase + kR1 + ws * kBStage);
+                        } else {
+                            bd = next_b();
+                        }
 #pragma unroll
                         for (int k = 0; k < 2; ++k)
                             umma_i8(acc12, ad + 2 * (2 * hf + k), bd + 2 * k, kIdescI8,
                                     (c > 0 || hf > 0 || k > 0) ? 1u : 0u);
-                        release_b();
+                        if (ws >= kXStages) release_b();
                     }
                     umma_commit(&B.a_empty[as]);
                     if (++as == kAStages) { as = 0; ap ^= 1; }
@@ -494,6 +547,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 }
                 DS_TRACE(2, tile, 2);
                 wait_bar(&B.drained, pdr);           // E1: acc drained, H1 stored
+                mbar_wait(&B.e1b_done, static_cast<uint32_t>(tile & 1));   // the builders' E1 columns
+                tc_fence_after();
                 DS_TRACE(2, tile, 3);
                 gemm(sbase + kR1, 4, acc12, false);  // G2_0
                 umma_commit(&B.acc12_full);
@@ -502,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     DS_TRACE(2, tile, 2 + 2 * j);
                     gemm(sbase + kR1, 4, acc12, false);       // G2_j
                     umma_commit(&B.acc12_full);
+                    if (j == 3) umma_commit(&B.r1_free);      // H1 read for the last time
                     wait_bar(&B.h2_ready, prd);      // H2_{j-1} stored
                     DS_TRACE(2, tile, 3 + 2 * j);
                     if (j == 1) {                    // acc3 drained by E3 of the previous tile
