@@ -47,7 +47,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(obj)
         if not force and _mtime(obj) > max(_mtime(path), hdr_time, _mtime(__file__)):
             continue
-        flags = list(COMMON)
+        flags = list(COMMON) + os.environ.get("DS_EXTRA_NVCC", "").split()   # experiments
         if src in EXACT_FP64:
             flags += ["-fmad=false"]
         cmd = [NVCC, *ARCH, *flags, "-c", path, "-o", obj]

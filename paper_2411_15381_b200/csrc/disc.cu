@@ -19,20 +19,34 @@
 // W2[255,1023] = 1, so h2[:,1023] = 16 and W3[1023,:] is layer 3's bias.
 // The epilogue therefore never adds a bias after GEMM2/GEMM3.
 //
-// One CTA per SM, persistent over whole images, M = 128 tokens per tile.
-//   warps 0-3   A-builder: 128-bit loads of 16 B pixel runs (thread = token,
-//               prefetched one chunk ahead) stored as-is into a 2-stage SW128
-//               ring (6 chunks of K = 128 bytes per tile); one thread
-//               bulk-prefetches the tiles two ahead into L2
-//   warps 4-11  epilogue: tcgen05.ld of the TMEM accumulators, activation,
+// SM pairs (cta_group::2), persistent over whole images. Each CTA of a pair
+// owns 128 tokens of a 256-token pair tile and HALF of every weight stage
+// (128 of the 256 output rows), so each SM streams 0.6 MB of weights per 128
+// tokens instead of 1.2 MB; one thread of the leader CTA issues M = 256 MMAs
+// that read both CTAs' shared memory and write both CTAs' TMEM.
+//   warps 0-3   A-builder: 128-bit loads of 16 B pixel runs (thread = token)
+//               stored as-is into a 2-stage SW128 ring (6 chunks of K = 128
+//               bytes per tile); one thread bulk-prefetches the tiles two
+//               ahead into L2; after GEMM1 they also run E1 on columns
+//               [192, 256)
+//   warps 4-11  epilogue: tcgen05.ld of this CTA's TMEM lanes, activation,
 //               bf16 pack, SW128 stores of H1/H2 (next GEMM's A operand), and
-//               the head dot product + per-image mean
-//   warp 12     weight producer: 1-D bulk TMA of pre-swizzled 16 KB weight
-//               stages (256 x 64 B, SW64; L2 evict-last) into a 4-stage ring
-//   warp 13     TMEM allocator + the single thread issuing tcgen05.mma
-// TMEM (512 columns): [0,256) accumulates GEMM1 (s32) and each 256-wide
-// N-chunk j of GEMM2 (f32); [256,512) accumulates GEMM3. MMA issue order per
-// tile i:
+//               the head dot product + per-image sum
+//   warp 12     weight producer: tensor-map TMA of this CTA's 16 KB half of
+//               each pre-swizzled 32 KB stage (256 rows x 128 B, SW128; L2
+//               evict-last) into a 4-stage ring; completion lands on the
+//               LEADER's barrier (cta_group::2)
+//   warp 13     TMEM allocator (both CTAs) + the MMA-issuing thread (leader)
+//   warp 14     W1 stages 0-3 into the H1 region, which is idle during GEMM1
+// Every weight stage and A chunk is 4 MMAs (K = 64 bf16 / 128 int8), so the
+// issuing thread waits once per 512 MMA-cycles (waits every 2 MMAs cost the
+// tensor pipe ~15%, tools/i8_rate_probe.cu).
+// Readiness of the peer CTA's shared memory (A chunks, H1/H2 stores, drained
+// accumulators) reaches the leader through one remote mbarrier arrive per
+// event after a named barrier; the MMA commits multicast to both CTAs.
+// TMEM (512 columns per CTA): [0,256) accumulates GEMM1 (s32) and each
+// 256-wide N-chunk j of GEMM2 (f32); [256,512) accumulates GEMM3. MMA issue
+// order per pair tile i:
 //   G1(i) | G3_3(i-1) | G2_0(i) | G2_1(i) G3_0(i) | G2_2(i) G3_1(i) | G2_3(i) G3_2(i)
 // The epilogue signals "accumulator drained" as soon as its TMEM loads land
 // (packed bf16 values stay in registers) and stores H2_j only after the GEMM3
@@ -45,6 +59,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "ds_internal.h"
@@ -54,38 +69,40 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kM = 128;                 // tokens per CTA per tile
+constexpr int kM = 128;                 // tokens per CTA per tile (256 per pair)
 constexpr int kD0 = DS_DISC_D0, kD1 = DS_DISC_D1, kD2 = DS_DISC_D2, kD3 = DS_DISC_D3;
-constexpr int kBStage = 16384;          // one blob stage: 256 rows (N) x 64 bytes of K, SW64
-constexpr int kW1Stages = 12, kWChunkStages = 8;   // W1: K = 768 int8; W2/W3 chunk: K = 256 bf16
-constexpr int kBlobStages = kW1Stages + 8 * kWChunkStages;   // W1 | W2_0..3 | W3_0..3 = 76
-constexpr int kAChunk = 16384;          // 128 token rows x 128 bytes of K (u8), SW128
-constexpr int kChunksPerTile = 6;       // K = 768 = 6 x 128
+constexpr int kBStage = 32768;          // one blob stage: 256 rows (N) x 128 bytes of K, SW128
+constexpr int kBHalf = kBStage / 2;     // the N-half one CTA loads
+constexpr int kW1Stages = 6, kWChunkStages = 4;    // W1: K = 768 int8; W2/W3 chunk: K = 256 bf16
+constexpr int kBlobStages = kW1Stages + 8 * kWChunkStages;   // W1 | W2_0..3 | W3_0..3 = 38
+constexpr int kAChunk = 16384;          // 128 token rows x 128 bytes of K, SW128
+constexpr int kChunksPerTile = 6;       // K = 768 = 6 x 128 (u8)
 constexpr int kThreads = 480;
 constexpr float kConst = 16.0f;         // value of the constant features
 constexpr int kAStages = 2, kBStages = 4;
-constexpr int kXStages = 4;            // W1 stages 0-3 land in the H1 region (free during GEMM1)
+constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (idle during GEMM1)
 constexpr int kE1Split = 192;           // E1 columns [0,192): epilogue warps; [192,256): A-builders
-// shared memory map (bytes)
+// shared memory map (bytes, per CTA)
 constexpr int kR1 = 0;                              // H1: 4 K-chunks x 16 KB (bf16, SW128)
 constexpr int kR2 = kR1 + 65536;                    // H2_j: 4 K-chunks x 16 KB
 constexpr int kARing = kR2 + 65536;
 constexpr int kBRing = kARing + kAStages * kAChunk;
-constexpr int kB1 = kBRing + kBStages * kBStage;    // float b1[256]
+constexpr int kB1 = kBRing + kBStages * kBHalf;     // float b1[256]
 constexpr int kHW = kB1 + 1024;                     // float head_w[256]
 constexpr int kBar = kHW + 1024;                    // mbarriers + misc
 constexpr int kSmemBytes = kBar + 512;
 static_assert(kSmemBytes <= 232448, "shared memory budget");
-constexpr uint32_t kIdescF16 = idesc_bf16_f32(128, 256);
-constexpr uint32_t kIdescI8 = idesc_u8s8_s32(128, 256);
+static_assert(kXStages * kBHalf <= 65536, "X stages fit the H1 region");
+constexpr uint32_t kIdescF16 = idesc_bf16_f32(256, 256);
+constexpr uint32_t kIdescI8 = idesc_u8s8_s32(256, 256);
 
 struct DiscParams {
+    CUtensorMap wmap;   // the weight blob as [38*256 rows x 128 B] (a box = one N-half)
     float b1[kD1];
     float hw[kD3];
     float s1;           // layer-1 scale: h1_pre = s1 * acc + b1
     const uint8_t* images;
-    const uint8_t* wblob;
-    float* part;        // per image: sum over tokens of the head scores
+    float* part;        // per (image, CTA rank): sum over tokens of the head scores
     long long n_img;
     int h, w, px, tokens, tiles_per_img;
     long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr = off)
@@ -157,13 +174,6 @@ __device__ __forceinline__ void e1_columns(uint32_t tmem_lane, int c_lo, uint32_
     }
 }
 
-// K-major SW64 descriptor: 64 B rows, 8-row atoms of 512 B.
-__device__ __forceinline__ uint64_t desc_k_sw64(uint32_t smem_addr) {
-    const uint64_t lo = ((smem_addr >> 4) & 0x3FFFu) | (1u << 16);
-    const uint64_t hi = (512u >> 4) | (1u << 14) | (4u << 29);
-    return lo | (hi << 32);
-}
-
 struct Bars {
     uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
@@ -180,7 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     float* s_hw = reinterpret_cast<float*>(smem + kHW);
     const uint32_t sbase = smem_u32(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long unit = blockIdx.x, nunits = gridDim.x;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const long long unit = cluster_id_x(), nunits = nclusters_x();   // pair index / count
 
     if (sbase & 1023u) __trap();   // SW128 operand tiles need 1024-byte alignment
     if (P.trace && threadIdx.x == 0) {   // debug: per-CTA start time and SM id
@@ -194,8 +206,11 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         s_hw[threadIdx.x] = P.hw[threadIdx.x];
     }
     if (threadIdx.x == 0) {
+        // The leader's barriers also count the peer's single relayed arrival;
+        // weight-stage barriers get both halves' bytes through cta_group::2 TMA.
+        const uint32_t peer = leader ? 1u : 0u;
         for (int s = 0; s < kAStages; ++s) {
-            mbar_init(&B.a_full[s], 128);
+            mbar_init(&B.a_full[s], 128 + peer);
             mbar_init(&B.a_empty[s], 1);
         }
         for (int s = 0; s < kBStages; ++s) {
@@ -203,28 +218,49 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             mbar_init(&B.b_empty[s], 1);
         }
         mbar_init(&B.acc12_full, 1);
-        mbar_init(&B.drained, 256);
-        mbar_init(&B.h2_ready, 256);
+        mbar_init(&B.drained, 256 + peer);
+        mbar_init(&B.h2_ready, 256 + peer);
         mbar_init(&B.h2_free, 1);
         mbar_init(&B.acc3_full, 1);
-        mbar_init(&B.acc3_empty, 256);
+        mbar_init(&B.acc3_empty, 256 + peer);
         for (int s = 0; s < kXStages; ++s) mbar_init(&B.x_full[s], 1);
         mbar_init(&B.r1_free, 1);
-        mbar_init(&B.e1b_done, 128);
+        mbar_init(&B.e1b_done, 128 + peer);
         fence_mbar_init();
     }
-    if (warp == 13) tmem_alloc<512>(&B.tmem_base);
+    if (warp == 13) tmem_alloc2<512>(&B.tmem_base);
     tc_fence_before();
     __syncthreads();
+    cluster_sync();   // peer barriers initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = B.tmem_base;
 
+    // A role's arrival on the LEADER's barrier: the leader's threads arrive
+    // locally; the peer's group syncs on a named barrier and one thread
+    // forwards a single cluster-scope arrive.
+    auto group_signal = [&](uint64_t* bar, uint32_t bar_id, uint32_t threads, bool first) {
+        if (leader) {
+            mbar_arrive(bar);
+        } else {
+            named_bar_sync(bar_id, threads);
+            if (first) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+        }
+    };
+
+    // Flat 128-token tiles of this pair's images (images unit, unit + nunits, ...);
+    // CTA `rank` takes flat tiles 2k + rank. A pair tile whose second half runs
+    // past the end recomputes the last tile and writes nothing (a "ghost").
     const long long n_img = P.n_img;
     const int tpi = P.tiles_per_img;
     const long long my_imgs = unit < n_img ? (n_img - 1 - unit) / nunits + 1 : 0;
-    const long long my_tiles = my_imgs * tpi;
+    const long long my_flat = my_imgs * tpi;
+    const long long my_tiles = (my_flat + 1) / 2;          // pair tiles
     const long long img_bytes = static_cast<long long>(P.h) * P.w * 3;
     const long long row_bytes = static_cast<long long>(P.w) * 3;
+    auto flat_of = [&](long long tile) {                   // this CTA's flat tile
+        const long long f = 2 * tile + rank;
+        return f < my_flat ? f : my_flat - 1;
+    };
 
     if (warp < 4) {
         // ===================== A-builder (128 threads, thread = token) =========
@@ -234,8 +270,9 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         // operand (SW128 chunk j = q%8 of the token's row).
         const int tl = threadIdx.x;
         auto token_base = [&](long long tile) -> const uint8_t* {
-            const long long img = unit + (tile / tpi) * nunits;
-            const int tok = static_cast<int>(tile % tpi) * kM + tl;
+            const long long f = flat_of(tile);
+            const long long img = unit + (f / tpi) * nunits;
+            const int tok = static_cast<int>(f % tpi) * kM + tl;
             const int py = tok / P.px, px = tok - py * P.px;
             return P.images + img * img_bytes + (static_cast<long long>(py) * 16) * row_bytes +
                    px * 48;
@@ -246,8 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         // The pixels of a tile are one contiguous byte range of whole patch
         // rows (or a small superset); bulk-prefetch it into L2.
         auto prefetch_tile = [&](long long tile) {
-            const long long img = unit + (tile / tpi) * nunits;
-            const int tok0 = static_cast<int>(tile % tpi) * kM;
+            const long long f = flat_of(tile);
+            const long long img = unit + (f / tpi) * nunits;
+            const int tok0 = static_cast<int>(f % tpi) * kM;
             const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
             const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
             const long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
@@ -289,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     st_shared_v4(st + sw128(tl, j), buf[c & 1][j].x, buf[c & 1][j].y, buf[c & 1][j].z,
                                  buf[c & 1][j].w);
                 fence_proxy_async_smem();
-                mbar_arrive(&B.a_full[astage]);
+                group_signal(&B.a_full[astage], 2, 128, tl == 0);
                 if (tl == 0) DS_TRACE(4, tile, c);
                 if (++astage == kAStages) { astage = 0; aphase ^= 1; }
                 if (c + 2 < kChunksPerTile) load_chunk(pbase, c + 2, buf[c & 1]);
@@ -304,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             e1_columns<(256 - kE1Split) / 32>(tmem_lane, kE1Split, tl, sbase + kR1, s_b1, s1x2);
             fence_proxy_async_smem();
             tc_fence_before();
-            mbar_arrive(&B.e1b_done);
+            group_signal(&B.e1b_done, 2, 128, tl == 0);
             if (tile + 1 < my_tiles) {
                 pbase = token_base(tile + 1);
                 load_chunk(pbase, 0, buf[0]);
@@ -344,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     part[e & 3] += fmaxf(__uint_as_float(v1[e]), 0.0f) * s_hw[c0 + 32 + e];
             }
             tc_fence_before();
-            mbar_arrive(&B.acc3_empty);
+            group_signal(&B.acc3_empty, 3, 256, first);
             DS_TRACE(1, tile, 11);
             float p = (part[0] + part[1]) + (part[2] + part[3]);
 #pragma unroll
@@ -356,11 +394,15 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 float s = 0.0f;
 #pragma unroll
                 for (int w = 0; w < 8; ++w) s += B.warp_part[b][w];
-                img_acc += s;
-                if (tile % tpi == tpi - 1) {
-                    const long long img = unit + (tile / tpi) * nunits;
-                    P.part[img] = img_acc;
-                    img_acc = 0.0f;
+                const long long f = 2 * tile + rank;
+                if (f < my_flat) {                 // ghost tiles write nothing
+                    img_acc += s;
+                    // flush at this CTA's last tile of the image
+                    if (f + 2 >= my_flat || (f + 2) / tpi != f / tpi) {
+                        const long long img = unit + (f / tpi) * nunits;
+                        P.part[img * 2 + rank] = img_acc;
+                        img_acc = 0.0f;
+                    }
                 }
             }
         };
@@ -376,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                                       s1x2);
             fence_proxy_async_smem();
             tc_fence_before();
-            mbar_arrive(&B.drained);
+            group_signal(&B.drained, 3, 256, first);
             DS_TRACE(1, tile, 1);
 
             // ---- E3 of the previous tile (its G3_3 was issued after G1(tile)) ----
@@ -400,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                                                            __uint_as_float(v[2 * e + 1]));
                 }
                 tc_fence_before();
-                mbar_arrive(&B.drained);            // MMA may overwrite acc[0,256)
+                group_signal(&B.drained, 3, 256, first);   // MMA may overwrite acc[0,256)
                 if (tile > 0 || j > 0) {            // GEMM3 reading the previous H2 chunk done
                     mbar_wait(&B.h2_free, pfree);
                     pfree ^= 1;
@@ -416,15 +458,16 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     }
                 }
                 fence_proxy_async_smem();
-                mbar_arrive(&B.h2_ready);
+                group_signal(&B.h2_ready, 3, 256, first);
                 DS_TRACE(1, tile, 3 + 2 * j);
             }
         }
         if (my_tiles > 0) e3(my_tiles - 1);
     } else if (warp == 12) {
-        // ===================== weight producer ==============================
+        // ===================== weight producer (both CTAs) ====================
         if (lane == 0) {
             const uint64_t policy = policy_evict_last();
+            prefetch_tmap(&P.wmap);
             int bs = 0;
             uint32_t bp = 0;
             long long ptile = 0;   // trace only
@@ -432,10 +475,12 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 for (int t = first; t < first + count; ++t) {
                     mbar_wait(&B.b_empty[bs], bp ^ 1);
                     if (t < 16) DS_TRACE(6, ptile, t);
-                    mbar_arrive_expect_tx(&B.b_full[bs], kBStage);
-                    bulk_g2s_hint(smem + kBRing + bs * kBStage,
-                                  P.wblob + static_cast<size_t>(t) * kBStage, kBStage,
-                                  &B.b_full[bs], policy);
+                    // both CTAs load their N-half; completion lands on the leader's
+                    // barrier, which expects the whole stage
+                    if (leader) mbar_arrive_expect_tx(&B.b_full[bs], kBStage);
+                    tma_2d_pair(sbase + kBRing + bs * kBHalf, &P.wmap, 0,
+                                t * 256 + static_cast<int>(rank) * 128,
+                                mapa_shared(smem_u32(&B.b_full[bs]), 0), policy);
                     if (++bs == kBStages) { bs = 0; bp ^= 1; }
                 }
             };
@@ -459,46 +504,44 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             for (long long tile = 0; tile < my_tiles; ++tile) {
                 if (tile > 0) mbar_wait(&B.r1_free, static_cast<uint32_t>((tile - 1) & 1));
                 for (int k = 0; k < kXStages; ++k) {
-                    mbar_arrive_expect_tx(&B.x_full[k], kBStage);
-                    bulk_g2s_hint(smem + kR1 + k * kBStage, P.wblob + static_cast<size_t>(k) * kBStage,
-                                  kBStage, &B.x_full[k], policy);
+                    if (leader) mbar_arrive_expect_tx(&B.x_full[k], kBStage);
+                    tma_2d_pair(sbase + kR1 + k * kBHalf, &P.wmap, 0,
+                                k * 256 + static_cast<int>(rank) * 128,
+                                mapa_shared(smem_u32(&B.x_full[k]), 0), policy);
                 }
             }
         }
     } else {
-        // ===================== MMA issuer (warp 13, one thread) ==============
-        if (lane == 0) {
+        // ===================== MMA issuer (leader warp 13, one thread) ========
+        if (lane == 0 && leader) {
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0, pdr = 0, prd = 0, pe3 = 0;
             long long trace_tile = 0;   // trace only
             int trace_stage = 0;
             const uint32_t acc12 = tmem, acc3 = tmem + 256;
-            // next weight stage: wait until it landed, return its descriptor
+            // next ring stage: wait until both halves landed, return its descriptor
             auto next_b = [&]() -> uint64_t {
                 mbar_wait(&B.b_full[bs], bp);
                 tc_fence_after();
                 if (trace_stage < 16) DS_TRACE(7, trace_tile, trace_stage);
                 ++trace_stage;
-                return desc_k_sw64(sbase + kBRing + bs * kBStage);
+                return desc_k_sw128(sbase + kBRing + bs * kBHalf);
             };
             auto release_b = [&]() {
-                umma_commit(&B.b_empty[bs]);
+                umma_commit_pair(&B.b_empty[bs], 0x3);
                 if (++bs == kBStages) { bs = 0; bp ^= 1; }
             };
-            // bf16 GEMM, K = 64 x nk from an SW128 A region (nk chunks of 16 KB)
-            // against 2*nk weight stages (K = 32 each).
+            // bf16 GEMM, K = 64 x nk from an SW128 A region (nk chunks of 16 KB),
+            // one weight stage (K = 64) per chunk
             auto gemm = [&](uint32_t a_region, int nk, uint32_t acc, bool acc_in) {
                 for (int kc = 0; kc < nk; ++kc) {
                     const uint64_t ad = desc_k_sw128(a_region + kc * kAChunk);
+                    const uint64_t bd = next_b();
 #pragma unroll
-                    for (int hf = 0; hf < 2; ++hf) {
-                        const uint64_t bd = next_b();
-#pragma unroll
-                        for (int k = 0; k < 2; ++k)
-                            umma_bf16(acc, ad + 2 * (2 * hf + k), bd + 2 * k, kIdescF16,
-                                     (acc_in || kc > 0 || hf > 0 || k > 0) ? 1u : 0u);
-                        release_b();
-                    }
+                    for (int k = 0; k < 4; ++k)
+                        umma_bf16_pair(acc, ad + 2 * k, bd + 2 * k, kIdescF16,
+                                       (acc_in || kc > 0 || k > 0) ? 1u : 0u);
+                    release_b();
                 }
             };
             auto wait_bar = [&](uint64_t* bar, uint32_t& ph) {
@@ -510,40 +553,36 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 DS_TRACE(2, tile, 0);
                 trace_tile = tile;
                 trace_stage = 0;
-                // G1: 6 u8 A chunks (K = 128 bytes) x 2 int8 weight stages (K = 64);
-                // stages 0-3 come from the H1 region (x_full), the rest from the ring
+                // G1: 6 u8 A chunks (K = 128 bytes) x 6 int8 weight stages; stages
+                // 0-3 come from the H1 region (x_full), 4-5 from the ring
                 for (int c = 0; c < kChunksPerTile; ++c) {
                     mbar_wait(&B.a_full[as], ap);
                     tc_fence_after();
                     DS_TRACE(5, tile, c);
                     const uint64_t ad = desc_k_sw128(sbase + kARing + as * kAChunk);
-#pragma unroll
-                    for (int hf = 0; hf < 2; ++hf) {
-                        const int ws = 2 * c + hf;
-                        uint64_t bd;
-                        if (ws < kXStages) {
-                            mbar_wait(&B.x_full[ws], static_cast<uint32_t>(tile & 1));
-                            tc_fence_after();
-                            bd = desc_k_sw64(sbase + kR1 + ws * kBStage);
-                        } else {
-                            bd = next_b();
-                        }
-#pragma unroll
-                        for (int k = 0; k < 2; ++k)
-                            umma_i8(acc12, ad + 2 * (2 * hf + k), bd + 2 * k, kIdescI8,
-                                    (c > 0 || hf > 0 || k > 0) ? 1u : 0u);
-                        if (ws >= kXStages) release_b();
+                    uint64_t bd;
+                    if (c < kXStages) {
+                        mbar_wait(&B.x_full[c], static_cast<uint32_t>(tile & 1));
+                        tc_fence_after();
+                        bd = desc_k_sw128(sbase + kR1 + c * kBHalf);
+                    } else {
+                        bd = next_b();
                     }
-                    umma_commit(&B.a_empty[as]);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        umma_i8_pair(acc12, ad + 2 * k, bd + 2 * k, kIdescI8,
+                                     (c > 0 || k > 0) ? 1u : 0u);
+                    if (c >= kXStages) release_b();
+                    umma_commit_pair(&B.a_empty[as], 0x3);
                     if (++as == kAStages) { as = 0; ap ^= 1; }
                 }
-                umma_commit(&B.acc12_full);
+                umma_commit_pair(&B.acc12_full, 0x3);
                 DS_TRACE(2, tile, 1);
                 if (tile > 0) {                      // G3_3 of the previous tile
                     wait_bar(&B.h2_ready, prd);
                     gemm(sbase + kR2, 4, acc3, true);
-                    umma_commit(&B.h2_free);
-                    umma_commit(&B.acc3_full);
+                    umma_commit_pair(&B.h2_free, 0x3);
+                    umma_commit_pair(&B.acc3_full, 0x3);
                 }
                 DS_TRACE(2, tile, 2);
                 wait_bar(&B.drained, pdr);           // E1: acc drained, H1 stored
@@ -551,13 +590,13 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 tc_fence_after();
                 DS_TRACE(2, tile, 3);
                 gemm(sbase + kR1, 4, acc12, false);  // G2_0
-                umma_commit(&B.acc12_full);
+                umma_commit_pair(&B.acc12_full, 0x3);
                 for (int j = 1; j < 4; ++j) {
                     wait_bar(&B.drained, pdr);       // E2_{j-1} has the values in registers
                     DS_TRACE(2, tile, 2 + 2 * j);
                     gemm(sbase + kR1, 4, acc12, false);       // G2_j
-                    umma_commit(&B.acc12_full);
-                    if (j == 3) umma_commit(&B.r1_free);      // H1 read for the last time
+                    umma_commit_pair(&B.acc12_full, 0x3);
+                    if (j == 3) umma_commit_pair(&B.r1_free, 0x3);   // H1 read for the last time
                     wait_bar(&B.h2_ready, prd);      // H2_{j-1} stored
                     DS_TRACE(2, tile, 3 + 2 * j);
                     if (j == 1) {                    // acc3 drained by E3 of the previous tile
@@ -566,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                         tc_fence_after();
                     }
                     gemm(sbase + kR2, 4, acc3, j > 1);        // G3_{j-1}
-                    umma_commit(&B.h2_free);
+                    umma_commit_pair(&B.h2_free, 0x3);
                 }
                 wait_bar(&B.drained, pdr);           // E2_3 drained: acc[0,256) free
                 DS_TRACE(2, tile, 10);
@@ -574,8 +613,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             if (my_tiles > 0) {
                 wait_bar(&B.h2_ready, prd);
                 gemm(sbase + kR2, 4, acc3, true);    // G3_3 of the last tile
-                umma_commit(&B.h2_free);
-                umma_commit(&B.acc3_full);
+                umma_commit_pair(&B.h2_free, 0x3);
+                umma_commit_pair(&B.acc3_full, 0x3);
             }
         }
     }
@@ -583,18 +622,19 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     __syncthreads();
     if (P.trace && threadIdx.x == 0)
         P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
+    cluster_sync();     // both CTAs done with TMEM / remote barriers
     if (warp == 13) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem);
+        tmem_dealloc2<512>(tmem);
     }
 }
 
-// logit = (per-image sum of the head scores) / tokens + b_head
+// logit = (sum of the pair's per-image head sums) / tokens + b_head
 __global__ void finalize_kernel(const float* __restrict__ part, long long n, int tokens, float hb,
                                 int logits, float* __restrict__ out) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float logit = part[i] / static_cast<float>(tokens) + hb;
+    const float logit = (part[2 * i] + part[2 * i + 1]) / static_cast<float>(tokens) + hb;
     out[i] = logits ? logit : 1.0f / (1.0f + expf(-logit));
 }
 
@@ -650,30 +690,31 @@ __global__ void gen_weights_kernel(uint64_t seed, int8_t* q1, uint16_t* w2, uint
     }
 }
 
-// Pre-swizzled blob of 16 KB stages (256 rows = N x 64 bytes of K, SW64):
-//   stages  0..11 : Q1 (int8), K-range [64s, 64s+64)
-//   stages 12..43 : W2 N-chunk j (rows 256j..), K-range [32k, 32k+32) (bf16), j-major
-//   stages 44..75 : W3 K-chunk j (input rows 256j + 32k ..), all 256 outputs
+// Pre-swizzled blob of 32 KB stages (256 rows = N x 128 bytes of K, SW128;
+// rows 0-127 and 128-255 are the two contiguous 16 KB N-halves):
+//   stages  0..5  : Q1 (int8), K-range [128s, 128s+128)
+//   stages  6..21 : W2 N-chunk j (rows 256j..), K-range [64k, 64k+64) (bf16), j-major
+//   stages 22..37 : W3 K-chunk j (input rows 256j + 64k ..), all 256 outputs
 __global__ void tile_weights_kernel(const int8_t* q1, const uint16_t* w2, const uint16_t* w3,
                                     uint8_t* blob) {
     const int t = blockIdx.x;
     uint8_t* out = blob + static_cast<size_t>(t) * kBStage;
-    for (int e = threadIdx.x; e < 256 * 64; e += blockDim.x) {   // (row n, K byte kb)
-        const int n = e / 64, kb = e % 64;
-        const uint32_t byte = (n >> 3) * 512u + (n & 7) * 64u +
-                              ((((kb >> 4) ^ ((n >> 1) & 3))) << 4) + (kb & 15);
+    for (int e = threadIdx.x; e < 256 * 128; e += blockDim.x) {   // (row n, K byte kb)
+        const int n = e / 128, kb = e % 128;
+        const uint32_t byte = (n >> 3) * 1024u + (n & 7) * 128u +
+                              ((((kb >> 4) ^ (n & 7))) << 4) + (kb & 15);
         if (t < kW1Stages) {
-            out[byte] = static_cast<uint8_t>(q1[(64 * t + kb) * kD1 + n]);
+            out[byte] = static_cast<uint8_t>(q1[(128 * t + kb) * kD1 + n]);
         } else if (!(kb & 1)) {
             const int kl = kb >> 1;
             uint16_t v;
             if (t < kW1Stages + 4 * kWChunkStages) {
                 const int u = t - kW1Stages, j = u / kWChunkStages, k = u % kWChunkStages;
-                v = w2[(32 * k + kl) * kD2 + 256 * j + n];
+                v = w2[(64 * k + kl) * kD2 + 256 * j + n];
             } else {
                 const int u = t - kW1Stages - 4 * kWChunkStages, j = u / kWChunkStages,
                           k = u % kWChunkStages;
-                v = w3[(256 * j + 32 * k + kl) * kD3 + n];
+                v = w3[(256 * j + 64 * k + kl) * kD3 + n];
             }
             *reinterpret_cast<uint16_t*>(out + byte) = v;
         }
@@ -696,6 +737,32 @@ __global__ void fold_bias_kernel(const int8_t* q1, uint64_t seed, float* b1) {
 }
 
 } // namespace
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static ds_status make_weight_tmap(const void* blob, CUtensorMap* out) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    DS_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+        return dsi::fail(DS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    // [rows = 38 stages x 256][128 bytes] row-major; a box of 128 rows copies
+    // one pre-swizzled N-half of a stage (16 KB, contiguous) byte for byte.
+    const cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(kBlobStages) * 256};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {128, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = reinterpret_cast<EncodeFn>(fn)(
+        out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(blob), dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return dsi::fail(DS_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return DS_OK;
+}
 
 struct ds_disc {
     ds_ctx* ctx = nullptr;
@@ -722,7 +789,6 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     if (n <= 0) return DS_OK;
     DiscParams p = d->params;
     p.images = images;
-    p.wblob = d->d_blob;
     p.n_img = n;
     p.h = h;
     p.w = w;
@@ -731,15 +797,28 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     p.tiles_per_img = tokens / kM;
     p.trace = trace;
     float* part = nullptr;
-    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * n, st));
+    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * 2 * n, st));
+    DS_CUDA_TRY(cudaMemsetAsync(part, 0, sizeof(float) * 2 * n, st));
     p.part = part;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->ctx->device);
-    const int units = static_cast<int>(n < sms ? n : sms);
+    const int pairs = static_cast<int>(n < sms / 2 ? n : sms / 2);
     // per device (one ds_ctx per GPU in a process): cheap, so set every launch
     DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kSmemBytes));
-    disc_kernel<<<static_cast<unsigned>(units), kThreads, kSmemBytes, st>>>(p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, disc_kernel, p));
     DS_LAUNCH_CHECK(d->ctx, "disc_kernel");
     finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(part, n, tokens, d->hb,
                                                                            logits, out);
@@ -781,6 +860,10 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
     fold_bias_kernel<<<1, 256, 0, st>>>(d->d_q1, weight_seed, d->d_b1);
     ctx->launches.fetch_add(3);
     if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(dsi::cuda_fail(e, "weight init"));
+    {
+        const ds_status ts = make_weight_tmap(d->d_blob, &d->params.wmap);
+        if (ts != DS_OK) return cleanup(ts);
+    }
     if ((e = cudaMemcpyAsync(d->params.b1, d->d_b1, sizeof(d->params.b1), cudaMemcpyDeviceToHost,
                              st)) != cudaSuccess)
         return cleanup(dsi::cuda_fail(e, "copy b1"));
