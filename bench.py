@@ -62,6 +62,7 @@ CPU_LATENT_SAMPLE = 200_000   # queries for the CPU reference scorer
 WL_RATES = [2500.0] * 400     # 400 s at 2,500 qps: 1,000,811 arrivals at seed 3
 WL_SEED = 3
 N_CSV = 1_000_000
+N_SCALE = 1_000_000           # config 5: queries over the whole world
 CPU_CSV_SAMPLE = 200_000      # records through the reference's write_csv
 
 
@@ -76,54 +77,70 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock, power and throttle reasons sampled DURING the timed region:
+    NVML polled every 2 ms from a thread (nvidia-smi's 100 ms cadence misses
+    most of a ~0.1 s timed region); nvidia-smi as the fallback."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.rows = []     # (sm_mhz, max_mhz, power_w, set of reason names)
+        self.stop_flag = False
+        self.thread = None
+        self.err = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            def run():
+                while not self.stop_flag:
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((float(sm), float(mx), pw,
+                                          {k for k, b in bits.items() if rs & b}))
+                    except Exception as e:   # keep sampling
+                        self.err = str(e)
+                    time.sleep(0.002)
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+        except Exception as e:
+            self.err = str(e)
+            self.thread = None
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
+        self.stop_flag = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": [f"no clock samples ({self.err})"]}
+        try:   # raw samples for inspection (not part of the JSON line)
+            with open(os.path.join(ROOT, "gpurun_out", "clocks_raw.csv"), "w") as f:
+                for r in self.rows:
+                    f.write(f"{r[0]},{r[1]},{r[2]},{'|'.join(sorted(r[3]))}\n")
         except Exception:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            pass
+        pmax = max(r[2] for r in self.rows)
+        # samples taken while the GPU was busy (power >= half the peak seen)
+        busy = [r for r in self.rows if r[2] >= 0.5 * pmax] or self.rows
         reasons = set()
-        for r in self.rows:
-            if len(r) < 8:
-                continue
-            for k, nm in enumerate(names):
-                if r[4 + k].lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        for r in busy:
+            reasons |= r[3]
+        return {"sm_mhz": statistics.median(r[0] for r in busy),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": sorted(reasons),
+                "power_w_max": pmax, "samples_under_load": len(busy),
+                "samples": len(self.rows), "source": "nvml, 2 ms"}
 
 
 def dist_env():
@@ -432,7 +449,6 @@ def run_gpu(args):
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
-    time.sleep(0.3)
     n0 = ctx.launches()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
@@ -484,6 +500,110 @@ def run_gpu(args):
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_value = ws * N_IMG / allmax([e2e_s])[0]
     h2d = N_IMG * H * W * 3 + grid_np.nbytes + 2 * abi.CURVE.itemsize
+
+    # ---- image legs for the other configs ------------------------
+    def timed(fn, reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    # config 5 (scale-out): 1M queries over the world, contiguous id shards of
+    # 1M/N per GPU scored in 5K chunks from the resident pool, routed at t = 0.5
+    # with global ids, then the routed-count all-gather -> global offsets
+    n5 = N_SCALE // ws
+    id5 = rank * n5
+    conf5 = torch.empty(n5, dtype=torch.float32, device=dev)
+    heavy5 = torch.empty(n5, dtype=torch.int64, device=dev)
+    count5 = torch.empty(1, dtype=torch.int64, device=dev)
+    thr5 = torch.tensor([0.5], dtype=torch.float64, device=dev)
+
+    def scale_step():
+        with torch.cuda.stream(stream):
+            for off in range(0, n5, N_IMG):
+                m = min(N_IMG, n5 - off)
+                native.check(L.ds_disc_score_device(
+                    disc.handle, native.c_p(images.data_ptr()), m, H, W,
+                    native.c_p(conf5.data_ptr() + 4 * off), native.c_p(ctx.stream)))
+            native.check(L.ds_route_device(ctx.handle, native.c_p(conf5.data_ptr()), abi.CONF_F32,
+                                           n5, native.c_p(thr5.data_ptr()), 1, id5,
+                                           native.c_p(heavy5.data_ptr()),
+                                           native.c_p(count5.data_ptr()), native.c_p(ctx.stream)))
+            if ws > 1:
+                ddist.global_offsets_device(count5)
+    scale_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    scale_ms = allmax([timed(scale_step, 1)])[0]
+    scale_value = N_SCALE / (scale_ms / 1000.0)
+    scale_routed = int(count5.item())
+
+    # config 1 (cascade 1): the same pool in light batches of 32 -- per batch:
+    # score, observe the 32 confidences into the curve, route at the plan's
+    # threshold (cluster.cpp:288-307 order)
+    B1 = 32
+    conf1 = torch.empty(N_IMG, dtype=torch.float32, device=dev)
+    heavy1 = torch.empty(B1, dtype=torch.int64, device=dev)
+    count1 = torch.empty(1, dtype=torch.int64, device=dev)
+    curve1 = torch.empty_like(prior_t)
+
+    def batch32_step():
+        with torch.cuda.stream(stream):
+            curve1.copy_(prior_t)
+            for off in range(0, N_IMG, B1):
+                m = min(B1, N_IMG - off)
+                cp = native.c_p(conf1.data_ptr() + 4 * off)
+                native.check(L.ds_disc_score_device(
+                    disc.handle, native.c_p(images.data_ptr() + off * H * W * 3), m, H, W, cp,
+                    native.c_p(ctx.stream)))
+                native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve1.data_ptr()),
+                                                       cp, abi.CONF_F32, m, DECAY,
+                                                       native.c_p(ctx.stream)))
+                native.check(L.ds_route_device(ctx.handle, cp, abi.CONF_F32, m,
+                                               native.c_p(thr5.data_ptr()), 1, id0 + off,
+                                               native.c_p(heavy1.data_ptr()),
+                                               native.c_p(count1.data_ptr()),
+                                               native.c_p(ctx.stream)))
+    batch32_step()
+    torch.cuda.synchronize()
+    b32_ms = allmax([timed(batch32_step, 2)])[0]
+    b32_value = ws * N_IMG / (b32_ms / 1000.0)
+    b32_batch_us = b32_ms * 1000.0 / ((N_IMG + B1 - 1) // B1)
+    b32_parity = bool(torch.equal(conf1, conf))
+    del conf1
+
+    # config 3 (cascade 3): 5K synthetic 1024x1024 images (15.7 GB) per GPU,
+    # score + route at the 101 thresholds + curve replay
+    N3, H3 = N_IMG, 1024
+    images3 = torch.empty(N3 * H3 * H3 * 3, dtype=torch.uint8, device=dev)
+    native.check(L.ds_synth_images_device(ctx.handle, 3, id0, N3, H3, H3,
+                                          native.c_p(images3.data_ptr()), native.c_p(ctx.stream)))
+    conf3 = torch.empty(N3, dtype=torch.float32, device=dev)
+
+    def c3_step():
+        with torch.cuda.stream(stream):
+            native.check(L.ds_disc_score_device(disc.handle, native.c_p(images3.data_ptr()), N3,
+                                                H3, H3, native.c_p(conf3.data_ptr()),
+                                                native.c_p(ctx.stream)))
+            native.check(L.ds_route_device(ctx.handle, native.c_p(conf3.data_ptr()), abi.CONF_F32,
+                                           N3, native.c_p(grid_t.data_ptr()), NT, id0,
+                                           native.c_p(heavy.data_ptr()),
+                                           native.c_p(counts.data_ptr()), native.c_p(ctx.stream)))
+            curve_t.copy_(prior_t)
+            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve_t.data_ptr()),
+                                                   native.c_p(conf3.data_ptr()), abi.CONF_F32,
+                                                   N3, DECAY, native.c_p(ctx.stream)))
+    c3_step()
+    torch.cuda.synchronize()
+    c3_ms = allmax([timed(c3_step, 3)])[0]
+    c3_value = ws * N3 / (c3_ms / 1000.0)
+    c3_tflops = N3 * DISC_FLOP_BF16_EQ * 4 / (c3_ms / 1000.0) / 1e12
+    del images3
 
     # ---- planner leg (config 4) -------------------------------------------------
     pro, cas, grid, offs = planner_inputs()
@@ -661,6 +781,20 @@ def run_gpu(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "parity": {"route_counts_vs_confidences": parity_ok},
+            "scaleout": {"value": scale_value, "unit": "images/s", "queries": N_SCALE,
+                         "queries_per_gpu": n5, "ms": scale_ms, "routed_at_0.5_rank0": scale_routed,
+                         "config": "config 5: 1M 512x512 queries, contiguous id shards, 5K "
+                                   "resident pool, route t=0.5, routed-count all-gather"},
+            "cascade1_batch32": {"value": b32_value, "unit": "images/s",
+                                 "us_per_batch": b32_batch_us, "batch": B1,
+                                 "parity_vs_full_batch": b32_parity,
+                                 "config": "config 1: 5K 512x512 in light batches of 32: score, "
+                                           "observe into the curve, route at t=0.5"},
+            "cascade3": {"value": c3_value, "unit": "images/s", "image_hw": [H3, H3],
+                         "images": N3, "ms_per_step": c3_ms,
+                         "disc_bf16eq_tflops_step": c3_tflops,
+                         "config": "config 3: 5K 1024x1024 (15.7 GB), score + route at 101 "
+                                   "thresholds + curve replay"},
             "planner": {"value": plan_value, "unit": "candidates/s", "problems": len(pro),
                         "candidates_per_problem": CANDS_PER_PROBLEM, "ms_per_batch": plan_ms,
                         "e2e": {"value": plan_e2e, "unit": "candidates/s"}},
