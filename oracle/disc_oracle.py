@@ -5,7 +5,8 @@ PARITY UNPINNED against the reference: the reference has no discriminator
 network (SURVEY.md 8(c) row "Discriminator network (S9)"). This is
 a restatement of THIS repo's PatchDisc definition (DESIGN.md
 "Discriminator"): layer 1 as the exact integer GEMM the kernel runs (u8 pixels
-x int8 weights, int64 here / s32 on the tensor cores -- identical sums), then
+x int8 weights, exact integer sums in fp64 here / s32 on the tensor cores --
+identical values), then
 fp32 numpy with the same bf16 rounding points as the GPU kernel (H1 and H2
 are rounded to bf16 before the next GEMM), used to check
 paper_2411_15381_b200/csrc/disc.cu within the north_star tolerance
@@ -68,14 +69,16 @@ def patches(images: np.ndarray) -> np.ndarray:
 
 
 def disc_forward(images: np.ndarray, wts: dict, logits: bool = False) -> np.ndarray:
-    q1 = wts["q1"].astype(np.int64)
+    q1 = wts["q1"].astype(np.float64)
     s1 = np.float32(wts["s1"])
     w2 = bf16_bits_to_f32(wts["w2"])
     w3 = bf16_bits_to_f32(wts["w3"])
     out = np.zeros(len(images), np.float32)
     for i in range(len(images)):
-        x = patches(images[i:i + 1])[0].astype(np.int64)
-        acc = (x @ q1).astype(np.float32)               # exact s32 sums, then f32 (|acc| < 2^25)
+        x = patches(images[i:i + 1])[0].astype(np.float64)
+        # the exact integer sums (|acc| <= 768*255*127 < 2^53: every fp64 partial
+        # sum is an exact integer in any order, so BLAS dgemm is exact), then f32
+        acc = (x @ q1).astype(np.float32)
         h1 = round_bf16(gelu_tanh(acc * s1 + wts["b1"]))
         h2 = round_bf16(np.maximum(h1 @ w2 + wts["b2"], 0.0))
         h3 = np.maximum(h2 @ w3 + wts["b3"], 0.0)

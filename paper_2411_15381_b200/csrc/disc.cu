@@ -81,7 +81,11 @@ constexpr int kThreads = 480;
 constexpr float kConst = 16.0f;         // value of the constant features
 constexpr int kAStages = 2, kBStages = 4;
 constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (idle during GEMM1)
-constexpr int kE1Split = 192;           // E1 columns [0,192): epilogue warps; [192,256): A-builders
+#ifndef DS_E1_SPLIT
+#define DS_E1_SPLIT 192
+#endif
+constexpr int kE1Split = DS_E1_SPLIT;   // E1 columns [0,192): epilogue warps; [192,256): A-builders
+static_assert(kE1Split % 64 == 0 && kE1Split >= 64 && kE1Split <= 256, "E1 split: 32-column blocks per half");
 // shared memory map (bytes, per CTA)
 constexpr int kR1 = 0;                              // H1: 4 K-chunks x 16 KB (bf16, SW128)
 constexpr int kR2 = kR1 + 65536;                    // H2_j: 4 K-chunks x 16 KB
@@ -315,7 +319,9 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         for (long long tile = 0; tile < my_tiles; ++tile) {
             if (tl == 0) {
                 DS_TRACE(0, tile, 0);
+#if !defined(DS_NO_PF) && !defined(DS_PF_LATE)
                 if (tile + 2 < my_tiles) prefetch_tile(tile + 2);
+#endif
             }
 #pragma unroll
             for (int c = 0; c < kChunksPerTile; ++c) {
@@ -337,12 +343,17 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             // acc12_full phase of E1(tile) has parity tile & 1; the barrier cannot
             // be behind it (the A slots just freed were released after GEMM2_3 of
             // the previous tile) nor past it (GEMM2_0 waits for e1b_done).
-            mbar_wait(&B.acc12_full, static_cast<uint32_t>(tile & 1));
-            tc_fence_after();
-            e1_columns<(256 - kE1Split) / 32>(tmem_lane, kE1Split, tl, sbase + kR1, s_b1, s1x2);
-            fence_proxy_async_smem();
-            tc_fence_before();
+            if constexpr (kE1Split < 256) {
+                mbar_wait(&B.acc12_full, static_cast<uint32_t>(tile & 1));
+                tc_fence_after();
+                e1_columns<(256 - kE1Split) / 32>(tmem_lane, kE1Split, tl, sbase + kR1, s_b1, s1x2);
+                fence_proxy_async_smem();
+                tc_fence_before();
+            }
             group_signal(&B.e1b_done, 2, 128, tl == 0);
+#ifdef DS_PF_LATE
+            if (tl == 0 && tile + 3 < my_tiles) prefetch_tile(tile + 3);
+#endif
             if (tile + 1 < my_tiles) {
                 pbase = token_base(tile + 1);
                 load_chunk(pbase, 0, buf[0]);
