@@ -641,6 +641,48 @@ def run_gpu(args):
         ctx.plan_batch(pro, cas, grid, offs)
     plan_e2e = ws * len(pro) * CANDS_PER_PROBLEM / allmax([(time.perf_counter() - t0) / 3])[0]
 
+    # ---- planner, threshold-range sharded: every rank searches its slice of
+    # the 101-point grid for the SAME problems, then an all-reduce MIN of the
+    # packed selection keys (NCCL) and the decode (SURVEY 8(e) "by t-range")
+    G_T = int(grid.size)
+    t_lo, t_hi = ddist.shard_range(G_T, ws, rank)
+    d_keys = torch.empty(len(pro), dtype=torch.int64, device=dev)
+    d_out2 = torch.empty_like(d_out)
+    i64max = torch.iinfo(torch.int64).max
+
+    def tplan_step():
+        with torch.cuda.stream(stream):
+            native.check(L.ds_plan_keys_device(ctx.handle, native.c_p(d_pro.data_ptr()), len(pro),
+                                               native.c_p(d_cas.data_ptr()), len(cas),
+                                               native.c_p(d_grid.data_ptr()),
+                                               native.c_p(d_offs.data_ptr()), 1, t_lo, t_hi,
+                                               native.c_p(d_keys.data_ptr()),
+                                               native.c_p(ctx.stream)))
+            if ws > 1:
+                # uint64 keys as int64 with "none" (all ones = -1) -> INT64_MAX
+                k = torch.where(d_keys == -1, torch.full_like(d_keys, i64max), d_keys)
+                if backend == "gloo":
+                    kc = k.cpu()
+                    dist.all_reduce(kc, op=dist.ReduceOp.MIN)
+                    k = kc.to(dev)
+                else:
+                    dist.all_reduce(k, op=dist.ReduceOp.MIN)
+                d_keys.copy_(torch.where(k == i64max, torch.full_like(k, -1), k))
+            native.check(L.ds_plan_from_keys_device(ctx.handle, native.c_p(d_pro.data_ptr()),
+                                                    len(pro), native.c_p(d_cas.data_ptr()),
+                                                    len(cas), native.c_p(d_grid.data_ptr()),
+                                                    native.c_p(d_offs.data_ptr()), 1,
+                                                    native.c_p(d_keys.data_ptr()),
+                                                    native.c_p(d_out2.data_ptr()),
+                                                    native.c_p(ctx.stream)))
+    tplan_step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    tplan_ms = allmax([timed(tplan_step, max(3, args.steps // 2))])[0]
+    tplan_value = len(pro) * CANDS_PER_PROBLEM / (tplan_ms / 1000.0)
+    tplan_parity = bool(torch.equal(d_out2, d_out))
+
     # ---- latent leg (config 5: 1M queries per GPU, reference-parity scorer) ------
     lconf = torch.empty(N_LATENT, dtype=torch.float64, device=dev)
     lheavy = torch.empty(N_LATENT, dtype=torch.int64, device=dev)
@@ -795,6 +837,13 @@ def run_gpu(args):
                          "disc_bf16eq_tflops_step": c3_tflops,
                          "config": "config 3: 5K 1024x1024 (15.7 GB), score + route at 101 "
                                    "thresholds + curve replay"},
+            "planner_t_sharded": {"value": tplan_value, "unit": "candidates/s",
+                                  "problems": len(pro), "grid_slice": [t_lo, t_hi],
+                                  "ms_per_batch": tplan_ms, "scaling": "strong",
+                                  "parity_vs_problem_sharded": tplan_parity,
+                                  "config": "config 4 problems, each rank a contiguous slice of "
+                                            "the threshold grid, all-reduce MIN of the packed "
+                                            "keys, decode"},
             "planner": {"value": plan_value, "unit": "candidates/s", "problems": len(pro),
                         "candidates_per_problem": CANDS_PER_PROBLEM, "ms_per_batch": plan_ms,
                         "e2e": {"value": plan_e2e, "unit": "candidates/s"}},

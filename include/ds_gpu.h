@@ -160,6 +160,35 @@ ds_status ds_plan_batch_device(ds_ctx* ctx, const ds_problem* problems, int32_t 
                                const ds_cascade* cascades, int32_t n_cascades,
                                const double* grid_values, const int32_t* grid_offsets,
                                int32_t n_grids, ds_plan* out, void* stream);
+/* Threshold-range sharding of the planner ("shard t-ranges
+ * ... ncclAllReduce(uint64 key, ncclMin) per problem"). ds_plan_keys searches
+ * only grid indices [t_lo, t_hi) of each grid-mode problem (DS_SOLVE,
+ * DS_SOLVE_FIXED_BATCHES) and returns its packed selection key
+ *   (G-1-t_idx)<<40 | (x1+x2)<<28 | (255-b1_idx)<<20 | (255-b2_idx)<<12 | x1
+ * (UINT64_MAX: no valid candidate in the range; always for the other modes),
+ * whose unsigned order is the reference's choice order (allocator.cpp:57-67,
+ * 91-121), so the minimum over disjoint ranges -- one per GPU -- equals the
+ * full search's key. ds_plan_from_keys turns the reduced keys into the plans
+ * ds_plan_batch returns (decode, or the reference's fallbacks; non-grid modes
+ * are solved whole). Same validation and errors as ds_plan_batch. */
+ds_status ds_plan_keys(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                       const ds_cascade* cascades, int32_t n_cascades, const double* grid_values,
+                       const int32_t* grid_offsets, int32_t n_grids, int32_t t_lo, int32_t t_hi,
+                       uint64_t* keys);
+ds_status ds_plan_keys_device(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                              const ds_cascade* cascades, int32_t n_cascades,
+                              const double* grid_values, const int32_t* grid_offsets,
+                              int32_t n_grids, int32_t t_lo, int32_t t_hi, uint64_t* keys,
+                              void* stream);
+ds_status ds_plan_from_keys(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                            const ds_cascade* cascades, int32_t n_cascades,
+                            const double* grid_values, const int32_t* grid_offsets,
+                            int32_t n_grids, const uint64_t* keys, ds_plan* out);
+ds_status ds_plan_from_keys_device(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                                   const ds_cascade* cascades, int32_t n_cascades,
+                                   const double* grid_values, const int32_t* grid_offsets,
+                                   int32_t n_grids, const uint64_t* keys, ds_plan* out,
+                                   void* stream);
 /* Host-side validation only (the checks ds_plan_batch runs before launch). */
 ds_status ds_plan_validate(const ds_problem* problems, int32_t n, const ds_cascade* cascades,
                            int32_t n_cascades, const double* grid_values,

@@ -678,6 +678,44 @@ int dso_solve_one(const ds_problem* p, const ds_cascade* c, const double* grid, 
     return DS_ERR_INVALID_ARGUMENT;
 }
 
+/* Threshold-range restatement of search (allocator.cpp:91-121) for the
+ * t-sharded planner: grid indices [t_lo, t_hi) walked from the top, the
+ * winner encoded as the packed key whose unsigned order is the reference's
+ * choice order (first valid t from the top, then better_than):
+ *   (G-1-t_idx)<<40 | (x1+x2)<<28 | (255-b1_idx)<<20 | (255-b2_idx)<<12 | x1.
+ * UINT64_MAX when the slice has no valid candidate or the mode is not a grid
+ * mode (DS_SOLVE, DS_SOLVE_FIXED_BATCHES). Inputs are assumed valid. */
+int dso_plan_keys(const ds_problem* problems, int32_t n, const ds_cascade* cascades,
+                  const double* grid_values, const int32_t* grid_offsets, int32_t t_lo,
+                  int32_t t_hi, uint64_t* keys) {
+    for (int i = 0; i < n; ++i) {
+        const ds_problem* p = &problems[i];
+        const ds_cascade* c = &cascades[p->cascade];
+        keys[i] = UINT64_MAX;
+        if (p->mode != DS_SOLVE && p->mode != DS_SOLVE_FIXED_BATCHES) continue;
+        const double* g = grid_values + grid_offsets[p->grid];
+        const int G = grid_offsets[p->grid + 1] - grid_offsets[p->grid];
+        int b1s[DS_MAX_BATCHES], b2s[DS_MAX_BATCHES], n1 = 0, n2 = 0;
+        for (int k = 0; k < c->light.n; ++k)
+            if (p->mode == DS_SOLVE || c->light.batch[k] == p->fixed_b1) b1s[n1++] = c->light.batch[k];
+        for (int k = 0; k < c->heavy.n; ++k)
+            if (p->mode == DS_SOLVE || c->heavy.batch[k] == p->fixed_b2) b2s[n2++] = c->heavy.batch[k];
+        const int hi = t_hi < G ? t_hi : G, lo = t_lo > 0 ? t_lo : 0;
+        int err = 0;
+        for (int t = hi - 1; t >= lo; --t) {
+            cand best = search(p, c, &g[t], 1, b1s, n1, b2s, n2, &err);
+            if (err) return err;
+            if (!best.valid) continue;
+            const int bi = find_batch(&c->light, best.plan.b1), bj = find_batch(&c->heavy, best.plan.b2);
+            keys[i] = ((uint64_t)(G - 1 - t) << 40) | ((uint64_t)(best.plan.x1 + best.plan.x2) << 28) |
+                      ((uint64_t)(255 - bi) << 20) | ((uint64_t)(255 - bj) << 12) |
+                      (uint64_t)best.plan.x1;
+            break;
+        }
+    }
+    return DS_OK;
+}
+
 typedef struct {
     const ds_problem* p;
     const ds_cascade* c;

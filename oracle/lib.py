@@ -111,5 +111,6 @@ def port():
         lib.dso_route_loop.argtypes = [c_p, i64, f64, ctypes.c_int, f64, c_p, c_p, c_p]
         lib.dso_solve_one.argtypes = [c_p, c_p, c_p, ctypes.c_int, c_p]
         lib.dso_plan_batch.argtypes = [c_p, i32, c_p, c_p, c_p, c_p, c_p, ctypes.c_int]
+        lib.dso_plan_keys.argtypes = [c_p, i32, c_p, c_p, c_p, i32, i32, c_p]
         _port = lib
     return _port

@@ -115,17 +115,19 @@ __device__ __forceinline__ unsigned long long tie_key(int x1, int x2, int i, int
            static_cast<unsigned long long>(x1);
 }
 
-// The search (allocator.cpp:91-121) over thresholds `grid[0..G)` walked from
-// the top, restricted to b1 index set [i0, i1) and b2 index set [j0, j1).
-// Returns the winning key (kNone if no candidate is valid).
-__device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int n1, int n2,
-                                     int i0, int i1, int j0, int j1, double need_light,
-                                     double total, int S) {
+// The search (allocator.cpp:91-121) over thresholds `grid[t_lo..t_hi)` of a
+// grid of G walked from the top, restricted to b1 index set [i0, i1) and b2
+// index set [j0, j1). Returns the winning key (kNone if no candidate is valid).
+// Keys carry the GLOBAL threshold index, so the minimum over disjoint
+// threshold ranges (e.g. one range per GPU) is the key of the full search.
+__device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int t_lo, int t_hi,
+                                     int n1, int n2, int i0, int i1, int j0, int j1,
+                                     double need_light, double total, int S) {
     const int ni = i1 - i0, nj = j1 - j0;
     unsigned long long best = kNone;
     int parity = 0;
-    for (int hi = G; hi > 0; hi -= kTChunk) {
-        const int lo = hi > kTChunk ? hi - kTChunk : 0;
+    for (int hi = t_hi; hi > t_lo; hi -= kTChunk) {
+        const int lo = hi - kTChunk > t_lo ? hi - kTChunk : t_lo;
         const int cnt = hi - lo;
         for (int k = threadIdx.x; k < cnt; k += kThreads)
             s.ft[k] = __dmul_rn(need_light, deferral_fraction(s, total, grid[lo + k]));
@@ -247,7 +249,13 @@ __global__ void __launch_bounds__(kThreads)
 plan_sweep_kernel(const ds_problem* __restrict__ problems, int n,
                   const ds_cascade* __restrict__ cascades,
                   const double* __restrict__ grid_values,
-                  const int32_t* __restrict__ grid_offsets, ds_plan* __restrict__ out) {
+                  const int32_t* __restrict__ grid_offsets, ds_plan* __restrict__ out,
+                  int t_lo, int t_hi, unsigned long long* __restrict__ keys_out,
+                  const unsigned long long* __restrict__ keys_in) {
+    // keys_out: search grid indices [t_lo, t_hi) only and write the packed key
+    //           (grid modes; kNone for the others) instead of a plan.
+    // keys_in : skip the search of grid modes and decode the given key (the
+    //           min over ranks of keys_out), with the reference's fallbacks.
     __shared__ PlanSmem s;
     const int pi = blockIdx.x;
     if (pi >= n) return;
@@ -329,8 +337,19 @@ plan_sweep_kernel(const ds_problem* __restrict__ problems, int n,
             grid = grid_values + grid_offsets[p.grid];
             G = grid_offsets[p.grid + 1] - grid_offsets[p.grid];
         }
-        const unsigned long long key =
-            search(s, grid, G, n1, n2, i0, i1, j0, j1, need_light, total, S);
+        const bool grid_mode = mode != DS_SOLVE_PINNED;
+        unsigned long long key;
+        if (keys_in && grid_mode) {
+            key = keys_in[pi];
+        } else {
+            const int lo = keys_out && grid_mode ? (t_lo > 0 ? t_lo : 0) : 0;
+            const int hi = keys_out && grid_mode ? (t_hi < G ? t_hi : G) : G;
+            key = search(s, grid, G, lo, hi, n1, n2, i0, i1, j0, j1, need_light, total, S);
+        }
+        if (keys_out) {
+            if (tid == 0) keys_out[pi] = grid_mode ? key : kNone;
+            return;
+        }
         if (key != kNone) {
             decode(s, key, grid, G, plan);
         } else if (mode == DS_SOLVE) {
@@ -387,6 +406,9 @@ plan_sweep_kernel(const ds_problem* __restrict__ problems, int n,
             plan.threshold = t;
             plan.feasible = 0;
         }
+    } else if (keys_out) {
+        if (tid == 0) keys_out[pi] = kNone;
+        return;
     } else if (tid == 0) {
         if (mode == DS_SOLVE_SINGLE_LIGHT || mode == DS_SOLVE_SINGLE_HEAVY) {
             const bool light = mode == DS_SOLVE_SINGLE_LIGHT;
@@ -541,15 +563,64 @@ extern "C" ds_status ds_plan_batch_device(ds_ctx* ctx, const ds_problem* problem
     if (n <= 0) return DS_OK;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     plan_sweep_kernel<<<n, kThreads, 0, st>>>(problems, n, cascades, grid_values, grid_offsets,
-                                              out);
+                                              out, 0, 0, nullptr, nullptr);
     DS_LAUNCH_CHECK(ctx, "plan_sweep_kernel");
     return DS_OK;
 }
 
-extern "C" ds_status ds_plan_batch(ds_ctx* ctx, const ds_problem* problems, int32_t n,
-                                   const ds_cascade* cascades, int32_t n_cascades,
-                                   const double* grid_values, const int32_t* grid_offsets,
-                                   int32_t n_grids, ds_plan* out) {
+extern "C" ds_status ds_plan_keys_device(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                                         const ds_cascade* cascades, int32_t n_cascades,
+                                         const double* grid_values, const int32_t* grid_offsets,
+                                         int32_t n_grids, int32_t t_lo, int32_t t_hi,
+                                         uint64_t* keys, void* stream) {
+    (void)n_cascades;
+    (void)n_grids;
+    if (!ctx || (n > 0 && !keys)) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (t_lo < 0 || t_hi < t_lo) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "bad threshold range");
+    if (n <= 0) return DS_OK;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    plan_sweep_kernel<<<n, kThreads, 0, st>>>(problems, n, cascades, grid_values, grid_offsets,
+                                              nullptr, t_lo, t_hi,
+                                              reinterpret_cast<unsigned long long*>(keys), nullptr);
+    DS_LAUNCH_CHECK(ctx, "plan_sweep_kernel");
+    return DS_OK;
+}
+
+extern "C" ds_status ds_plan_from_keys_device(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                                              const ds_cascade* cascades, int32_t n_cascades,
+                                              const double* grid_values,
+                                              const int32_t* grid_offsets, int32_t n_grids,
+                                              const uint64_t* keys, ds_plan* out, void* stream) {
+    (void)n_cascades;
+    (void)n_grids;
+    if (!ctx || (n > 0 && (!keys || !out))) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (n <= 0) return DS_OK;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    plan_sweep_kernel<<<n, kThreads, 0, st>>>(problems, n, cascades, grid_values, grid_offsets,
+                                              out, 0, 0, nullptr,
+                                              reinterpret_cast<const unsigned long long*>(keys));
+    DS_LAUNCH_CHECK(ctx, "plan_sweep_kernel");
+    return DS_OK;
+}
+
+namespace {
+
+// Host-buffer entry points: validate (the reference's checks), stage the
+// inputs into the ctx scratch, run `launch` on the device copies, copy `out_bytes`
+// of results back from the scratch tail.
+struct Staged {
+    ds_problem* p;
+    ds_cascade* c;
+    double* g;
+    int32_t* o;
+    char* out;
+};
+
+template <class Launch>
+ds_status staged_call(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                      const ds_cascade* cascades, int32_t n_cascades, const double* grid_values,
+                      const int32_t* grid_offsets, int32_t n_grids, const void* in_extra,
+                      size_t in_bytes, void* out, size_t out_bytes, Launch launch) {
     if (!ctx) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null ctx");
     ds_status st = ds_plan_validate(problems, n, cascades, n_cascades, grid_values,
                                     grid_offsets, n_grids);
@@ -560,9 +631,10 @@ extern "C" ds_status ds_plan_batch(ds_ctx* ctx, const ds_problem* problems, int3
     const size_t bc = dsi::align_up(sizeof(ds_cascade) * n_cascades, 256);
     const size_t bg = dsi::align_up(sizeof(double) * (n_vals > 0 ? n_vals : 1), 256);
     const size_t bo = dsi::align_up(sizeof(int32_t) * (n_grids + 1), 256);
-    const size_t bout = dsi::align_up(sizeof(ds_plan) * n, 256);
+    const size_t bi = dsi::align_up(in_bytes > 0 ? in_bytes : 1, 256);
+    const size_t bout = dsi::align_up(out_bytes, 256);
     char* d = nullptr;
-    st = dsi::ensure_scratch(ctx, bp + bc + bg + bo + bout, reinterpret_cast<void**>(&d));
+    st = dsi::ensure_scratch(ctx, bp + bc + bg + bo + bi + bout, reinterpret_cast<void**>(&d));
     if (st != DS_OK) return st;
     DS_CUDA_TRY(cudaMemcpyAsync(d, problems, sizeof(ds_problem) * n, cudaMemcpyHostToDevice,
                                 ctx->stream));
@@ -573,15 +645,60 @@ extern "C" ds_status ds_plan_batch(ds_ctx* ctx, const ds_problem* problems, int3
                                     cudaMemcpyHostToDevice, ctx->stream));
     DS_CUDA_TRY(cudaMemcpyAsync(d + bp + bc + bg, grid_offsets, sizeof(int32_t) * (n_grids + 1),
                                 cudaMemcpyHostToDevice, ctx->stream));
-    ds_plan* dout = reinterpret_cast<ds_plan*>(d + bp + bc + bg + bo);
-    st = ds_plan_batch_device(ctx, reinterpret_cast<ds_problem*>(d), n,
-                              reinterpret_cast<ds_cascade*>(d + bp), n_cascades,
-                              reinterpret_cast<double*>(d + bp + bc),
-                              reinterpret_cast<int32_t*>(d + bp + bc + bg), n_grids, dout,
-                              ctx->stream);
+    char* din = d + bp + bc + bg + bo;
+    if (in_bytes > 0)
+        DS_CUDA_TRY(cudaMemcpyAsync(din, in_extra, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    Staged sp{reinterpret_cast<ds_problem*>(d), reinterpret_cast<ds_cascade*>(d + bp),
+              reinterpret_cast<double*>(d + bp + bc), reinterpret_cast<int32_t*>(d + bp + bc + bg),
+              din + bi};
+    st = launch(sp, din);
     if (st != DS_OK) return st;
-    DS_CUDA_TRY(cudaMemcpyAsync(out, dout, sizeof(ds_plan) * n, cudaMemcpyDeviceToHost,
-                                ctx->stream));
+    DS_CUDA_TRY(cudaMemcpyAsync(out, sp.out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return DS_OK;
+}
+
+} // namespace
+
+extern "C" ds_status ds_plan_batch(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                                   const ds_cascade* cascades, int32_t n_cascades,
+                                   const double* grid_values, const int32_t* grid_offsets,
+                                   int32_t n_grids, ds_plan* out) {
+    return staged_call(ctx, problems, n, cascades, n_cascades, grid_values, grid_offsets, n_grids,
+                       nullptr, 0, out, sizeof(ds_plan) * (n > 0 ? n : 0),
+                       [&](const Staged& sp, char*) {
+                           return ds_plan_batch_device(ctx, sp.p, n, sp.c, n_cascades, sp.g, sp.o,
+                                                       n_grids, reinterpret_cast<ds_plan*>(sp.out),
+                                                       ctx->stream);
+                       });
+}
+
+extern "C" ds_status ds_plan_keys(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                                  const ds_cascade* cascades, int32_t n_cascades,
+                                  const double* grid_values, const int32_t* grid_offsets,
+                                  int32_t n_grids, int32_t t_lo, int32_t t_hi, uint64_t* keys) {
+    if (t_lo < 0 || t_hi < t_lo) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "bad threshold range");
+    return staged_call(ctx, problems, n, cascades, n_cascades, grid_values, grid_offsets, n_grids,
+                       nullptr, 0, keys, sizeof(uint64_t) * (n > 0 ? n : 0),
+                       [&](const Staged& sp, char*) {
+                           return ds_plan_keys_device(ctx, sp.p, n, sp.c, n_cascades, sp.g, sp.o,
+                                                      n_grids, t_lo, t_hi,
+                                                      reinterpret_cast<uint64_t*>(sp.out),
+                                                      ctx->stream);
+                       });
+}
+
+extern "C" ds_status ds_plan_from_keys(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                                       const ds_cascade* cascades, int32_t n_cascades,
+                                       const double* grid_values, const int32_t* grid_offsets,
+                                       int32_t n_grids, const uint64_t* keys, ds_plan* out) {
+    return staged_call(ctx, problems, n, cascades, n_cascades, grid_values, grid_offsets, n_grids,
+                       keys, sizeof(uint64_t) * (n > 0 ? n : 0), out,
+                       sizeof(ds_plan) * (n > 0 ? n : 0),
+                       [&](const Staged& sp, char* din) {
+                           return ds_plan_from_keys_device(
+                               ctx, sp.p, n, sp.c, n_cascades, sp.g, sp.o, n_grids,
+                               reinterpret_cast<const uint64_t*>(din),
+                               reinterpret_cast<ds_plan*>(sp.out), ctx->stream);
+                       });
 }

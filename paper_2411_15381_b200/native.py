@@ -76,6 +76,12 @@ SIGNATURES = [
     ("ds_plan_batch", ctypes.c_int, [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, c_p]),
     ("ds_plan_batch_device", ctypes.c_int, [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, c_p, c_p]),
     ("ds_plan_validate", ctypes.c_int, [c_p, i32, c_p, i32, c_p, c_p, i32]),
+    ("ds_plan_keys", ctypes.c_int, [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, i32, i32, c_p]),
+    ("ds_plan_keys_device", ctypes.c_int,
+     [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, i32, i32, c_p, c_p]),
+    ("ds_plan_from_keys", ctypes.c_int, [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, c_p, c_p]),
+    ("ds_plan_from_keys_device", ctypes.c_int,
+     [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, c_p, c_p, c_p]),
     ("ds_score_latent", ctypes.c_int, [c_p, c_p, u64, i64, c_p, c_p]),
     ("ds_score_latent_device", ctypes.c_int, [c_p, c_p, u64, i64, c_p, c_p, c_p]),
     ("ds_route", ctypes.c_int, [c_p, c_p, i32, i64, c_p, i32, i64, c_p, c_p]),
@@ -168,6 +174,35 @@ class Context:
         check(lib().ds_plan_batch(self.handle, abi.ptr(problems), len(problems),
                                   abi.ptr(cascades), len(cascades), abi.ptr(grid_values),
                                   abi.ptr(grid_offsets), len(grid_offsets) - 1, abi.ptr(out)))
+        return out
+
+    def plan_keys(self, problems: np.ndarray, cascades: np.ndarray, grid_values: np.ndarray,
+                  grid_offsets: np.ndarray, t_lo: int, t_hi: int) -> np.ndarray:
+        """Packed selection keys of the search restricted to grid indices
+        [t_lo, t_hi) (uint64; 2**64-1 = none), see ds_plan_keys."""
+        problems = np.ascontiguousarray(problems, abi.PROBLEM)
+        cascades = np.ascontiguousarray(cascades, abi.CASCADE)
+        grid_values = np.ascontiguousarray(grid_values, np.float64)
+        grid_offsets = np.ascontiguousarray(grid_offsets, np.int32)
+        keys = np.zeros(len(problems), np.uint64)
+        check(lib().ds_plan_keys(self.handle, abi.ptr(problems), len(problems), abi.ptr(cascades),
+                                 len(cascades), abi.ptr(grid_values), abi.ptr(grid_offsets),
+                                 len(grid_offsets) - 1, t_lo, t_hi, abi.ptr(keys)))
+        return keys
+
+    def plan_from_keys(self, problems: np.ndarray, cascades: np.ndarray,
+                       grid_values: np.ndarray, grid_offsets: np.ndarray,
+                       keys: np.ndarray) -> np.ndarray:
+        problems = np.ascontiguousarray(problems, abi.PROBLEM)
+        cascades = np.ascontiguousarray(cascades, abi.CASCADE)
+        grid_values = np.ascontiguousarray(grid_values, np.float64)
+        grid_offsets = np.ascontiguousarray(grid_offsets, np.int32)
+        keys = np.ascontiguousarray(keys, np.uint64)
+        out = np.zeros(len(problems), abi.PLAN)
+        check(lib().ds_plan_from_keys(self.handle, abi.ptr(problems), len(problems),
+                                      abi.ptr(cascades), len(cascades), abi.ptr(grid_values),
+                                      abi.ptr(grid_offsets), len(grid_offsets) - 1,
+                                      abi.ptr(keys), abi.ptr(out)))
         return out
 
     # ---- latent scorer --------------------------------------------------

@@ -142,3 +142,73 @@ def test_curve_shards_combine_exactly_at_decay_one():
         lib.port().dso_curve_observe(abi.ptr(c), abi.ptr(s), len(s), 1.0)
         parts.append(c)
     assert np.array_equal(parts[0]["bin_mass"] + parts[1]["bin_mass"], whole["bin_mass"])
+
+
+def _decode_key(key, p, cas, gv, go):
+    """Packed selection key -> (x1, x2, b1, b2, threshold) (ds_plan_keys layout)."""
+    key = int(key)
+    c = cas[p["cascade"]]
+    G = int(go[p["grid"] + 1] - go[p["grid"]])
+    t_idx = G - 1 - (key >> 40)
+    x1 = key & 0xFFF
+    tot = (key >> 28) & 0xFFF
+    b1 = int(c["light"]["batch"][255 - ((key >> 20) & 0xFF)])
+    b2 = int(c["heavy"]["batch"][255 - ((key >> 12) & 0xFF)])
+    return x1, tot - x1, b1, b2, float(gv[go[p["grid"]] + t_idx])
+
+
+def _tplan_worker(rank, world, port, name, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz")))
+        pro, cas, gv, go = g["problems"], g["cascades"], g["grid_values"], g["grid_offsets"]
+        G = int(max(go[1:] - go[:-1]))
+
+        def keys_fn(t_lo, t_hi):
+            k = np.zeros(len(pro), np.uint64)
+            assert lib.port().dso_plan_keys(abi.ptr(pro), len(pro), abi.ptr(cas), abi.ptr(gv),
+                                            abi.ptr(go), t_lo, t_hi, abi.ptr(k)) == 0
+            return k
+        got = ddist.plan_t_sharded(keys_fn, lambda k: k, G)
+        if rank == 0:
+            q.put((got, keys_fn(0, G)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name", [(2, "config4"), (3, "wide_random"), (2, "alloc_random_2024")])
+def test_t_sharded_planner_argmin_equals_reference(world, name):
+    """Threshold-range sharding: per-rank keys of grid slices,
+    MIN all-reduce -> the full search's key, which decodes to the reference's
+    plan (golden sets written by the reference itself)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tplan_worker, args=(r, world, port, name, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got, full = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(got, full)
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz")))
+    pro, cas, gv, go = g["problems"], g["cascades"], g["grid_values"], g["grid_offsets"]
+    want = g["want_solve"] if "want_solve" in g else g["want"]
+    found = 0
+    for i in np.flatnonzero(got != ddist.KEY_NONE):
+        x1, x2, b1, b2, t = _decode_key(got[i], pro[i], cas, gv, go)
+        w = want[i]
+        assert (x1, x2, b1, b2, t) == (w["x1"], w["x2"], w["b1"], w["b2"], w["threshold"]), i
+        assert w["feasible"] == 1
+        found += 1
+    grid_mode = np.isin(pro["mode"], [abi.SOLVE, abi.SOLVE_FIXED_BATCHES])
+    assert np.array_equal(got != ddist.KEY_NONE, grid_mode & (want["feasible"] == 1))
+    assert found >= 5
+    # keys in int64 for the reduction keep the unsigned order
+    k = np.array([0, 5, 2**62, int(ddist.KEY_NONE)], np.uint64)
+    assert np.array_equal(ddist.keys_from_i64(ddist.keys_to_i64(k)), k)
+    assert list(np.argsort(ddist.keys_to_i64(k))) == [0, 1, 2, 3]

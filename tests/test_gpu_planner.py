@@ -240,3 +240,29 @@ def test_empty_and_large_batches(ctx, golden):
     big = np.tile(pro, 6)          # 18432 problems in one launch
     got = ctx.plan_batch(big, cas, gv, go)
     assert_plans_equal(got, np.tile(g["want_solve"], 6), "tiled")
+
+
+@pytest.mark.parametrize("name,key,shards", [("config4", "want_solve", 4),
+                                             ("wide_random", "want", 3),
+                                             ("alloc_random_2024", "want_solve", 2),
+                                             ("accept_c1", "want_solve", 8)])
+def test_t_sharded_keys_min_then_decode_equals_reference(ctx, golden, name, key, shards):
+    """ds_plan_keys over disjoint threshold slices (one per GPU in the sharded
+    planner), element-wise MIN (the all-reduce), ds_plan_from_keys -> exactly
+    the reference's plans; every slice's keys equal the C restatement's."""
+    from paper_2411_15381_b200 import dist as ddist
+    g = golden(name)
+    pro, cas, gv, go = planner_set(g)
+    G = int(max(go[1:] - go[:-1]))
+    port = lib.port()
+    red = np.full(len(pro), ddist.KEY_NONE, np.uint64)
+    for r in range(shards):
+        lo, hi = ddist.shard_range(G, shards, r)
+        k = ctx.plan_keys(pro, cas, gv, go, lo, hi)
+        want_k = np.zeros(len(pro), np.uint64)
+        port.dso_plan_keys(abi.ptr(pro), len(pro), abi.ptr(cas), abi.ptr(gv), abi.ptr(go),
+                           lo, hi, abi.ptr(want_k))
+        assert np.array_equal(k, want_k), (name, r)
+        red = np.minimum(red, k)
+    assert np.array_equal(red, ctx.plan_keys(pro, cas, gv, go, 0, G))
+    assert_plans_equal(ctx.plan_from_keys(pro, cas, gv, go, red), g[key], name)
