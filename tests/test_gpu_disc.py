@@ -126,3 +126,12 @@ def test_disc_single_tile_images(disc, weights):
     """128 tokens per image (128x256): one token tile per image."""
     imgs = disc_oracle.synth_images(9, 3, 5, 128, 256)
     check_conf(disc.score(imgs), disc_oracle.disc_forward(imgs, weights))
+
+
+def test_disc_matches_torch_fp32_reference(disc, weights):
+    """The kernel vs a plain PyTorch fp32 reference of the same network
+    (tests/torch_ref.py, independent of the numpy oracle), 512^2 and 1024^2."""
+    from tests.torch_ref import disc_forward_torch
+    for seed, n, hw in ((21, 5, 512), (22, 2, 1024)):
+        imgs = disc_oracle.synth_images(seed, 0, n, hw, hw)
+        check_conf(disc.score(imgs), disc_forward_torch(imgs, weights))

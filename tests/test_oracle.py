@@ -344,3 +344,15 @@ def test_port_csv_vs_reference_fresh(tmp_path):
         out = np.zeros(n, np.uint8)
         fn(P(rows), len(rows), P(out), n)
         assert out.tobytes() == (tmp_path / f"{name}.csv").read_bytes(), name
+
+
+def test_disc_numpy_oracle_agrees_with_torch_reference():
+    """Two independent CPU restatements of the discriminator (numpy oracle,
+    PyTorch fp32) agree within the north_star tolerance on the host weights."""
+    from oracle import disc_oracle
+    from tests.torch_ref import disc_forward_torch
+    w = disc_oracle.gen_weights(2024, calibrate=True)
+    imgs = disc_oracle.synth_images(5, 0, 3, 256, 512)
+    a = disc_oracle.disc_forward(imgs, w).astype(np.float64)
+    b = disc_forward_torch(imgs, w)
+    assert np.all(np.abs(a - b) <= 1e-3 * np.maximum(np.abs(a), 1e-2)), np.abs(a - b).max()
