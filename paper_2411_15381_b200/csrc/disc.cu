@@ -81,6 +81,14 @@ constexpr int kThreads = 480;
 constexpr float kConst = 16.0f;         // value of the constant features
 constexpr int kAStages = 2, kBStages = 4;
 constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (idle during GEMM1)
+#ifndef DS_AW
+#define DS_AW 1
+#endif
+#ifndef DS_E3_FIRST
+#define DS_E3_FIRST 0
+#endif
+constexpr int kAWStages = DS_AW ? 2 : 0; // W2_0 stages 0-1 land in the A ring (idle from GEMM1's
+                                        // end until GEMM2_0 has read them)
 #ifndef DS_E1_SPLIT
 #define DS_E1_SPLIT 192
 #endif
@@ -181,7 +189,7 @@ __device__ __forceinline__ void e1_columns(uint32_t tmem_lane, int c_lo, uint32_
 struct Bars {
     uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
-    uint64_t x_full[kXStages], r1_free, e1b_done;
+    uint64_t x_full[kXStages], r1_free, e1b_done, aw_full[2], aw_free;
     uint32_t tmem_base;
     float warp_part[2][8];
 };
@@ -230,6 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         for (int s = 0; s < kXStages; ++s) mbar_init(&B.x_full[s], 1);
         mbar_init(&B.r1_free, 1);
         mbar_init(&B.e1b_done, 128 + peer);
+        for (int s = 0; s < 2; ++s) mbar_init(&B.aw_full[s], 1);
+        mbar_init(&B.aw_free, 1);
         fence_mbar_init();
     }
     if (warp == 13) tmem_alloc2<512>(&B.tmem_base);
@@ -319,13 +329,14 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         for (long long tile = 0; tile < my_tiles; ++tile) {
             if (tl == 0) {
                 DS_TRACE(0, tile, 0);
-#if !defined(DS_NO_PF) && !defined(DS_PF_LATE)
                 if (tile + 2 < my_tiles) prefetch_tile(tile + 2);
-#endif
             }
 #pragma unroll
             for (int c = 0; c < kChunksPerTile; ++c) {
                 mbar_wait(&B.a_empty[astage], aphase ^ 1);
+                // the A slots carried GEMM2_0's first weight stages after GEMM1
+                if (kAWStages && c == 0 && tile > 0)
+                    mbar_wait(&B.aw_free, static_cast<uint32_t>((tile - 1) & 1));
                 if (tl == 0) DS_TRACE(3, tile, c);
                 const uint32_t st = sbase + kARing + astage * kAChunk;
 #pragma unroll
@@ -351,9 +362,6 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 tc_fence_before();
             }
             group_signal(&B.e1b_done, 2, 128, tl == 0);
-#ifdef DS_PF_LATE
-            if (tl == 0 && tile + 3 < my_tiles) prefetch_tile(tile + 3);
-#endif
             if (tile + 1 < my_tiles) {
                 pbase = token_base(tile + 1);
                 load_chunk(pbase, 0, buf[0]);
@@ -432,8 +440,10 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             group_signal(&B.drained, 3, 256, first);
             DS_TRACE(1, tile, 1);
 
+#if DS_E3_FIRST
             // ---- E3 of the previous tile (its G3_3 was issued after G1(tile)) ----
             if (tile > 0) e3(tile - 1);
+#endif
 
             // ---- E2_j: acc[0,256) -> ReLU -> bf16 (registers) -> H2 (R2) --------
             for (int j = 0; j < 4; ++j) {
@@ -471,6 +481,11 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 fence_proxy_async_smem();
                 group_signal(&B.h2_ready, 3, 256, first);
                 DS_TRACE(1, tile, 3 + 2 * j);
+#if !DS_E3_FIRST
+                // ---- E3 of the previous tile: after E2_0, so GEMM2_1 is not held
+                // behind it; it must finish before GEMM3_0 (after GEMM2_1)
+                if (j == 0 && tile > 0) e3(tile - 1);
+#endif
             }
         }
         if (my_tiles > 0) e3(my_tiles - 1);
@@ -500,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 ptile = tile;
                 put(W1 + kXStages, kW1Stages - kXStages);
                 if (tile > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
-                put(W2, kWChunkStages);
+                put(W2 + kAWStages, kWChunkStages - kAWStages);
                 for (int j = 1; j < 4; ++j) {
                     put(W2 + j * kWChunkStages, kWChunkStages);
                     put(W3 + (j - 1) * kWChunkStages, kWChunkStages);
@@ -519,6 +534,18 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     tma_2d_pair(sbase + kR1 + k * kBHalf, &P.wmap, 0,
                                 k * 256 + static_cast<int>(rank) * 128,
                                 mapa_shared(smem_u32(&B.x_full[k]), 0), policy);
+                }
+                if (kAWStages) {
+                    // GEMM1 of this tile complete (acc12_full phase 5*tile; the
+                    // barrier cannot be past it: GEMM2_0 needs these stages):
+                    // the A slots are free until aw_free
+                    mbar_wait(&B.acc12_full, static_cast<uint32_t>(tile & 1));
+                    for (int k = 0; k < kAWStages; ++k) {
+                        if (leader) mbar_arrive_expect_tx(&B.aw_full[k], kBStage);
+                        tma_2d_pair(sbase + kARing + k * kAChunk, &P.wmap, 0,
+                                    (kW1Stages + k) * 256 + static_cast<int>(rank) * 128,
+                                    mapa_shared(smem_u32(&B.aw_full[k]), 0), policy);
+                    }
                 }
             }
         }
@@ -600,7 +627,24 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 mbar_wait(&B.e1b_done, static_cast<uint32_t>(tile & 1));   // the builders' E1 columns
                 tc_fence_after();
                 DS_TRACE(2, tile, 3);
-                gemm(sbase + kR1, 4, acc12, false);  // G2_0
+                // G2_0: its first kAWStages weight stages sit in the A slots
+                for (int kc = 0; kc < 4; ++kc) {
+                    const uint64_t ad = desc_k_sw128(sbase + kR1 + kc * kAChunk);
+                    uint64_t bd;
+                    if (kc < kAWStages) {
+                        mbar_wait(&B.aw_full[kc], static_cast<uint32_t>(tile & 1));
+                        tc_fence_after();
+                        bd = desc_k_sw128(sbase + kARing + kc * kAChunk);
+                    } else {
+                        bd = next_b();
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        umma_bf16_pair(acc12, ad + 2 * k, bd + 2 * k, kIdescF16,
+                                       (kc > 0 || k > 0) ? 1u : 0u);
+                    if (kc >= kAWStages) release_b();
+                }
+                if (kAWStages) umma_commit_pair(&B.aw_free, 0x3);
                 umma_commit_pair(&B.acc12_full, 0x3);
                 for (int j = 1; j < 4; ++j) {
                     wait_bar(&B.drained, pdr);       // E2_{j-1} has the values in registers
