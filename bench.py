@@ -187,7 +187,7 @@ def cpu_images_leg(n_img: int):
                              abi.ptr(curve), abi.ptr(idx), abi.ptr(cnt))
         kind = "port"
     dt = time.perf_counter() - t0
-    return n_img / dt, kind
+    return n_img / dt, kind, conf
 
 
 def cpu_planner_leg(problems, cascades, grid, offs, threads):
@@ -341,7 +341,7 @@ def run_reference(args):
     vals = []
     kind = None
     for i in range(args.warmup + args.steps):
-        v, kind = cpu_images_leg(max(4, CPU_DISC_SAMPLE // 4))
+        v, kind, _ = cpu_images_leg(max(4, CPU_DISC_SAMPLE // 4))
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -863,12 +863,19 @@ def run_gpu(args):
         }
         if ws == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
-            cv, ck = cpu_images_leg(CPU_DISC_SAMPLE)
+            cv, ck, cpu_conf = cpu_images_leg(CPU_DISC_SAMPLE)
             line["cpu_baseline"] = {"value": cv, "unit": "images/s", "cores": threads,
                                     "kind": "port" if ck != "reference" else ck,
                                     "sample": f"{CPU_DISC_SAMPLE} images 512x512: numpy port of "
                                               "the discriminator (no reference network) + the "
                                               "reference route loop at 101 thresholds"}
+            # image confidences of the same images (ids 0..95 of the pool) vs the
+            # CPU restatement, north_star's 1e-3 relative floored at 1e-2
+            g = c_host[:len(cpu_conf)]
+            rel = np.abs(g - cpu_conf) / np.maximum(np.abs(cpu_conf), 1e-2)
+            line["parity"]["disc_vs_cpu_port"] = {"images": int(len(cpu_conf)),
+                                                  "max_rel_err": float(rel.max()),
+                                                  "within_1e-3": bool(rel.max() <= 1e-3)}
             sub = slice(0, CPU_PLAN_SAMPLE)
             pv, pk, cpu_plans = cpu_planner_leg(np.ascontiguousarray(pro[sub]), cas, grid, offs,
                                                 threads)
