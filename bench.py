@@ -63,6 +63,8 @@ WL_RATES = [2500.0] * 400     # 400 s at 2,500 qps: 1,000,811 arrivals at seed 3
 WL_SEED = 3
 N_CSV = 1_000_000
 N_SCALE = 1_000_000           # config 5: queries over the whole world
+WORKLOAD = ("cascade2: 5K synthetic 512x512 images/GPU, discriminator score + route at 101 "
+            "thresholds + curve replay")
 CPU_CSV_SAMPLE = 200_000      # records through the reference's write_csv
 
 
@@ -350,8 +352,9 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * max(4, CPU_DISC_SAMPLE // 4) / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": "cascade2 5K 512x512 score+route (101 thresholds)",
-                                        "global_batch": N_IMG, "sample_images": max(4, CPU_DISC_SAMPLE // 4)},
+        "data": "synthetic", "config": {"workload": WORKLOAD, "global_batch": N_IMG,
+                                        "image_hw": [H, W], "thresholds": 101,
+                                        "sample_images": max(4, CPU_DISC_SAMPLE // 4)},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": kind,
                          "sample": f"{max(4, CPU_DISC_SAMPLE // 4)} images 512x512 per step"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0,
@@ -802,8 +805,7 @@ def run_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u8xs8->s32 (layer 1), bf16 x bf16 -> f32 (layers 2-3)",
             "data": "synthetic (device-generated 512x512 u8 images; seeded PatchDisc weights)",
-            "config": {"workload": "cascade2: 5K synthetic 512x512 images/GPU, discriminator "
-                                   "score + route at 101 thresholds + curve replay",
+            "config": {"workload": WORKLOAD,
                        "global_batch": ws * N_IMG, "image_hw": [H, W],
                        "thresholds": NT, "parallelism": f"dp{ws} (query shards)",
                        "l2": "inputs 3.9 GB/GPU > 126 MB L2, no flush"},
