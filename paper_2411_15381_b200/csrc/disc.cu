@@ -114,7 +114,7 @@ struct DiscParams {
     float hw[kD3];
     float s1;           // layer-1 scale: h1_pre = s1 * acc + b1
     const uint8_t* images;
-    float* part;        // per (image, CTA rank): sum over tokens of the head scores
+    float* part;        // per 128-token tile: sum over its tokens of the head scores
     long long n_img;
     int h, w, px, tokens, tiles_per_img;
     long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr = off)
@@ -261,19 +261,22 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         }
     };
 
-    // Flat 128-token tiles of this pair's images (images unit, unit + nunits, ...);
-    // CTA `rank` takes flat tiles 2k + rank. A pair tile whose second half runs
-    // past the end recomputes the last tile and writes nothing (a "ghost").
+    // Flat 128-token tiles f = image * tiles_per_img + tile-in-image; pair tile
+    // k covers f = 2k (leader) and 2k + 1 (peer), and the pairs take pair
+    // tiles round robin (k = unit, unit + nunits, ...), so a small batch still
+    // spreads over every SM pair. A pair tile whose second half runs past the
+    // end recomputes the last tile and writes nothing (a "ghost").
     const long long n_img = P.n_img;
     const int tpi = P.tiles_per_img;
-    const long long my_imgs = unit < n_img ? (n_img - 1 - unit) / nunits + 1 : 0;
-    const long long my_flat = my_imgs * tpi;
-    const long long my_tiles = (my_flat + 1) / 2;          // pair tiles
+    const long long n_flat = n_img * tpi;
+    const long long n_pair_tiles = (n_flat + 1) / 2;
+    const long long my_tiles = unit < n_pair_tiles ? (n_pair_tiles - 1 - unit) / nunits + 1 : 0;
     const long long img_bytes = static_cast<long long>(P.h) * P.w * 3;
     const long long row_bytes = static_cast<long long>(P.w) * 3;
+    auto flat_raw = [&](long long tile) { return 2 * (unit + tile * nunits) + rank; };
     auto flat_of = [&](long long tile) {                   // this CTA's flat tile
-        const long long f = 2 * tile + rank;
-        return f < my_flat ? f : my_flat - 1;
+        const long long f = flat_raw(tile);
+        return f < n_flat ? f : n_flat - 1;
     };
 
     if (warp < 4) {
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         const int tl = threadIdx.x;
         auto token_base = [&](long long tile) -> const uint8_t* {
             const long long f = flat_of(tile);
-            const long long img = unit + (f / tpi) * nunits;
+            const long long img = f / tpi;
             const int tok = static_cast<int>(f % tpi) * kM + tl;
             const int py = tok / P.px, px = tok - py * P.px;
             return P.images + img * img_bytes + (static_cast<long long>(py) * 16) * row_bytes +
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         // rows (or a small superset); bulk-prefetch it into L2.
         auto prefetch_tile = [&](long long tile) {
             const long long f = flat_of(tile);
-            const long long img = unit + (f / tpi) * nunits;
+            const long long img = f / tpi;
             const int tok0 = static_cast<int>(f % tpi) * kM;
             const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
             const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
@@ -378,7 +381,6 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         const bool first = ew == 0 && lane == 0;
         const uint64_t s1x2 = f2_pack(P.s1, P.s1);
         uint32_t p12 = 0, p3 = 0, pfree = 0;
-        float img_acc = 0.0f;
 
         // E3: ReLU(acc3) . w_head over this thread's 128 columns -> per-image sum
         auto e3 = [&](long long tile) {
@@ -413,16 +415,8 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 float s = 0.0f;
 #pragma unroll
                 for (int w = 0; w < 8; ++w) s += B.warp_part[b][w];
-                const long long f = 2 * tile + rank;
-                if (f < my_flat) {                 // ghost tiles write nothing
-                    img_acc += s;
-                    // flush at this CTA's last tile of the image
-                    if (f + 2 >= my_flat || (f + 2) / tpi != f / tpi) {
-                        const long long img = unit + (f / tpi) * nunits;
-                        P.part[img * 2 + rank] = img_acc;
-                        img_acc = 0.0f;
-                    }
-                }
+                const long long f = flat_raw(tile);
+                if (f < n_flat) P.part[f] = s;      // ghost tiles write nothing
             }
         };
 
@@ -684,12 +678,14 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     }
 }
 
-// logit = (sum of the pair's per-image head sums) / tokens + b_head
-__global__ void finalize_kernel(const float* __restrict__ part, long long n, int tokens, float hb,
-                                int logits, float* __restrict__ out) {
+// logit = (sum of the image's per-tile head sums, in tile order) / tokens + b_head
+__global__ void finalize_kernel(const float* __restrict__ part, long long n, int tpi, int tokens,
+                                float hb, int logits, float* __restrict__ out) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float logit = (part[2 * i] + part[2 * i + 1]) / static_cast<float>(tokens) + hb;
+    float s = 0.0f;
+    for (int t = 0; t < tpi; ++t) s += part[i * tpi + t];
+    const float logit = s / static_cast<float>(tokens) + hb;
     out[i] = logits ? logit : 1.0f / (1.0f + expf(-logit));
 }
 
@@ -851,13 +847,14 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     p.tokens = tokens;
     p.tiles_per_img = tokens / kM;
     p.trace = trace;
-    float* part = nullptr;
-    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * 2 * n, st));
-    DS_CUDA_TRY(cudaMemsetAsync(part, 0, sizeof(float) * 2 * n, st));
+    const long long n_flat = static_cast<long long>(n) * p.tiles_per_img;
+    float* part = nullptr;   // one head sum per 128-token tile, every entry written
+    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * n_flat, st));
     p.part = part;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->ctx->device);
-    const int pairs = static_cast<int>(n < sms / 2 ? n : sms / 2);
+    const long long pair_tiles = (n_flat + 1) / 2;
+    const int pairs = static_cast<int>(pair_tiles < sms / 2 ? pair_tiles : sms / 2);
     // per device (one ds_ctx per GPU in a process): cheap, so set every launch
     DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kSmemBytes));
@@ -875,8 +872,8 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     cfg.numAttrs = 1;
     DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, disc_kernel, p));
     DS_LAUNCH_CHECK(d->ctx, "disc_kernel");
-    finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(part, n, tokens, d->hb,
-                                                                           logits, out);
+    finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+        part, n, p.tiles_per_img, tokens, d->hb, logits, out);
     DS_LAUNCH_CHECK(d->ctx, "finalize_kernel");
     cudaFreeAsync(part, st);
     return DS_OK;
