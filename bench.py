@@ -555,29 +555,52 @@ def run_gpu(args):
     count1 = torch.empty(1, dtype=torch.int64, device=dev)
     curve1 = torch.empty_like(prior_t)
 
-    def batch32_step():
+    def batch32_step(sp=None):
+        sp = native.c_p(ctx.stream) if sp is None else sp
+        curve1.copy_(prior_t)
+        for off in range(0, N_IMG, B1):
+            m = min(B1, N_IMG - off)
+            cp = native.c_p(conf1.data_ptr() + 4 * off)
+            native.check(L.ds_disc_score_device(
+                disc.handle, native.c_p(images.data_ptr() + off * H * W * 3), m, H, W, cp, sp))
+            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve1.data_ptr()),
+                                                   cp, abi.CONF_F32, m, DECAY, sp))
+            native.check(L.ds_route_device(ctx.handle, cp, abi.CONF_F32, m,
+                                           native.c_p(thr5.data_ptr()), 1, id0 + off,
+                                           native.c_p(heavy1.data_ptr()),
+                                           native.c_p(count1.data_ptr()), sp))
+
+    def batch32_eager():
         with torch.cuda.stream(stream):
-            curve1.copy_(prior_t)
-            for off in range(0, N_IMG, B1):
-                m = min(B1, N_IMG - off)
-                cp = native.c_p(conf1.data_ptr() + 4 * off)
-                native.check(L.ds_disc_score_device(
-                    disc.handle, native.c_p(images.data_ptr() + off * H * W * 3), m, H, W, cp,
-                    native.c_p(ctx.stream)))
-                native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve1.data_ptr()),
-                                                       cp, abi.CONF_F32, m, DECAY,
-                                                       native.c_p(ctx.stream)))
-                native.check(L.ds_route_device(ctx.handle, cp, abi.CONF_F32, m,
-                                               native.c_p(thr5.data_ptr()), 1, id0 + off,
-                                               native.c_p(heavy1.data_ptr()),
-                                               native.c_p(count1.data_ptr()),
-                                               native.c_p(ctx.stream)))
-    batch32_step()
+            batch32_step()
+    batch32_eager()
     torch.cuda.synchronize()
-    b32_ms = allmax([timed(batch32_step, 2)])[0]
+    b32_ms = allmax([timed(batch32_eager, 2)])[0]
     b32_value = ws * N_IMG / (b32_ms / 1000.0)
     b32_batch_us = b32_ms * 1000.0 / ((N_IMG + B1 - 1) // B1)
     b32_parity = bool(torch.equal(conf1, conf))
+    # the same 157 batches captured once into a CUDA graph (launch overhead off
+    # the per-batch path, as a streaming server would run a fixed batch plan)
+    g_stream = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(g_stream):
+        batch32_step(native.c_p(g_stream.cuda_stream))   # warm-up on the capture stream
+    torch.cuda.synchronize()
+    with torch.cuda.graph(graph, stream=g_stream):
+        batch32_step(native.c_p(g_stream.cuda_stream))
+    conf1.fill_(-1.0)           # the replay must recompute every confidence
+    ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(g_stream):
+        graph.replay()
+        g_stream.synchronize()
+        b32g_parity = bool(torch.equal(conf1, conf))
+        ga.record(g_stream)
+        for _ in range(2):
+            graph.replay()
+        gb.record(g_stream)
+    torch.cuda.synchronize()
+    b32g_ms = allmax([ga.elapsed_time(gb) / 2])[0]
+    del graph
     del conf1
 
     # config 3 (cascade 3): 5K synthetic 1024x1024 images (15.7 GB) per GPU,
@@ -832,6 +855,11 @@ def run_gpu(args):
             "cascade1_batch32": {"value": b32_value, "unit": "images/s",
                                  "us_per_batch": b32_batch_us, "batch": B1,
                                  "parity_vs_full_batch": b32_parity,
+                                 "cuda_graph": {"value": ws * N_IMG / (b32g_ms / 1000.0),
+                                                "unit": "images/s",
+                                                "us_per_batch": b32g_ms * 1000.0 / (
+                                                    (N_IMG + B1 - 1) // B1),
+                                                "parity_vs_full_batch": b32g_parity},
                                  "config": "config 1: 5K 512x512 in light batches of 32: score, "
                                            "observe into the curve, route at t=0.5"},
             "cascade3": {"value": c3_value, "unit": "images/s", "image_hw": [H3, H3],

@@ -824,6 +824,7 @@ struct ds_disc {
     float* d_b1 = nullptr;
     DiscParams params{};       // b1 + head + s1 (device-independent part)
     float hb = 0.0f;           // head bias
+    int sms = 0;               // SM count of ctx->device (set once, with the smem attribute)
 };
 
 namespace {
@@ -851,13 +852,13 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     float* part = nullptr;   // one head sum per 128-token tile, every entry written
     DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * n_flat, st));
     p.part = part;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->ctx->device);
+    if (d->sms == 0) {   // once per ds_disc (one device); kept off the per-launch path
+        DS_CUDA_TRY(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->ctx->device));
+        DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSmemBytes));
+    }
     const long long pair_tiles = (n_flat + 1) / 2;
-    const int pairs = static_cast<int>(pair_tiles < sms / 2 ? pair_tiles : sms / 2);
-    // per device (one ds_ctx per GPU in a process): cheap, so set every launch
-    DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSmemBytes));
+    const int pairs = static_cast<int>(pair_tiles < d->sms / 2 ? pair_tiles : d->sms / 2);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
     cfg.blockDim = dim3(kThreads);
