@@ -79,7 +79,10 @@ constexpr int kAChunk = 16384;          // 128 token rows x 128 bytes of K, SW12
 constexpr int kChunksPerTile = 6;       // K = 768 = 6 x 128 (u8)
 constexpr int kThreads = 480;
 constexpr float kConst = 16.0f;         // value of the constant features
-constexpr int kAStages = 2, kBStages = 4;
+#ifndef DS_A_STAGES
+#define DS_A_STAGES 2
+#endif
+constexpr int kAStages = DS_A_STAGES, kBStages = 6 - DS_A_STAGES;   // 6 x 16 KB of rings
 constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (idle during GEMM1)
 #ifndef DS_AW
 #define DS_AW 1
