@@ -232,7 +232,7 @@ def cpu_latent_leg(n, threads):
         lib.port().dso_route_loop(abi.ptr(conf), n, 0.5, 1, DECAY, abi.ptr(curve), abi.ptr(idx),
                                   abi.ptr(cnt))
         kind = "port"
-    return n / (time.perf_counter() - t0), kind
+    return n / (time.perf_counter() - t0), kind, conf, idx[:int(cnt[0])]
 
 
 def cpu_workload_leg(threads):
@@ -478,6 +478,13 @@ def run_gpu(args):
     cnt_host = counts.cpu().numpy()
     want_cnt = np.array([(c_host < t).sum() for t in workloads.make_grid(0.01)])
     parity_ok = bool(np.array_equal(cnt_host, want_cnt))
+    # K2 lists at t = 0.5 (grid index 50): the ordered ids of c < t, exactly
+    heavy50 = heavy[50 * N_IMG: 50 * N_IMG + int(cnt_host[50])].cpu().numpy()
+    lists_ok = bool(np.array_equal(heavy50, np.flatnonzero(c_host < 0.5) + id0))
+    # K3 curve after the step vs the C restatement on the same confidences, bit for bit
+    cw = prior.copy()
+    _olib.port().dso_curve_observe(abi.ptr(cw), abi.ptr(c_host), len(c_host), DECAY)
+    curve_ok = curve_t.cpu().numpy().tobytes() == cw.tobytes()
 
     # ---- e2e: the C-ABI calls with HOST buffers, copies inside the timed region
     pinned = torch.empty(N_IMG * H * W * 3, dtype=torch.uint8, pin_memory=True)
@@ -745,6 +752,8 @@ def run_gpu(args):
     latent_step(ev=True)
     torch.cuda.synchronize()
     lat_ms = [levs[i].elapsed_time(levs[i + 1]) for i in range(3)]
+    lconf_host = lconf.cpu().numpy()
+    lheavy_host = lheavy[:int(lcount.item())].cpu().numpy()
     latent_value = ws * N_LATENT / (allmax([sum(lat_ms)])[0] / 1000.0)
 
     # ---- workload leg: arrivals (K8) + Query records (K4) --------------------
@@ -847,7 +856,9 @@ def run_gpu(args):
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clocks,
-            "parity": {"route_counts_vs_confidences": parity_ok},
+            "parity": {"route_counts_vs_confidences": parity_ok,
+                       "route_ids_at_0.5_vs_cpu": lists_ok,
+                       "curve_bits_vs_cpu": bool(curve_ok)},
             "scaleout": {"value": scale_value, "unit": "images/s", "queries": N_SCALE,
                          "queries_per_gpu": n5, "ms": scale_ms, "routed_at_0.5_rank0": scale_routed,
                          "config": "config 5: 1M 512x512 queries, contiguous id shards, 5K "
@@ -915,11 +926,20 @@ def run_gpu(args):
                           f"{threads} threads"}
             line["planner"]["parity_vs_cpu"] = bool(
                 gpu_plans[sub].tobytes() == cpu_plans.tobytes())
-            lv, lk = cpu_latent_leg(CPU_LATENT_SAMPLE, threads)
+            lv, lk, lconf_cpu, lidx_cpu = cpu_latent_leg(CPU_LATENT_SAMPLE, threads)
             line["latent"]["cpu_baseline"] = {
                 "value": lv, "unit": "queries/s", "cores": threads, "kind": lk,
                 "sample": f"{CPU_LATENT_SAMPLE} queries: sample_query on {threads} threads + "
                           "sequential observe/defers loop"}
+            # the same ids on the GPU: confidences (rel <= 1e-12) and the
+            # ordered heavy ids at t = 0.5 (the GPU list's prefix below the sample size)
+            g = lconf_host[:CPU_LATENT_SAMPLE]
+            rel = np.abs(g - lconf_cpu) / np.maximum(np.abs(lconf_cpu), 1e-2)
+            gl = lheavy_host[lheavy_host < CPU_LATENT_SAMPLE]
+            line["latent"]["parity_vs_cpu"] = {
+                "queries": CPU_LATENT_SAMPLE, "max_rel_err": float(rel.max()),
+                "within_1e-12": bool(rel.max() <= 1e-12),
+                "heavy_ids_equal": bool(np.array_equal(gl, lidx_cpu))}
             wv, wav, wk, wa = cpu_workload_leg(threads)
             line["workload"]["cpu_baseline"] = {
                 "value": wv, "unit": "queries/s", "arrivals_per_s": wav, "cores": threads,
