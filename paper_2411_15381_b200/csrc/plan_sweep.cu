@@ -10,12 +10,12 @@
 //      order, so f(t) is bit-identical);
 //   2. thresholds walked from the top in chunks of kTChunk: x2[t][b2] for the
 //      chunk, then each thread takes (b1, b2) pairs and decides that pair's
-//      (t, b1, b2) candidates from the top t down, scoring each as a packed
-//      u64 key whose unsigned order is the reference's selection order ("first
-//      feasible t from the top", then Candidate::better_than,
-//      allocator.cpp:57-67):
+//      (t, b1, b2) candidates, scoring each as a packed u64 key whose unsigned
+//      order is the reference's selection order ("first feasible t from the
+//      top", then Candidate::better_than, allocator.cpp:57-67):
 //          (G-1-t_idx)<<40 | (x1+x2)<<28 | (255-b1_idx)<<20 | (255-b2_idx)<<12 | x1
-//      (a pair's first valid t is its minimum key, so its walk stops there);
+//      (a pair's first valid t is its minimum key; x2 is monotone in t, so the
+//      pair's valid t form a prefix of the chunk and a binary search finds it);
 //   3. warp-shuffle min, then a block min over 8 warps; the first chunk with a
 //      finite key holds the global minimum, so the walk stops there (the
 //      reference's early exit, allocator.cpp:118).
@@ -142,22 +142,29 @@ __device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int
         // first valid t is the pair's best (larger t = smaller key), so the
         // walk stops there. Every (t, b1, b2) candidate of the chunk is still
         // decided (reference semantics); only provably worse keys are skipped.
+        // x2[t][j] is non-decreasing in t (the deferral fraction is, and
+        // min_servers is monotone in the demand), so a pair's valid thresholds
+        // in the chunk are a prefix [0, k] of it and its first valid t from the
+        // top is k: found by binary search instead of walking down from the top.
         unsigned long long mine = kNone;
         for (int pr = threadIdx.x; pr < ni * nj; pr += kThreads) {
             const int i = i0 + pr / nj, j = j0 + pr % nj;
             if (!((s.lat[i] >> j) & 1ull)) continue;
             const int x1 = s.x1[i];
             if (x1 > S) continue;
-            const unsigned long long tie_lo = tie_key(x1, 0, i, j);   // x2 added below
-            for (int tl = cnt - 1; tl >= 0; --tl) {
-                const int x2 = s.x2[tl * kMaxB + j];
-                if (x1 + x2 > S) continue;
-                const unsigned long long key =
-                    (static_cast<unsigned long long>(G - 1 - (lo + tl)) << 40) +
-                    (static_cast<unsigned long long>(x2) << 28) + tie_lo;
-                mine = key < mine ? key : mine;
-                break;
+            const int cap = S - x1;
+            const int* col = s.x2 + j;
+            if (col[0] > cap) continue;            // even the chunk's lowest t is invalid
+            int a = 0, b = cnt - 1;                // col[a * kMaxB] <= cap
+            while (a < b) {
+                const int mid = (a + b + 1) >> 1;
+                if (col[mid * kMaxB] <= cap) a = mid;
+                else b = mid - 1;
             }
+            const unsigned long long key =
+                (static_cast<unsigned long long>(G - 1 - (lo + a)) << 40) +
+                (static_cast<unsigned long long>(col[a * kMaxB]) << 28) + tie_key(x1, 0, i, j);
+            mine = key < mine ? key : mine;
         }
         best = block_min(mine, parity ? s.red2 : s.red);
         parity ^= 1;
