@@ -87,6 +87,16 @@ ds_status ds_ctx_create(int device, ds_ctx** out) {
                                            "device is sm_" + std::to_string(prop.major) +
                                                std::to_string(prop.minor));
     DS_CUDA_TRY(cudaSetDevice(device));
+    // The per-launch stream-ordered temporaries (cudaMallocAsync) come from the
+    // device's default pool; keep freed blocks cached in it instead of returning
+    // them to the driver at every synchronization (a re-map costs tens of us).
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = 1ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     ds_ctx* ctx = new ds_ctx();
     ctx->device = device;
     e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);

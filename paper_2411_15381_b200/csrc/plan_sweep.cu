@@ -258,7 +258,8 @@ plan_sweep_kernel(const ds_problem* __restrict__ problems, int n,
                   const double* __restrict__ grid_values,
                   const int32_t* __restrict__ grid_offsets, ds_plan* __restrict__ out,
                   int t_lo, int t_hi, unsigned long long* __restrict__ keys_out,
-                  const unsigned long long* __restrict__ keys_in) {
+                  const unsigned long long* __restrict__ keys_in,
+                  const double* __restrict__ prefix_tab) {
     // keys_out: search grid indices [t_lo, t_hi) only and write the packed key
     //           (grid modes; kNone for the others) instead of a plan.
     // keys_in : skip the search of grid modes and decode the given key (the
@@ -288,13 +289,10 @@ plan_sweep_kernel(const ds_problem* __restrict__ problems, int n,
         s.b2[j] = b;
         s.e2[j] = e;
         s.T2[j] = __ddiv_rn(static_cast<double>(b), e);
-    } else if (tid == 128) {
-        double acc = 0.0;   // profiles.cpp:104: below += bin_mass[i], in order
-        s.prefix[0] = 0.0;
-        for (int k = 0; k < DS_CURVE_BINS; ++k) {
-            acc = __dadd_rn(acc, c->deferral.bin_mass[k]);
-            s.prefix[k + 1] = acc;
-        }
+    } else if (tid >= 128 && tid - 128 <= DS_CURVE_BINS) {
+        // the cascade's sequential prefix table (built once per call by
+        // curve_prefix_kernel, in the reference's summation order)
+        s.prefix[tid - 128] = prefix_tab[p.cascade * (DS_CURVE_BINS + 1) + (tid - 128)];
     }
     __syncthreads();
 
@@ -559,20 +557,55 @@ extern "C" ds_status ds_plan_validate(const ds_problem* problems, int32_t n,
     return DS_OK;
 }
 
+namespace {
+
+// deferral_fraction's running sum below each bin (profiles.cpp:98-106): one
+// thread per cascade adds the bins in order, so every prefix entry is
+// bit-identical to the reference's `below`.
+__global__ void curve_prefix_kernel(const ds_cascade* __restrict__ cascades, int nc,
+                                    double* __restrict__ tab) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    double acc = 0.0;   // profiles.cpp:104: below += bin_mass[i], in order
+    double* t = tab + static_cast<size_t>(c) * (DS_CURVE_BINS + 1);
+    t[0] = 0.0;
+    for (int k = 0; k < DS_CURVE_BINS; ++k) {
+        acc = __dadd_rn(acc, cascades[c].deferral.bin_mass[k]);
+        t[k + 1] = acc;
+    }
+}
+
+ds_status launch_sweep(ds_ctx* ctx, const ds_problem* problems, int32_t n,
+                       const ds_cascade* cascades, int32_t n_cascades, const double* grid_values,
+                       const int32_t* grid_offsets, ds_plan* out, int t_lo, int t_hi,
+                       unsigned long long* keys_out, const unsigned long long* keys_in,
+                       cudaStream_t st) {
+    if (n_cascades <= 0) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "no cascades");
+    double* tab = nullptr;
+    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tab),
+                                sizeof(double) * (DS_CURVE_BINS + 1) * n_cascades, st));
+    curve_prefix_kernel<<<(n_cascades + 31) / 32, 32, 0, st>>>(cascades, n_cascades, tab);
+    DS_LAUNCH_CHECK(ctx, "curve_prefix_kernel");
+    plan_sweep_kernel<<<n, kThreads, 0, st>>>(problems, n, cascades, grid_values, grid_offsets,
+                                              out, t_lo, t_hi, keys_out, keys_in, tab);
+    DS_LAUNCH_CHECK(ctx, "plan_sweep_kernel");
+    cudaFreeAsync(tab, st);
+    return DS_OK;
+}
+
+} // namespace
+
 extern "C" ds_status ds_plan_batch_device(ds_ctx* ctx, const ds_problem* problems, int32_t n,
                                           const ds_cascade* cascades, int32_t n_cascades,
                                           const double* grid_values,
                                           const int32_t* grid_offsets, int32_t n_grids,
                                           ds_plan* out, void* stream) {
-    (void)n_cascades;
     (void)n_grids;
     if (!ctx) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null ctx");
     if (n <= 0) return DS_OK;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    plan_sweep_kernel<<<n, kThreads, 0, st>>>(problems, n, cascades, grid_values, grid_offsets,
-                                              out, 0, 0, nullptr, nullptr);
-    DS_LAUNCH_CHECK(ctx, "plan_sweep_kernel");
-    return DS_OK;
+    return launch_sweep(ctx, problems, n, cascades, n_cascades, grid_values, grid_offsets, out, 0,
+                        0, nullptr, nullptr, st);
 }
 
 extern "C" ds_status ds_plan_keys_device(ds_ctx* ctx, const ds_problem* problems, int32_t n,
@@ -580,17 +613,13 @@ extern "C" ds_status ds_plan_keys_device(ds_ctx* ctx, const ds_problem* problems
                                          const double* grid_values, const int32_t* grid_offsets,
                                          int32_t n_grids, int32_t t_lo, int32_t t_hi,
                                          uint64_t* keys, void* stream) {
-    (void)n_cascades;
     (void)n_grids;
     if (!ctx || (n > 0 && !keys)) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
     if (t_lo < 0 || t_hi < t_lo) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "bad threshold range");
     if (n <= 0) return DS_OK;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    plan_sweep_kernel<<<n, kThreads, 0, st>>>(problems, n, cascades, grid_values, grid_offsets,
-                                              nullptr, t_lo, t_hi,
-                                              reinterpret_cast<unsigned long long*>(keys), nullptr);
-    DS_LAUNCH_CHECK(ctx, "plan_sweep_kernel");
-    return DS_OK;
+    return launch_sweep(ctx, problems, n, cascades, n_cascades, grid_values, grid_offsets, nullptr,
+                        t_lo, t_hi, reinterpret_cast<unsigned long long*>(keys), nullptr, st);
 }
 
 extern "C" ds_status ds_plan_from_keys_device(ds_ctx* ctx, const ds_problem* problems, int32_t n,
@@ -598,16 +627,12 @@ extern "C" ds_status ds_plan_from_keys_device(ds_ctx* ctx, const ds_problem* pro
                                               const double* grid_values,
                                               const int32_t* grid_offsets, int32_t n_grids,
                                               const uint64_t* keys, ds_plan* out, void* stream) {
-    (void)n_cascades;
     (void)n_grids;
     if (!ctx || (n > 0 && (!keys || !out))) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
     if (n <= 0) return DS_OK;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    plan_sweep_kernel<<<n, kThreads, 0, st>>>(problems, n, cascades, grid_values, grid_offsets,
-                                              out, 0, 0, nullptr,
-                                              reinterpret_cast<const unsigned long long*>(keys));
-    DS_LAUNCH_CHECK(ctx, "plan_sweep_kernel");
-    return DS_OK;
+    return launch_sweep(ctx, problems, n, cascades, n_cascades, grid_values, grid_offsets, out, 0,
+                        0, nullptr, reinterpret_cast<const unsigned long long*>(keys), st);
 }
 
 namespace {
