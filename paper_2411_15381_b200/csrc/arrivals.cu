@@ -178,7 +178,9 @@ __device__ __forceinline__ void load_striped(const double* __restrict__ e, int64
 }
 
 __global__ void __launch_bounds__(kSumThreads, 1)
-target_sum_kernel(const double* __restrict__ e, int64_t n, double* __restrict__ T) {
+target_sum_kernel(const double* __restrict__ e, int64_t n, double* __restrict__ T,
+                  const int* __restrict__ only_if) {
+    if (only_if && !*only_if) return;   // the grid-wide pass succeeded
     extern __shared__ double sbuf_all[];
     __shared__ unsigned long long s_wsum[2][kSumThreads / 32];
     __shared__ unsigned s_wmin[2][kSumThreads / 32];
@@ -295,6 +297,323 @@ target_sum_kernel(const double* __restrict__ e, int64_t n, double* __restrict__ 
             i += tile_len;
         }
     }
+}
+
+// ---- K8c, grid-wide: the same exact running sum without the single SM ------
+// (1) an approximate fp64 prefix sum A_i of the draws (block sums, one-block
+//     scan of the block sums, in-block scans) fixes the binade p_i of every
+//     accumulator T_{i-1}; A differs from the sequentially rounded T by at
+//     most ~D ulps, so outside a margin around powers of two the binade is the
+//     true one;
+// (2) each step outside the margin, with no rounding tie and staying in its
+//     binade, adds the exact integer r_i = rint(e_i / ulp(p_i)) to the
+//     accumulator's mantissa; the others are "special" and done as real fp64
+//     adds: step 0, binade crossings, ties (~log2(D) + a few in all);
+// (3) an exact int64 scan of r, one sequential pass over the special steps
+//     (their fp64 adds and each segment's starting mantissa), and a grid-wide
+//     write of every T_i = (M_segment + R_i - R_segment_start) * ulp.
+// Every assumption is re-checked exactly (each segment's mantissa must stay
+// below 2^53); if one fails, or the specials overflow their buffer, a device
+// flag makes the single-CTA target_sum_kernel above redo the whole sum.
+constexpr int kTsThreads = 256;
+constexpr int kTsPer = 8;
+constexpr int kTsBlock = kTsThreads * kTsPer;   // steps per block
+constexpr int kTsMaxSpecial = 1 << 16;
+
+__device__ __forceinline__ int binade_of(double x) {   // biased exponent (x > 0, normal)
+    return static_cast<int>(static_cast<unsigned long long>(__double_as_longlong(x)) >> 52);
+}
+// x within relative `margin` of a power of two (either side), or not a
+// positive normal number
+__device__ __forceinline__ bool near_pow2(double x, double margin) {
+    if (!(x > 0.0)) return true;
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    const int ex = static_cast<int>(b >> 52);
+    if (ex == 0 || ex >= 2046) return true;
+    const double f = __longlong_as_double(static_cast<long long>((b & ((1ULL << 52) - 1)) |
+                                                                 (1023ULL << 52)));   // [1, 2)
+    return f - 1.0 < margin || 2.0 - f < 2.0 * margin;
+}
+
+template <typename T, typename Op>
+__device__ __forceinline__ T block_incl_scan(T v, T* sh, Op op) {   // kTsThreads threads
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = op(v, t);
+    }
+    if (lane == 31) sh[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        T w = lane < kTsThreads / 32 ? sh[lane] : T(0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w = op(w, t);
+        }
+        if (lane < kTsThreads / 32) sh[lane] = w;
+    }
+    __syncthreads();
+    const T before = warp > 0 ? sh[warp - 1] : T(0);
+    __syncthreads();
+    return warp > 0 ? op(before, v) : v;
+}
+
+struct TsAdd {
+    template <typename T>
+    __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
+};
+
+// (1a) per-block sums of the draws
+__global__ void __launch_bounds__(kTsThreads) ts_block_sum_kernel(const double* __restrict__ e,
+                                                                  int64_t n,
+                                                                  double* __restrict__ bsum) {
+    __shared__ double sh[kTsThreads / 32];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kTsBlock + threadIdx.x * kTsPer;
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kTsPer; ++q) v += base + q < n ? e[base + q] : 0.0;
+    v = block_incl_scan(v, sh, TsAdd());
+    if (threadIdx.x == kTsThreads - 1) bsum[blockIdx.x] = v;
+}
+
+// one block: exclusive scan of v[0..nb) in place, the total into v[nb]
+template <typename T>
+__global__ void __launch_bounds__(kTsThreads) ts_scan_blocks_kernel(T* __restrict__ v, int64_t nb) {
+    __shared__ T sh[kTsThreads / 32];
+    T carry = T(0);
+    for (int64_t c = 0; c < nb; c += kTsThreads) {
+        const int64_t k = c + threadIdx.x;
+        const T x = k < nb ? v[k] : T(0);
+        const T inc = block_incl_scan(x, sh, TsAdd());
+        if (k < nb) v[k] = carry + (inc - x);
+        carry = carry + sh[kTsThreads / 32 - 1];   // this chunk's total
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) v[nb] = carry;
+}
+
+// (1b)+(2) approximate prefix -> binade, integer increments, specials
+__global__ void __launch_bounds__(kTsThreads)
+ts_local_kernel(const double* __restrict__ e, int64_t n, const double* __restrict__ boff,
+                double margin, long long* __restrict__ r, unsigned char* __restrict__ special,
+                long long* __restrict__ brsum, long long* __restrict__ bspec) {
+    __shared__ double shd[kTsThreads / 32];
+    __shared__ long long shl[kTsThreads / 32];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kTsBlock + threadIdx.x * kTsPer;
+    double ev[kTsPer];
+    double loc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kTsPer; ++q) {
+        ev[q] = base + q < n ? e[base + q] : 0.0;
+        loc += ev[q];
+    }
+    const double incl = block_incl_scan(loc, shd, TsAdd());
+    double acc = boff[blockIdx.x] + (incl - loc);   // ~T_{base-1}
+    long long rs = 0, sp = 0;
+#pragma unroll
+    for (int q = 0; q < kTsPer; ++q) {
+        const int64_t i = base + q;
+        if (i >= n) break;
+        const double next = acc + ev[q];           // ~T_i
+        bool spec = i == 0 || near_pow2(acc, margin) || near_pow2(next, margin) ||
+                    binade_of(acc) != binade_of(next);
+        long long rr = 0;
+        if (!spec) {
+            const int bexp = binade_of(acc);
+            const double y = __dmul_rn(ev[q], __longlong_as_double(
+                                                  static_cast<long long>(2098 - bexp) << 52));
+            const double t = __dadd_rn(y, 0x1.0p52);            // rint(y), ties to even
+            const double d = __dsub_rn(__dsub_rn(t, 0x1.0p52), y);
+            if (!(y < 0x1.0p52) || d == 0.5 || d == -0.5 || bexp < 1023 - 60 || bexp > 1023 + 500)
+                spec = true;
+            else
+                rr = static_cast<long long>(static_cast<unsigned long long>(__double_as_longlong(t)) -
+                                            0x4330000000000000ULL);
+        }
+        r[i] = rr;
+        special[i] = spec ? 1 : 0;
+        rs += rr;
+        sp += spec ? 1 : 0;
+        acc = next;
+    }
+    rs = block_incl_scan(rs, shl, TsAdd());
+    const long long spt = block_incl_scan(sp, shl, TsAdd());
+    if (threadIdx.x == kTsThreads - 1) {
+        brsum[blockIdx.x] = rs;
+        bspec[blockIdx.x] = spt;
+    }
+}
+
+// (3a) in-block scans + block offsets: r -> inclusive R_i, special indices in order
+__global__ void __launch_bounds__(kTsThreads)
+ts_scan_kernel(int64_t n, long long* __restrict__ r, const unsigned char* __restrict__ special,
+               const long long* __restrict__ brsum, const long long* __restrict__ bspec,
+               long long* __restrict__ spec_idx, int* __restrict__ fail) {
+    __shared__ long long shl[kTsThreads / 32];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kTsBlock + threadIdx.x * kTsPer;
+    long long rv[kTsPer];
+    long long rs = 0, sp = 0;
+#pragma unroll
+    for (int q = 0; q < kTsPer; ++q) {
+        const bool in = base + q < n;
+        rv[q] = in ? r[base + q] : 0;
+        rs += rv[q];
+        sp += in && special[base + q] ? 1 : 0;
+    }
+    long long R = block_incl_scan(rs, shl, TsAdd()) - rs + brsum[blockIdx.x];
+    long long k = block_incl_scan(sp, shl, TsAdd()) - sp + bspec[blockIdx.x];
+#pragma unroll
+    for (int q = 0; q < kTsPer; ++q) {
+        const int64_t i = base + q;
+        if (i >= n) break;
+        R += rv[q];
+        r[i] = R;
+        if (special[i]) {
+            if (k < kTsMaxSpecial) spec_idx[k] = i;
+            else *fail = 1;
+            ++k;
+        }
+    }
+}
+
+struct TsSeg {
+    unsigned long long M, ebits;
+    long long Rbase;
+    long long pad;
+};
+
+// (3b) one block: the special steps in order (fp64 adds) and every segment's
+// start; checks that no segment leaves its binade
+__global__ void __launch_bounds__(kTsThreads)
+ts_skeleton_kernel(const double* __restrict__ e, int64_t n, const long long* __restrict__ R,
+                   const long long* __restrict__ spec_idx, const long long* __restrict__ bspec,
+                   int64_t nb, TsSeg* __restrict__ seg, double* __restrict__ T,
+                   int* __restrict__ fail) {
+    __shared__ long long s_idx[1024];
+    __shared__ long long s_rprev[1024];
+    __shared__ double s_e[1024];
+    __shared__ int s_fail;
+    const long long nspec = bspec[nb];   // total specials (end of the exclusive scan)
+    if (nspec > kTsMaxSpecial || *fail) {
+        if (threadIdx.x == 0) *fail = 1;
+        return;                          // uniform across the block
+    }
+    if (threadIdx.x == 0) s_fail = 0;
+    constexpr unsigned long long kLimit = (1ULL << 53) - 2;
+    unsigned long long M = 0, ebits = 0;
+    long long Rbase = 0;
+    for (long long c = 0; c < nspec; c += 1024) {
+        const int cnt = static_cast<int>(nspec - c < 1024 ? nspec - c : 1024);
+        __syncthreads();
+        for (int k = threadIdx.x; k < cnt; k += kTsThreads) {
+            const long long i = spec_idx[c + k];
+            s_idx[k] = i;
+            s_rprev[k] = i > 0 ? R[i - 1] : 0;
+            s_e[k] = e[i];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && !s_fail) {
+            for (int k = 0; k < cnt; ++k) {
+                const long long i = s_idx[k];
+                double Tcur;
+                if (i == 0) {
+                    Tcur = s_e[k];                              // T_0 = e_0
+                } else {
+                    const unsigned long long P = M + static_cast<unsigned long long>(s_rprev[k] - Rbase);
+                    if (c + k == 0 || P > kLimit) { s_fail = 1; break; }
+                    Tcur = __dadd_rn(from_binade(P, ebits), s_e[k]);
+                }
+                T[i] = Tcur;
+                const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(Tcur));
+                const int bexp = static_cast<int>(b >> 52);
+                if (bexp < 1023 - 60 || bexp > 1023 + 500) { s_fail = 1; break; }
+                ebits = static_cast<unsigned long long>(bexp) << 52;
+                M = (b & ((1ULL << 52) - 1)) | (1ULL << 52);
+                Rbase = s_rprev[k];   // r_i = 0 for a special step: R_i == R_{i-1}
+                seg[c + k] = TsSeg{M, ebits, Rbase, 0};
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (!s_fail && n > 0) {   // the last segment must end inside its binade
+            const unsigned long long P = M + static_cast<unsigned long long>(R[n - 1] - Rbase);
+            if (P > kLimit) s_fail = 1;
+        }
+        if (s_fail) *fail = 1;
+    }
+}
+
+// (3c) every non-special T_i from its segment
+__global__ void __launch_bounds__(kTsThreads)
+ts_write_kernel(int64_t n, const long long* __restrict__ R, const unsigned char* __restrict__ special,
+                const long long* __restrict__ bspec, const TsSeg* __restrict__ seg,
+                const int* __restrict__ fail, double* __restrict__ T) {
+    __shared__ long long shl[kTsThreads / 32];
+    if (*fail) return;
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kTsBlock + threadIdx.x * kTsPer;
+    long long sp = 0;
+#pragma unroll
+    for (int q = 0; q < kTsPer; ++q) sp += base + q < n && special[base + q] ? 1 : 0;
+    long long k = block_incl_scan(sp, shl, TsAdd()) - sp + bspec[blockIdx.x] - 1;
+#pragma unroll
+    for (int q = 0; q < kTsPer; ++q) {
+        const int64_t i = base + q;
+        if (i >= n) break;
+        if (special[i]) { ++k; continue; }
+        const TsSeg sg = seg[k];
+        T[i] = from_binade(sg.M + static_cast<unsigned long long>(R[i] - sg.Rbase), sg.ebits);
+    }
+}
+
+ds_status target_sum(ds_ctx* ctx, const double* e, int64_t D, double* T, cudaStream_t st) {
+    const int64_t nb = (D + kTsBlock - 1) / kTsBlock;
+    char* buf = nullptr;
+    const size_t b_r = dsi::align_up(sizeof(long long) * D, 256);
+    const size_t b_sp = dsi::align_up(static_cast<size_t>(D), 256);
+    const size_t b_nb = dsi::align_up(sizeof(long long) * (nb + 1), 256);
+    const size_t b_idx = dsi::align_up(sizeof(long long) * kTsMaxSpecial, 256);
+    const size_t b_seg = dsi::align_up(sizeof(TsSeg) * kTsMaxSpecial, 256);
+    const size_t total = b_r + b_sp + 3 * b_nb + b_idx + b_seg + 256;
+    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&buf), total, st));
+    char* q = buf;
+    long long* r = reinterpret_cast<long long*>(q); q += b_r;
+    unsigned char* special = reinterpret_cast<unsigned char*>(q); q += b_sp;
+    double* bsum = reinterpret_cast<double*>(q); q += b_nb;
+    long long* brsum = reinterpret_cast<long long*>(q); q += b_nb;
+    long long* bspec = reinterpret_cast<long long*>(q); q += b_nb;
+    long long* spec_idx = reinterpret_cast<long long*>(q); q += b_idx;
+    TsSeg* seg = reinterpret_cast<TsSeg*>(q); q += b_seg;
+    int* fail = reinterpret_cast<int*>(q);
+    DS_CUDA_TRY(cudaMemsetAsync(fail, 0, sizeof(int), st));
+    const double margin = 1e-7 + 4.0 * static_cast<double>(D) * 0x1.0p-52;
+    const unsigned g = static_cast<unsigned>(nb);
+    ts_block_sum_kernel<<<g, kTsThreads, 0, st>>>(e, D, bsum);
+    DS_LAUNCH_CHECK(ctx, "ts_block_sum_kernel");
+    ts_scan_blocks_kernel<double><<<1, kTsThreads, 0, st>>>(bsum, nb);
+    DS_LAUNCH_CHECK(ctx, "ts_scan_blocks_kernel");
+    ts_local_kernel<<<g, kTsThreads, 0, st>>>(e, D, bsum, margin, r, special, brsum, bspec);
+    DS_LAUNCH_CHECK(ctx, "ts_local_kernel");
+    ts_scan_blocks_kernel<long long><<<1, kTsThreads, 0, st>>>(brsum, nb);
+    DS_LAUNCH_CHECK(ctx, "ts_scan_blocks_kernel");
+    ts_scan_blocks_kernel<long long><<<1, kTsThreads, 0, st>>>(bspec, nb);
+    DS_LAUNCH_CHECK(ctx, "ts_scan_blocks_kernel");
+    ts_scan_kernel<<<g, kTsThreads, 0, st>>>(D, r, special, brsum, bspec, spec_idx, fail);
+    DS_LAUNCH_CHECK(ctx, "ts_scan_kernel");
+    ts_skeleton_kernel<<<1, kTsThreads, 0, st>>>(e, D, r, spec_idx, bspec, nb, seg, T, fail);
+    DS_LAUNCH_CHECK(ctx, "ts_skeleton_kernel");
+    ts_write_kernel<<<g, kTsThreads, 0, st>>>(D, r, special, bspec, seg, fail, T);
+    DS_LAUNCH_CHECK(ctx, "ts_write_kernel");
+    // fallback: the single-CTA exact scan, a no-op unless a check failed
+    DS_CUDA_TRY(cudaFuncSetAttribute(target_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kSumSmem)));
+    const int* gate = std::getenv("DS_TARGET_SUM_SEQUENTIAL") ? nullptr : fail;   // test hook
+    target_sum_kernel<<<1, kSumThreads, kSumSmem, st>>>(e, D, T, gate);
+    DS_LAUNCH_CHECK(ctx, "target_sum_kernel");
+    cudaFreeAsync(buf, st);
+    return DS_OK;
 }
 
 // ---- K8d: place targets in intervals ------------------------------------------
@@ -537,11 +856,8 @@ ds_status generate(ds_ctx* ctx, const double* rates, int32_t n_rates, double dt,
             if (blocks > 148 * 16) blocks = 148 * 16;
             exp_draws_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(raw, D, e);
             DS_LAUNCH_CHECK(ctx, "exp_draws_kernel");
-            DS_CUDA_TRY(cudaFuncSetAttribute(target_sum_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSumSmem)));
-            target_sum_kernel<<<1, kSumThreads, kSumSmem, st>>>(e, D, T);
-            DS_LAUNCH_CHECK(ctx, "target_sum_kernel");
+            s = target_sum(ctx, e, D, T, st);
+            if (s != DS_OK) return s;
         }
         place_kernel<<<static_cast<unsigned>(nb), kPlaceThreads, 0, st>>>(T, D, thr, ip, P, key,
                                                                            bmax, flags);

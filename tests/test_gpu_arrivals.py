@@ -192,3 +192,18 @@ def test_query_records_match_latent_columns(ctx):
         ctx.sample_query_records(m.pod(), arr[:10], 0.0)
     with pytest.raises(DomainError):
         ctx.sample_query_records(QueryOutcomeModel(easy_fraction=1.5).pod(), arr[:10], 1.0)
+
+
+def test_grid_wide_target_sum_equals_single_cta_scan(ctx, monkeypatch):
+    """K8c runs grid-wide (approximate prefix -> binades, exact integer scan,
+    fp64 adds only at the special steps); DS_TARGET_SUM_SEQUENTIAL forces the
+    single-CTA exact scan it falls back to. Both must give the same bits, and
+    the C restatement's, on a 1M-arrival trace and on bursty rates."""
+    for rates, seed in (([2500.0] * 400, 3), ([0.0, 9000.0, 1.0, 0.0, 52000.0, 3.0] * 5, 11)):
+        rates = np.asarray(rates, np.float64)
+        grid = ctx.generate_arrivals(rates, 1.0, seed, abi.ARRIVALS_POISSON)
+        monkeypatch.setenv("DS_TARGET_SUM_SEQUENTIAL", "1")
+        seq = ctx.generate_arrivals(rates, 1.0, seed, abi.ARRIVALS_POISSON)
+        monkeypatch.delenv("DS_TARGET_SUM_SEQUENTIAL")
+        assert grid.tobytes() == seq.tobytes()
+        assert grid.tobytes() == port_arrivals(rates, 1.0, seed, abi.ARRIVALS_POISSON).tobytes()
