@@ -19,7 +19,10 @@
 // W2[255,1023] = 1, so h2[:,1023] = 16 and W3[1023,:] is layer 3's bias.
 // The epilogue therefore never adds a bias after GEMM2/GEMM3.
 //
-// SM pairs (cta_group::2), persistent over whole images. Each CTA of a pair
+// SM pairs (cta_group::2), persistent; 256-token pair tiles are dealt round
+// robin over the pairs (one head sum per 128-token tile, summed per image in
+// tile order by finalize_kernel, so results do not depend on the batch
+// split). Each CTA of a pair
 // owns 128 tokens of a 256-token pair tile and HALF of every weight stage
 // (128 of the 256 output rows), so each SM streams 0.6 MB of weights per 128
 // tokens instead of 1.2 MB; one thread of the leader CTA issues M = 256 MMAs
@@ -31,7 +34,7 @@
 //               [192, 256)
 //   warps 4-11  epilogue: tcgen05.ld of this CTA's TMEM lanes, activation,
 //               bf16 pack, SW128 stores of H1/H2 (next GEMM's A operand), and
-//               the head dot product + per-image sum
+//               the head dot product (E3, per-tile sum)
 //   warp 12     weight producer: tensor-map TMA of this CTA's 16 KB half of
 //               each pre-swizzled 32 KB stage (256 rows x 128 B, SW128; L2
 //               evict-last) into a 4-stage ring; completion lands on the
@@ -51,7 +54,9 @@
 // The epilogue signals "accumulator drained" as soon as its TMEM loads land
 // (packed bf16 values stay in registers) and stores H2_j only after the GEMM3
 // still reading the previous H2 chunk committed, so G2_{j+1} overlaps E2_j and
-// G3_3(i-1) overlaps E1(i).
+// G3_3(i-1) overlaps E1(i). GEMM2_0's first two weight stages are parked in the
+// A slots (free from GEMM1's end until the next tile's first chunks), loaded
+// right after GEMM1 by warp 14; E3(i-1) runs after E2_0(i).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -86,9 +91,6 @@ constexpr int kAStages = DS_A_STAGES, kBStages = 6 - DS_A_STAGES;   // 6 x 16 KB
 constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (idle during GEMM1)
 #ifndef DS_AW
 #define DS_AW 1
-#endif
-#ifndef DS_E3_FIRST
-#define DS_E3_FIRST 0
 #endif
 constexpr int kAWStages = DS_AW ? 2 : 0; // W2_0 stages 0-1 land in the A ring (idle from GEMM1's
                                         // end until GEMM2_0 has read them)
@@ -437,11 +439,6 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             group_signal(&B.drained, 3, 256, first);
             DS_TRACE(1, tile, 1);
 
-#if DS_E3_FIRST
-            // ---- E3 of the previous tile (its G3_3 was issued after G1(tile)) ----
-            if (tile > 0) e3(tile - 1);
-#endif
-
             // ---- E2_j: acc[0,256) -> ReLU -> bf16 (registers) -> H2 (R2) --------
             for (int j = 0; j < 4; ++j) {
                 mbar_wait(&B.acc12_full, p12);
@@ -478,11 +475,9 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 fence_proxy_async_smem();
                 group_signal(&B.h2_ready, 3, 256, first);
                 DS_TRACE(1, tile, 3 + 2 * j);
-#if !DS_E3_FIRST
                 // ---- E3 of the previous tile: after E2_0, so GEMM2_1 is not held
                 // behind it; it must finish before GEMM3_0 (after GEMM2_1)
                 if (j == 0 && tile > 0) e3(tile - 1);
-#endif
             }
         }
         if (my_tiles > 0) e3(my_tiles - 1);
