@@ -135,3 +135,22 @@ def test_disc_matches_torch_fp32_reference(disc, weights):
     for seed, n, hw in ((21, 5, 512), (22, 2, 1024)):
         imgs = disc_oracle.synth_images(seed, 0, n, hw, hw)
         check_conf(disc.score(imgs), disc_forward_torch(imgs, weights))
+
+
+@pytest.mark.parametrize("n,h,w", [(1, 512, 512), (1, 128, 768), (3, 128, 768), (75, 128, 256),
+                                   (149, 128, 256)])
+def test_disc_pair_tile_edges(disc, weights, n, h, w):
+    """Pair tiles are dealt round robin over the SM pairs: one image, an odd
+    number of 128-token tiles (the last pair tile has a ghost half), more
+    pair tiles than pairs, and more images than SMs."""
+    imgs = disc_oracle.synth_images(31, 7, n, h, w)
+    got = disc.score(imgs)
+    check_conf(got, disc_oracle.disc_forward(imgs, weights))
+    # the same images scored one by one give the same bits (per-tile sums)
+    if n <= 3:
+        one = np.concatenate([disc.score(imgs[i:i + 1]) for i in range(n)])
+        assert np.array_equal(one, got)
+
+
+def test_disc_empty_batch(disc):
+    assert disc.score(np.zeros((0, 512, 512, 3), np.uint8)).shape == (0,)
