@@ -2,6 +2,8 @@
 
 Against the reference's own values (tests/golden/latent.npz from
 oracle/make_golden.py) and the C restatement (oracle/ds_oracle.c)."""
+import zlib
+
 import numpy as np
 import pytest
 
@@ -182,6 +184,87 @@ def test_curve_replay_long_vs_port(ctx, decay):
     lib.port().dso_curve_observe(abi.ptr(want), abi.ptr(conf), len(conf), decay)
     assert np.array_equal(got["bin_mass"].view(np.uint64), want["bin_mass"].view(np.uint64))
     assert np.float64(got["total_mass"]).view(np.uint64) == np.float64(want["total_mass"]).view(np.uint64)
+
+
+def _port_curve(curve, conf, decay):
+    want = curve.copy()
+    c = np.ascontiguousarray(conf, np.float64)
+    lib.port().dso_curve_observe(abi.ptr(want), abi.ptr(c), len(c), decay)
+    return want
+
+
+def _assert_same_bits(got, want):
+    assert np.array_equal(got["bin_mass"].view(np.uint64), want["bin_mass"].view(np.uint64))
+    assert np.float64(got["total_mass"]).view(np.uint64) == \
+        np.float64(want["total_mass"]).view(np.uint64)
+
+
+def _segmented_case(ctx, case):
+    rng = np.random.default_rng(zlib.crc32(case.encode()))
+    curve = workloads.uniform_prior()
+    if case == "latent_1m":
+        return curve, ctx.score_latent(workloads.query_model(), 0, 1_000_000), 0.999
+    if case == "latent_1m_f32":
+        c = ctx.score_latent(workloads.query_model(), 7, 1_000_000).astype(np.float32)
+        return curve, c, 0.999
+    if case == "one_bin":          # 100 bins decay without hits for the whole sequence
+        return curve, np.full(100_000, 0.375), 0.999
+    if case == "ragged":
+        return curve, rng.random(70_001), 0.99
+    if case == "slow_decay":       # the total's transient outlasts the sequence
+        return curve, rng.random(300_000), 0.99999
+    if case == "fast_decay":
+        return curve, rng.random(200_000), 1e-3
+    if case == "no_decay":
+        curve["bin_mass"][3] = 0.3           # fractional: the +1s round
+        return curve, rng.random(150_000), 1.0
+    if case == "two_phase":        # half the bins go quiet, then the other half
+        c = np.concatenate([rng.random(120_000) * 0.5, 0.5 + rng.random(120_000) * 0.5])
+        return curve, c, 0.999
+    if case == "large_state":
+        curve["bin_mass"][:] = np.linspace(1e-300, 1e300, 101)
+        curve["bin_mass"][7] = -0.0
+        curve["total_mass"] = 1e300
+        return curve, rng.random(100_000), 0.999
+    raise ValueError(case)
+
+
+@pytest.mark.parametrize("case", ["latent_1m", "latent_1m_f32", "one_bin", "ragged", "slow_decay",
+                                  "fast_decay", "no_decay", "two_phase", "large_state"])
+def test_curve_segmented_replay_vs_port(ctx, case):
+    """Sequences of >= 32K observations take the segmented speculative replay
+    (curve.cu, namespace spec): every segment replays from a closed-form guess
+    and is re-run from its predecessor's end until the states agree bit for
+    bit. The result must equal the sequential replay for any input, including
+    chains that never merge (hitless bins, d = 1, slow decay), which fall back
+    to the sequential walk."""
+    curve, conf, decay = _segmented_case(ctx, case)
+    got = ctx.curve_observe(curve, conf, decay)
+    _assert_same_bits(got, _port_curve(curve, conf.astype(np.float64), decay))
+
+
+def test_curve_segmented_invalid_confidence_stops_at_it(ctx):
+    """A confidence outside [0, 1] in a long sequence: the host variant raises
+    DomainError and the device variant leaves the curve replayed up to (not
+    including) that observation, where observe_confidence would throw."""
+    import torch
+    from paper_2411_15381_b200 import native
+    rng = np.random.default_rng(5)
+    conf = rng.random(200_000)
+    conf[123_457] = np.nan
+    conf[150_000] = 1.5
+    curve = workloads.uniform_prior()
+    with pytest.raises(DomainError):
+        ctx.curve_observe(curve, conf, 0.999)
+    dconf = torch.from_numpy(conf).cuda()
+    dcur = torch.from_numpy(curve.reshape(1).view(np.uint8).copy()).cuda()
+    torch.cuda.synchronize()
+    native.check(native.lib().ds_curve_observe_device(
+        ctx.handle, native.c_p(dcur.data_ptr()), native.c_p(dconf.data_ptr()), abi.CONF_F64,
+        len(conf), 0.999, None))
+    torch.cuda.synchronize()
+    got = dcur.cpu().numpy().view(abi.CURVE)[0]
+    _assert_same_bits(got, _port_curve(curve, conf[:123_457], 0.999))
 
 
 def test_curve_domain_errors(ctx):
