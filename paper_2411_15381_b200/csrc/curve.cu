@@ -17,7 +17,10 @@
 
 namespace {
 
-constexpr int kThreads = 128;   // 101 bins + total, padded to 4 warps
+// 101 bin threads on warps 0-3 and the total alone on warp 4: the total's loop
+// differs from the bins', so sharing a warp would run the two one after the other
+constexpr int kThreads = 160;
+constexpr int kTotalTid = 128;
 constexpr int kChunk = 4096;
 
 // m + 1 on a hit, else m. A real (divergent) branch rather than an
@@ -31,6 +34,87 @@ __device__ __forceinline__ double add_one_if(double m, bool hit) {
     return m;
 }
 
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+    return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+
+// The total's step t <- fl(fl(t*d) + 1), two roundings as in observe_confidence.
+template <bool kScale>
+__device__ __forceinline__ double total_exact(double t, double d) {
+    return __dadd_rn(kScale ? __dmul_rn(t, d) : t, 1.0);
+}
+
+#ifndef DS_TOTAL_DFMA
+#define DS_TOTAL_DFMA 1   // 0: the total always steps in the two-op form (A/B)
+#endif
+
+// f = RN(t*d + 1), ONE rounding, equals the reference's two-rounding step
+// RN(RN(t*d) + 1) whenever f lies in [2^k + 1 + 2u, 2^(k+1) - 2u] for some
+// 1 <= k <= 51, u = 2^(k-52). Proof: RN(y) = f with both neighbours of f in
+// binade k gives |y - f| <= u/2 for y = t*d + 1, so P = t*d lies in
+// [2^k + 1.5u, 2^(k+1) - 1 - 1.5u]; p = RN(P) is then in binade k with p + 1 <=
+// 2^(k+1) - u, a multiple of u (u <= 1/2), so RN(p + 1) = p + 1; and P + 1 =
+// (p + 1) + (P - p) with |P - p| <= u/2 rounds to p + 1 as well -- in a tie p is
+// even and (p + 1)/u = p/u + 2^(52-k) is even too, so ties-to-even picks p + 1.
+// Returns k, or -1 if f is outside every such interval.
+__device__ __forceinline__ int dfma_safe_binade(double f) {
+    const unsigned long long b = dbits(f);
+    const int k = static_cast<int>(b >> 52) - 1023;   // the sign bit makes k >= 1025
+    if (k < 1 || k > 51) return -1;
+    const unsigned long long m = b & ((1ull << 52) - 1);
+    return m >= (1ull << (52 - k)) + 2 && m <= (1ull << 52) - 2 ? k : -1;
+}
+
+// `len` steps of the total. The chain advances kRun steps at a time on single
+// DFMAs (one dependent fp64 op per step instead of two). The DFMA map is
+// monotone in t, so the outputs f_1..f_R of a run are monotone and lie between
+// f_1 and f_R: if both ends lie in the interval of the SAME binade k
+// (dfma_safe_binade), so does every output, and every step of the run equals
+// the two-rounding step. A run that fails the test (binade crossings, totals
+// below 2, negative or non-finite totals) is replayed in the exact two-op form.
+// The map is deterministic, so a step that leaves t unchanged proves the
+// rounded fixed point (~1/(1-d), reached after ~40K steps at d = 0.999): every
+// later step does too, `settled` is set and the replay stops.
+template <bool kScale>
+__device__ double total_run(double t, int64_t len, double d, bool& settled) {
+    constexpr int kRun = 32;
+    int64_t k = 0;
+    for (; k + kRun <= len; k += kRun) {
+        const double t0 = t;
+        bool fixed = false;
+        bool ok = false;
+        if (kScale && DS_TOTAL_DFMA) {
+            double prev = t, f1 = t;
+#pragma unroll
+            for (int u = 0; u < kRun; ++u) {
+                prev = t;
+                t = __fma_rn(t, d, 1.0);
+                if (u == 0) f1 = t;
+            }
+            const int k1 = dfma_safe_binade(f1);
+            ok = k1 >= 0 && dfma_safe_binade(t) == k1;
+            fixed = dbits(t) == dbits(prev);
+        }
+        if (!ok) {
+            t = t0;
+            fixed = false;
+#pragma unroll 4
+            for (int u = 0; u < kRun; ++u) {
+                const double x = total_exact<kScale>(t, d);
+                fixed |= dbits(x) == dbits(t);
+                t = x;
+            }
+        }
+        if (fixed) {
+            settled = true;
+            return t;
+        }
+    }
+    for (; k < len; ++k) t = total_exact<kScale>(t, d);
+    return t;
+}
+
 template <typename T, bool kScale>
 __global__ void __launch_bounds__(kThreads)
 curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int64_t n,
@@ -40,11 +124,11 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
     const int tid = threadIdx.x;
     double m = 0.0;
     if (tid < DS_CURVE_BINS) m = curve->bin_mass[tid];
-    else if (tid == DS_CURVE_BINS) m = curve->total_mass;
+    else if (tid == kTotalTid) m = curve->total_mass;
     bool settled = false;
     // the total-mass thread matches every observation; bin threads their own bin
     const unsigned mine = tid < DS_CURVE_BINS ? static_cast<unsigned>(tid) : 0xFFu;
-    const bool is_total = tid == DS_CURVE_BINS;
+    const bool is_total = tid == kTotalTid;
     for (int64_t base = 0; base < n; base += kChunk) {
         const int cnt = static_cast<int>(n - base < kChunk ? n - base : kChunk);
         if (tid == 0) chunk_bad = 0;
@@ -63,29 +147,12 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
             bins[k] = static_cast<unsigned char>(b);
         }
         __syncthreads();
-        if (tid <= DS_CURVE_BINS) {
+        if (tid < DS_CURVE_BINS || is_total) {
             if (!chunk_bad) {
                 if (is_total) {
-                    // every observation hits the total: t <- fl(fl(t*d) + 1). The map is
-                    // deterministic, so once a step leaves t unchanged (t reaches the
-                    // rounded fixed point, ~1/(1-d) after ~40K steps at d = 0.999) every
-                    // later step does too and the replay of the total can stop.
-                    // The fixed-point test runs once per 32 steps (one extra step,
-                    // discarded unless it proves the fixed point), off the chain.
-                    if (!settled) {
-                        int k = 0;
-                        for (; k + 32 <= cnt; k += 32) {
-                            if (kScale && __dadd_rn(__dmul_rn(m, decay), 1.0) == m) {
-                                settled = true;
-                                break;
-                            }
-#pragma unroll
-                            for (int u = 0; u < 32; ++u)
-                                m = __dadd_rn(kScale ? __dmul_rn(m, decay) : m, 1.0);
-                        }
-                        if (!settled)
-                            for (; k < cnt; ++k) m = __dadd_rn(kScale ? __dmul_rn(m, decay) : m, 1.0);
-                    }
+                    // every observation hits the total (total_run: DFMA chain,
+                    // verified; stops at the rounded fixed point)
+                    if (!settled) m = total_run<kScale>(m, cnt, decay, settled);
                 } else {
                     // 8 observations per 64-bit shared load; the add on a hit is a
                     // predicated instruction so a miss costs only the multiply
@@ -117,7 +184,7 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
         if (chunk_bad) break;
     }
     if (tid < DS_CURVE_BINS) curve->bin_mass[tid] = m;
-    else if (tid == DS_CURVE_BINS) curve->total_mass = m;
+    else if (is_total) curve->total_mass = m;
 }
 
 
@@ -267,14 +334,8 @@ __device__ __forceinline__ bool total_fixed(double t, double d) {
 // The total over `len` observations; a fixed point ends the replay early.
 template <bool kScale>
 __device__ double replay_total(double t, int64_t len, double d) {
-    int64_t k = 0;
-    for (; k + kCheck <= len; k += kCheck) {
-        if (total_fixed<kScale>(t, d)) return t;
-#pragma unroll
-        for (int u = 0; u < kCheck; ++u) t = total_step<kScale>(t, d);
-    }
-    for (; k < len; ++k) t = total_step<kScale>(t, d);
-    return t;
+    bool settled = false;
+    return total_run<kScale>(t, len, d, settled);
 }
 
 template <bool kScale>
@@ -352,7 +413,6 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
     __shared__ double plo[32];
     __shared__ double phi[kMaxL / 32];
     __shared__ double su[kThreads], se[kThreads];          // the total's segments
-    __shared__ int s_all_done;
     const int tid = threadIdx.x;
     const int j = blockIdx.x;
 

@@ -267,6 +267,21 @@ def test_curve_segmented_invalid_confidence_stops_at_it(ctx):
     _assert_same_bits(got, _port_curve(curve, conf[:123_457], 0.999))
 
 
+@pytest.mark.parametrize("n", [5_000, 40_000])
+@pytest.mark.parametrize("decay", [0.999, 0.5, 0.9999999, 1.0 - 2.0 ** -52, 1e-300, 1.0])
+def test_curve_total_chain_edge_starts(ctx, n, decay):
+    """The total's replay runs on a verified DFMA chain (curve.cu total_run):
+    starting totals that cross binades, sit on ties, are tiny, huge, zero or
+    negative must still give the two-rounding result bit for bit."""
+    rng = np.random.default_rng(n)
+    conf = rng.random(n)
+    for t0 in (0.0, -0.0, 0.3, 31.999999999999996, 5e-324, 1e-300, 1e300, -7.25, 2.0 ** 53 - 3):
+        curve = workloads.uniform_prior()
+        curve["total_mass"] = t0
+        got = ctx.curve_observe(curve, conf, decay)
+        _assert_same_bits(got, _port_curve(curve, conf, decay))
+
+
 def test_curve_domain_errors(ctx):
     c = workloads.uniform_prior()
     with pytest.raises(DomainError):
