@@ -43,6 +43,23 @@ def main(which):
             native.check(L.ds_score_latent_device(ctx.handle, abi.ptr(m), 0, 1_000_000,
                                                   native.c_p(c.data_ptr()), native.c_p(0), s))
         ctx.synchronize()
+    if which in ("curve", "all"):
+        # K3 on the latent leg's 1M confidences (segmented replay) and on 5K
+        # (single-CTA replay, the image step's size)
+        m = workloads.query_model()
+        c = torch.empty(1_000_000, dtype=torch.float64, device="cuda")
+        native.check(L.ds_score_latent_device(ctx.handle, abi.ptr(m), 0, 1_000_000,
+                                              native.c_p(c.data_ptr()), native.c_p(0), s))
+        prior = workloads.uniform_prior()
+        p_t = torch.from_numpy(prior.reshape(1).view(np.uint8).copy()).cuda()
+        cur = torch.empty_like(p_t)
+        for n in (1_000_000, 5_000):
+            for _ in range(3):
+                cur.copy_(p_t)
+                native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(cur.data_ptr()),
+                                                       native.c_p(c.data_ptr()), abi.CONF_F64, n,
+                                                       0.999, s))
+        ctx.synchronize()
     print("done")
 
 
