@@ -122,6 +122,7 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
     __shared__ __align__(16) unsigned char bins[kChunk];
     __shared__ int chunk_bad;
     const int tid = threadIdx.x;
+    if (tid == 0) *bad = 0x7fffffff;   // ordered before any atomicMin by the first __syncthreads
     double m = 0.0;
     if (tid < DS_CURVE_BINS) m = curve->bin_mass[tid];
     else if (tid == kTotalTid) m = curve->total_mass;
@@ -578,7 +579,6 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
 
 } // namespace spec
 
-__global__ void init_bad(int* bad) { *bad = 0x7fffffff; }
 
 __global__ void spec_init(int* changed, unsigned* bar, int* bad) {
     for (int i = threadIdx.x; i < spec::kMaxPasses * spec::kChains; i += blockDim.x) changed[i] = 0;
@@ -695,8 +695,6 @@ ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype,
         DS_LAUNCH_CHECK(ctx, "curve_spec_kernel");
         return DS_OK;
     }
-    init_bad<<<1, 1, 0, st>>>(dbad);
-    DS_LAUNCH_CHECK(ctx, "init_bad");
     if (dtype == DS_CONF_F64) {
         const double* c = static_cast<const double*>(conf);
         if (scale) curve_observe_kernel<double, true><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);

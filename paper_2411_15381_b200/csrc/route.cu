@@ -54,7 +54,9 @@ route_count_kernel(const T* __restrict__ conf, int64_t n, const double* __restri
     }
 }
 
-template <typename T>
+// kSingle: n fits one tile (n <= kTile, the light batches): no count pass, the
+// prefix of earlier tiles is 0 and the tile's own count is the total.
+template <typename T, bool kSingle = false>
 __global__ void __launch_bounds__(kThreads)
 route_scatter_kernel(const T* __restrict__ conf, int64_t n, const double* __restrict__ thr,
                      const int32_t* __restrict__ counts, int64_t index_base,
@@ -66,7 +68,9 @@ route_scatter_kernel(const T* __restrict__ conf, int64_t n, const double* __rest
     __shared__ long long s_prefix;
     __shared__ int warp_cnt[kPerThread][kThreads / 32];
     // exclusive prefix of earlier tiles (warp 0), and the grand total (last tile)
-    if (warp == 0) {
+    if (kSingle) {
+        if (threadIdx.x == 0) s_prefix = 0;
+    } else if (warp == 0) {
         long long acc = 0;
         for (int b = lane; b < tile; b += 32) acc += ck[b];
 #pragma unroll
@@ -106,6 +110,7 @@ route_scatter_kernel(const T* __restrict__ conf, int64_t n, const double* __rest
         }
         off += row;
     }
+    if (kSingle && threadIdx.x == 0) total_out[k] = off;
 }
 
 } // namespace
@@ -124,6 +129,18 @@ ds_status route_launch(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t n,
     if (tiles > 0x7fffffff || nt > 65535)
         return dsi::fail(DS_ERR_CAPACITY, "ds_route: too many tiles or thresholds");
     dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nt));
+    if (tiles == 1) {   // one launch for a light batch
+        if (dtype == DS_CONF_F64)
+            route_scatter_kernel<double, true><<<grid, kThreads, 0, st>>>(
+                static_cast<const double*>(conf), n, thresholds, nullptr, index_base, heavy_idx,
+                counts);
+        else
+            route_scatter_kernel<float, true><<<grid, kThreads, 0, st>>>(
+                static_cast<const float*>(conf), n, thresholds, nullptr, index_base, heavy_idx,
+                counts);
+        DS_LAUNCH_CHECK(ctx, "route_scatter_kernel");
+        return DS_OK;
+    }
     if (dtype == DS_CONF_F64) {
         route_count_kernel<double><<<grid, kThreads, 0, st>>>(
             static_cast<const double*>(conf), n, thresholds, scratch);
