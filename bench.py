@@ -510,6 +510,19 @@ def run_gpu(args):
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_value = ws * N_IMG / allmax([e2e_s])[0]
     h2d = N_IMG * H * W * 3 + grid_np.nbytes + 2 * abi.CURVE.itemsize
+    # what bounds e2e: the same pinned image bytes copied host -> device alone
+    # (one cudaMemcpyAsync per step, CUDA events), i.e. the PCIe roofline
+    pin_ms = []
+    for _ in range(3):
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a_.record(stream)
+            images.copy_(pinned)   # blocking: no host-allocator event outlives the context
+            b_.record(stream)
+        torch.cuda.synchronize()
+        pin_ms.append(a_.elapsed_time(b_))
+    h2d_gbs = pinned.numel() / (min(pin_ms) / 1000.0) / 1e9
+    e2e_gbs = N_IMG * H * W * 3 * (e2e_value / ws) / N_IMG / 1e9
 
     # ---- image legs for the other configs ------------------------
     def timed(fn, reps):
@@ -853,7 +866,10 @@ def run_gpu(args):
                          "note": "layer 1 (27% of FLOPs) is u8 x s8 on the int8 tensor path at "
                                  "2x the bf16 rate; its FLOPs count half"},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "bound": {"what": "host->device copy of the images (PCIe)",
+                              "achieved_gbs": e2e_gbs, "h2d_copy_alone_gbs": h2d_gbs,
+                              "frac": e2e_gbs / h2d_gbs}},
             "gpu_launches": launches,
             "clocks": clocks,
             "parity": {"route_counts_vs_confidences": parity_ok,
