@@ -32,6 +32,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // which oversleeps when the releasing arrive comes from the peer CTA.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+#if defined(DS_WAIT_HINT) && DS_WAIT_HINT > 0
+    // suspend-time hint (ns): the waiting thread sleeps until the phase
+    // completes or the hint expires instead of re-polling (experiment)
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}" ::"r"(a),
+        "r"(parity), "r"(static_cast<uint32_t>(DS_WAIT_HINT))
+        : "memory");
+#else
     asm volatile(
         "{\n\t"
         ".reg .pred P1;\n\t"
@@ -41,6 +54,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}" ::"r"(a),
         "r"(parity)
         : "memory");
+#endif
 }
 
 // ---- async proxy fences -------------------------------------------------------
