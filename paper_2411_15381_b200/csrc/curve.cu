@@ -11,6 +11,7 @@
 // staged through shared memory.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "ds_internal.h"
@@ -244,7 +245,18 @@ struct Ws {
     int* changed;         // [kMaxPasses][kChains]
     unsigned* bar;        // grid barrier arrivals
     int* bad;             // first invalid observation (INT_MAX if none)
+    unsigned long long* trace;   // debug (DS_CURVE_TRACE): phase timestamps, else nullptr
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SPEC_TRACE(slot)                                                        \
+    do {                                                                        \
+        if (ws.trace && threadIdx.x == 0) ws.trace[slot] = gtimer();            \
+    } while (0)
 
 __device__ __forceinline__ unsigned long long bits(double x) {
     return static_cast<unsigned long long>(__double_as_longlong(x));
@@ -411,6 +423,8 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
     extern __shared__ __align__(16) unsigned char sb[];   // [L] bins of this segment
     __shared__ double sh[kChains];
     __shared__ int sc[kChains];
+    __shared__ double swh[kThreads / 32][kChains];   // per-warp partial H
+    __shared__ double wsc[kThreads / 32][32];        // per-warp lane weights
     __shared__ double plo[32];
     __shared__ double phi[kMaxL / 32];
     __shared__ double su[kThreads], se[kThreads];          // the total's segments
@@ -419,6 +433,7 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
 
     if (j == S) {
         // ---- the total-mass CTA (not part of the grid barrier) ----
+        SPEC_TRACE(16);
         if (tid == 0)
             while (ld_acquire(ws.bar) < static_cast<unsigned>(S)) __nanosleep(128);
         __syncthreads();
@@ -436,6 +451,7 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
             se[tid] = replay_total<kScale>(t, e - a, d);
         }
         __syncthreads();
+        SPEC_TRACE(17);
         if (tid == 0) {
             const int segs = static_cast<int>((cover + lt - 1) / lt);
             double st = se[0];   // segment 0 starts at the true t0
@@ -453,38 +469,85 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
             }
             if (cover < n) st = replay_total<kScale>(st, n - cover, d);
             curve->total_mass = st;
+            SPEC_TRACE(18);
         }
         return;
     }
 
     // ---- phase 0: bins, hit counts, closed-form contributions ----
+    if (j == 0) SPEC_TRACE(0);
     const int64_t a = static_cast<int64_t>(j) * L;
     const int len = static_cast<int>(n - a < L ? n - a : L);
     if (tid < kChains) {
         sh[tid] = 0.0;
         sc[tid] = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) swh[w][tid] = 0.0;
     }
     if (tid < 32) plo[tid] = dpow(d, tid);
     for (int q = tid; q < (len + 31) / 32; q += kThreads) phi[q] = dpow(d, 32.0 * q);
     __syncthreads();
-    for (int k = tid; k < len; k += kThreads) {
-        const double c = static_cast<double>(conf[a + k]);
-        unsigned char bb;
-        if (!(c >= 0.0) || !(c <= 1.0)) {
-            atomicMin(ws.bad, static_cast<int>(a + k < 0x7fffffff ? a + k : 0x7fffffff));
-            bb = 255;
-        } else {
-            int b = static_cast<int>(floor(__dadd_rn(__dmul_rn(c, 100.0), 1e-9)));
-            b = b < 0 ? 0 : (b > DS_CURVE_BINS - 1 ? DS_CURVE_BINS - 1 : b);
-            bb = static_cast<unsigned char>(b);
-            const int i = len - 1 - k;   // d^i = d^(32q) d^r
-            const double w = phi[i >> 5] * plo[i & 31];
-            atomicAdd(&sh[b], w);
-            atomicAdd(&sc[b], 1);
+    if (j == 0) SPEC_TRACE(20);
+    // Bins first, 16 loads in flight per thread (the loop is bound by the
+    // confidences' HBM latency otherwise: ~25 us per segment).
+    for (int k0 = tid; k0 < len; k0 += 16 * kThreads) {
+        double cv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int k = k0 + u * kThreads;
+            cv[u] = k < len ? static_cast<double>(conf[a + k]) : 0.0;
         }
-        sb[k] = bb;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int k = k0 + u * kThreads;
+            if (k >= len) break;
+            const double c = cv[u];
+            unsigned char bb;
+            if (!(c >= 0.0) || !(c <= 1.0)) {
+                atomicMin(ws.bad, static_cast<int>(a + k < 0x7fffffff ? a + k : 0x7fffffff));
+                bb = 255;
+            } else {
+                // bin_of (profiles.cpp:60-65): floor(c*100 + 1e-9) clamped to [0, 100]
+                int b = static_cast<int>(floor(__dadd_rn(__dmul_rn(c, 100.0), 1e-9)));
+                b = b < 0 ? 0 : (b > DS_CURVE_BINS - 1 ? DS_CURVE_BINS - 1 : b);
+                bb = static_cast<unsigned char>(b);
+            }
+            sb[k] = bb;
+        }
     }
     __syncthreads();
+    if (j == 0) SPEC_TRACE(24);
+    // Closed-form contributions: each warp takes 32 consecutive observations at
+    // a time (lane = observation); lanes with the same bin are grouped
+    // (match_any) and the group's leader adds their weights d^(len-1-k) into the
+    // warp's own partial sums (shared-memory atomics on doubles were no faster).
+    {
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int k0 = 32 * warp; k0 < len; k0 += kThreads) {
+            const int k = k0 + lane;
+            const unsigned bb = k < len ? sb[k] : 0xFFFFu;
+            double w = 0.0;
+            if (bb < static_cast<unsigned>(DS_CURVE_BINS)) {
+                const int i = len - 1 - k;   // d^i = d^(32q) d^r
+                w = phi[i >> 5] * plo[i & 31];
+            }
+            wsc[warp][lane] = w;
+            const unsigned peers = __match_any_sync(0xffffffffu, bb);
+            __syncwarp();
+            if (bb < static_cast<unsigned>(DS_CURVE_BINS) && lane == __ffs(peers) - 1) {
+                double acc = 0.0;
+                for (unsigned m = peers; m; m &= m - 1) acc += wsc[warp][__ffs(m) - 1];
+                swh[warp][bb] += acc;
+                atomicAdd(&sc[bb], __popc(peers));
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (tid < DS_CURVE_BINS)
+        sh[tid] = (swh[0][tid] + swh[1][tid]) + (swh[2][tid] + swh[3][tid]);
+    __syncthreads();
+    if (j == 0) SPEC_TRACE(21);
     for (int k = tid * 16; k < len; k += kThreads * 16) {
         if (k + 16 <= len)
             *reinterpret_cast<uint4*>(ws.bins + a + k) = *reinterpret_cast<const uint4*>(sb + k);
@@ -495,8 +558,11 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
         ws.h[static_cast<int64_t>(j) * kChains + tid] = sh[tid];
         ws.cnt[static_cast<int64_t>(j) * kChains + tid] = sc[tid];
     }
+    if (j == 0) SPEC_TRACE(22);
+    if (j == S - 1) SPEC_TRACE(23);
     unsigned epoch = 0;
     grid_barrier(ws.bar, static_cast<unsigned>(S), epoch);
+    if (j == 0) SPEC_TRACE(1);
     const int bad = *reinterpret_cast<volatile int*>(ws.bad);
     if (bad != 0x7fffffff) {
         // the reference throws at the first invalid confidence: replay up to it
@@ -511,8 +577,17 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
     if (chain) {
         double g = curve->bin_mass[tid];
         if (j > 0) {
+            // g_j = d^(L j) m_0 + sum_{i<j} d^(L (j-1-i)) H_i; terms older than K
+            // segments weigh d^(L K) < 2^-60 and cannot move the guess
             const double dl = dpow(d, static_cast<double>(L));
-            for (int i = 0; i < j; ++i) {
+            const double lk = -static_cast<double>(L) * log(d);
+            const int K = lk > 0.0 ? static_cast<int>(fmin(60.0 * 0.6931471805599453 / lk + 1.0,
+                                                          static_cast<double>(j)))
+                                   : j;
+            const int i0 = j - K;
+            g = __dmul_rn(g, dpow(d, static_cast<double>(L) * i0));   // -0.0 stays -0.0
+#pragma unroll 4
+            for (int i = i0; i < j; ++i) {
                 const int64_t ri = static_cast<int64_t>(i) * kChains + tid;
                 g = ws.cnt[ri] ? __fma_rn(dl, g, ws.h[ri]) : __dmul_rn(dl, g);
             }
@@ -520,7 +595,9 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
         ws.u[row] = g;
         ws.e0[row] = replay_bin<kScale>(g, sb, len, mine, d);
     }
+    if (j == 0) SPEC_TRACE(2);
     grid_barrier(ws.bar, static_cast<unsigned>(S), epoch);
+    if (j == 0) SPEC_TRACE(3);
 
     // ---- passes ----
     bool resolved = !chain;
@@ -547,6 +624,7 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
             wr[row] = ev;
         }
         grid_barrier(ws.bar, static_cast<unsigned>(S), epoch);
+        if (j == 0) SPEC_TRACE(4 + pass);
         fin = wr;
         if (chain && !resolved)
             resolved = *reinterpret_cast<volatile int*>(&ws.changed[pass * kChains + tid]) == 0;
@@ -575,6 +653,7 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
         st = merged ? fin[ri] : r;
     }
     curve->bin_mass[tid] = st;
+    if (ws.trace && tid == 0) ws.trace[12] = gtimer();   // (a walker's end)
 }
 
 } // namespace spec
@@ -668,6 +747,11 @@ ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype,
         q += dsi::align_up(spec::kMaxPasses * spec::kChains * 4, 256);
         w.bar = reinterpret_cast<unsigned*>(q);
         w.bad = dbad;
+        static unsigned long long* trace_buf = nullptr;
+        static const bool want_trace = getenv("DS_CURVE_TRACE") != nullptr;
+        if (want_trace && !trace_buf) cudaMalloc(&trace_buf, 32 * sizeof(unsigned long long));
+        w.trace = want_trace ? trace_buf : nullptr;
+        if (w.trace) cudaMemsetAsync(w.trace, 0, 32 * sizeof(unsigned long long), st);
         spec_init<<<1, 256, 0, st>>>(w.changed, w.bar, w.bad);
         DS_LAUNCH_CHECK(ctx, "spec_init");
         cudaLaunchConfig_t cfg = {};
@@ -693,6 +777,24 @@ ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype,
         }
         if (e != cudaSuccess) return dsi::cuda_fail(e, "curve_spec_kernel");
         DS_LAUNCH_CHECK(ctx, "curve_spec_kernel");
+        if (w.trace) {   // debug: phase times (us from block 0's start) and pass counts
+            unsigned long long t[32];
+            int ch[spec::kMaxPasses * spec::kChains];
+            cudaMemcpyAsync(t, w.trace, sizeof(t), cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(ch, w.changed, sizeof(ch), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            auto us = [&](int i) { return t[i] ? (double)(t[i] - t[0]) / 1000.0 : -1.0; };
+            fprintf(stderr, "spec n=%lld L=%d S=%d: phase0 %.1f phase1 %.1f/%.1f passes", (long long)n, L, S,
+                    us(1), us(2), us(3));
+            for (int p = 0; p < spec::kMaxPasses; ++p) {
+                int c = 0, chains = 0;
+                for (int b = 0; b < spec::kChains; ++b) { c += ch[p * spec::kChains + b]; chains += ch[p * spec::kChains + b] > 0; }
+                fprintf(stderr, " [%.1f: %d segs, %d chains]", us(4 + p), c, chains);
+            }
+            fprintf(stderr, " (phase0: tables %.1f bins %.1f H %.1f writes %.1f last-block %.1f)", us(20), us(24), us(21), us(22), us(23));
+            fprintf(stderr, " walk-end %.1f | total CTA start %.1f spec %.1f walk %.1f us\n", us(12), us(16),
+                    us(17), us(18));
+        }
         return DS_OK;
     }
     if (dtype == DS_CONF_F64) {
