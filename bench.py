@@ -579,16 +579,14 @@ def run_gpu(args):
         sp = native.c_p(ctx.stream) if sp is None else sp
         curve1.copy_(prior_t)
         for off in range(0, N_IMG, B1):
+            # one light batch (cluster.cpp:288-307): score, observe, defer --
+            # the discriminator plus one fused tail launch
             m = min(B1, N_IMG - off)
-            cp = native.c_p(conf1.data_ptr() + 4 * off)
-            native.check(L.ds_disc_score_device(
-                disc.handle, native.c_p(images.data_ptr() + off * H * W * 3), m, H, W, cp, sp))
-            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve1.data_ptr()),
-                                                   cp, abi.CONF_F32, m, DECAY, sp))
-            native.check(L.ds_route_device(ctx.handle, cp, abi.CONF_F32, m,
-                                           native.c_p(thr5.data_ptr()), 1, id0 + off,
-                                           native.c_p(heavy1.data_ptr()),
-                                           native.c_p(count1.data_ptr()), sp))
+            native.check(L.ds_disc_batch_complete_device(
+                disc.handle, native.c_p(images.data_ptr() + off * H * W * 3), m, H, W,
+                native.c_p(conf1.data_ptr() + 4 * off), native.c_p(curve1.data_ptr()), DECAY,
+                native.c_p(thr5.data_ptr()), 1, id0 + off, native.c_p(heavy1.data_ptr()),
+                native.c_p(count1.data_ptr()), sp))
 
     def batch32_eager():
         with torch.cuda.stream(stream):
@@ -887,7 +885,7 @@ def run_gpu(args):
                                                 "us_per_batch": b32g_ms * 1000.0 / (
                                                     (N_IMG + B1 - 1) // B1),
                                                 "parity_vs_full_batch": b32g_parity},
-                                 "config": "config 1: 5K 512x512 in light batches of 32: score, "
+                                 "config": "config 1: 5K 512x512 in light batches of 32 (ds_disc_batch_complete_device): score, "
                                            "observe into the curve, route at t=0.5"},
             "cascade3": {"value": c3_value, "unit": "images/s", "image_hw": [H3, H3],
                          "images": N3, "ms_per_step": c3_ms,

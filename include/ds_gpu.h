@@ -376,6 +376,20 @@ ds_status ds_disc_score(ds_disc* disc, const uint8_t* nhwc, int64_t n, int32_t h
 ds_status ds_disc_score_device(ds_disc* disc, const uint8_t* nhwc, int64_t n, int32_t h,
                                int32_t w, float* conf, void* stream);
 
+/* One light batch as Simulation::handle_batch_complete (cluster.cpp:288-307)
+ * handles it: score the n images into conf, apply observe_confidence(curve,
+ * conf[i], decay) in batch order (profiles.cpp:108-120), then route every
+ * image at each threshold with Policy::defers (policies.cpp:37-39, strict <)
+ * into ordered heavy lists (row k of heavy_idx holds counts[k] ids, stride n).
+ * All pointers are device memory, stream-ordered. Bit-identical to
+ * ds_disc_score_device + ds_curve_observe_device + ds_route_device; batches of
+ * <= 2048 images run as the discriminator plus one fused tail launch. */
+ds_status ds_disc_batch_complete_device(ds_disc* disc, const uint8_t* nhwc, int64_t n,
+                                        int32_t h, int32_t w, float* conf, ds_curve* curve,
+                                        double decay, const double* thresholds,
+                                        int32_t n_thresholds, int64_t index_base,
+                                        int64_t* heavy_idx, int64_t* counts, void* stream);
+
 /* Synthetic image pool: pixel bytes are a pure
  * function of (seed, image id, pixel index); generated on the device. */
 ds_status ds_synth_images_device(ds_ctx* ctx, uint64_t seed, uint64_t id0, int64_t n,

@@ -677,14 +677,91 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
 }
 
 // logit = (sum of the image's per-tile head sums, in tile order) / tokens + b_head
+__device__ __forceinline__ float image_score(const float* __restrict__ part, long long i, int tpi,
+                                             int tokens, float hb, int logits) {
+    float s = 0.0f;
+    for (int t = 0; t < tpi; ++t) s += part[i * tpi + t];
+    const float logit = s / static_cast<float>(tokens) + hb;
+    return logits ? logit : 1.0f / (1.0f + expf(-logit));
+}
+
 __global__ void finalize_kernel(const float* __restrict__ part, long long n, int tpi, int tokens,
                                 float hb, int logits, float* __restrict__ out) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float s = 0.0f;
-    for (int t = 0; t < tpi; ++t) s += part[i * tpi + t];
-    const float logit = s / static_cast<float>(tokens) + hb;
-    out[i] = logits ? logit : 1.0f / (1.0f + expf(-logit));
+    out[i] = image_score(part, i, tpi, tokens, hb, logits);
+}
+
+// One light batch's completion after the discriminator, in one launch
+// (Simulation::handle_batch_complete, cluster.cpp:288-307): confidences from
+// the head sums (as finalize_kernel), then observe_confidence of each in batch
+// order (profiles.cpp:108-120; the arithmetic of curve.cu's single-CTA replay:
+// bins on warps 0-3, the total alone on warp 4, explicit _rn fp64), then
+// Policy::defers (strict <) at every threshold into ordered heavy lists (as
+// route.cu). Bit-identical to finalize + ds_curve_observe + ds_route.
+constexpr int kTailThreads = 160, kTailTotalTid = 128, kTailMax = 2048;
+__global__ void __launch_bounds__(kTailThreads)
+batch_tail_kernel(const float* __restrict__ part, int n, int tpi, int tokens, float hb,
+                  float* __restrict__ conf, ds_curve* __restrict__ curve, double decay,
+                  const double* __restrict__ thr, int nt, long long index_base,
+                  long long* __restrict__ heavy, long long* __restrict__ counts) {
+    __shared__ float sc[kTailMax];
+    __shared__ __align__(16) unsigned char sbin[kTailMax];
+    __shared__ int s_bad, wcnt[kTailThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_bad = n;
+    __syncthreads();
+    for (int i = tid; i < n; i += kTailThreads) {
+        const float c = image_score(part, i, tpi, tokens, hb, 0);
+        conf[i] = c;
+        sc[i] = c;
+        const double cd = static_cast<double>(c);
+        if (!(cd >= 0.0) || !(cd <= 1.0)) {
+            atomicMin(&s_bad, i);   // the reference throws here; the curve stops before it
+            sbin[i] = 255;
+        } else {
+            int b = static_cast<int>(floor(__dadd_rn(__dmul_rn(cd, 100.0), 1e-9)));
+            b = b < 0 ? 0 : (b > DS_CURVE_BINS - 1 ? DS_CURVE_BINS - 1 : b);
+            sbin[i] = static_cast<unsigned char>(b);
+        }
+    }
+    __syncthreads();
+    const int n_eff = s_bad;
+    const bool scale = decay != 1.0;
+    if (tid < DS_CURVE_BINS) {
+        double m = curve->bin_mass[tid];
+        for (int k = 0; k < n_eff; ++k) {
+            if (scale) m = __dmul_rn(m, decay);
+            if (sbin[k] == tid) m = __dadd_rn(m, 1.0);
+        }
+        curve->bin_mass[tid] = m;
+    } else if (tid == kTailTotalTid) {
+        double t = curve->total_mass;
+        for (int k = 0; k < n_eff; ++k) t = __dadd_rn(scale ? __dmul_rn(t, decay) : t, 1.0);
+        curve->total_mass = t;
+    }
+    for (int k = 0; k < nt; ++k) {
+        const double t = thr[k];
+        long long off = 0;
+        long long* out = heavy + static_cast<long long>(k) * n;
+        for (int base = 0; base < n; base += kTailThreads) {
+            const int i = base + tid;
+            const bool p = i < n && static_cast<double>(sc[i]) < t;
+            const unsigned bal = __ballot_sync(0xffffffffu, p);
+            __syncthreads();   // wcnt of the previous chunk consumed
+            if (lane == 0) wcnt[warp] = __popc(bal);
+            __syncthreads();
+            int before = 0, all = 0;
+#pragma unroll
+            for (int w = 0; w < kTailThreads / 32; ++w) {
+                before += w < warp ? wcnt[w] : 0;
+                all += wcnt[w];
+            }
+            if (p) out[off + before + __popc(bal & ((1u << lane) - 1u))] = index_base + i;
+            off += all;
+        }
+        if (tid == 0) counts[k] = off;
+    }
 }
 
 // ---- deterministic weights ---------------------------------------------------------
@@ -827,8 +904,19 @@ struct ds_disc {
 
 namespace {
 
+struct BatchTail {   // batch_tail_kernel arguments (ds_disc_batch_complete_device)
+    ds_curve* curve;
+    double decay;
+    const double* thr;
+    int nt;
+    long long index_base;
+    long long* heavy;
+    long long* counts;
+};
+
 ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w, float* out,
-                      int logits, cudaStream_t st, long long* trace = nullptr) {
+                      int logits, cudaStream_t st, long long* trace = nullptr,
+                      const BatchTail* tail = nullptr) {
     if (h % 16 || w % 16)
         return dsi::fail(DS_ERR_INVALID_ARGUMENT, "image height and width must be multiples of 16");
     const int tokens = (h / 16) * (w / 16);
@@ -871,9 +959,16 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     cfg.numAttrs = 1;
     DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, disc_kernel, p));
     DS_LAUNCH_CHECK(d->ctx, "disc_kernel");
-    finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
-        part, n, p.tiles_per_img, tokens, d->hb, logits, out);
-    DS_LAUNCH_CHECK(d->ctx, "finalize_kernel");
+    if (tail) {
+        batch_tail_kernel<<<1, kTailThreads, 0, st>>>(
+            part, static_cast<int>(n), p.tiles_per_img, tokens, d->hb, out, tail->curve, tail->decay,
+            tail->thr, tail->nt, tail->index_base, tail->heavy, tail->counts);
+        DS_LAUNCH_CHECK(d->ctx, "batch_tail_kernel");
+    } else {
+        finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+            part, n, p.tiles_per_img, tokens, d->hb, logits, out);
+        DS_LAUNCH_CHECK(d->ctx, "finalize_kernel");
+    }
     cudaFreeAsync(part, st);
     return DS_OK;
 }
@@ -993,6 +1088,41 @@ extern "C" ds_status ds_disc_score_device(ds_disc* d, const uint8_t* nhwc, int64
     if (!d || (n > 0 && (!nhwc || !conf))) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
     return launch_disc(d, nhwc, n, h, w, conf, 0, st);
+}
+
+// One light batch, cluster.cpp:288-307: score, observe in batch order, defer.
+// Batches of <= 2048 images take the discriminator plus ONE fused tail launch;
+// larger ones run the three stages as their own entry points (same results).
+extern "C" ds_status ds_disc_batch_complete_device(ds_disc* d, const uint8_t* nhwc, int64_t n,
+                                                   int32_t h, int32_t w, float* conf,
+                                                   ds_curve* curve, double decay,
+                                                   const double* thresholds, int32_t nt,
+                                                   int64_t index_base, int64_t* heavy_idx,
+                                                   int64_t* counts, void* stream) {
+    if (!d || !curve || (n > 0 && (!nhwc || !conf)) || (nt > 0 && (!thresholds || !counts)) ||
+        (nt > 0 && n > 0 && !heavy_idx) || nt < 0)
+        return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (!(decay > 0.0) || !(decay <= 1.0))
+        return dsi::fail(DS_ERR_DOMAIN, "curve decay must lie in (0, 1]");
+    if (n <= 0) {
+        if (nt > 0) {
+            cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+            DS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int64_t) * nt, st));
+        }
+        return DS_OK;
+    }
+    if (n > kTailMax) {
+        ds_status s = ds_disc_score_device(d, nhwc, n, h, w, conf, stream);
+        if (s == DS_OK) s = ds_curve_observe_device(d->ctx, curve, conf, DS_CONF_F32, n, decay, stream);
+        if (s == DS_OK && nt > 0)
+            s = ds_route_device(d->ctx, conf, DS_CONF_F32, n, thresholds, nt, index_base, heavy_idx,
+                                counts, stream);
+        return s;
+    }
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+    BatchTail tail{curve, decay, thresholds, nt, static_cast<long long>(index_base),
+                   reinterpret_cast<long long*>(heavy_idx), reinterpret_cast<long long*>(counts)};
+    return launch_disc(d, nhwc, n, h, w, conf, 0, st, nullptr, &tail);
 }
 
 // Host-buffer entry: the image upload is pipelined with scoring -- chunks of

@@ -94,6 +94,8 @@ SIGNATURES = [
     ("ds_disc_export", ctypes.c_int, [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
     ("ds_disc_score", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p]),
     ("ds_disc_score_device", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p, c_p]),
+    ("ds_disc_batch_complete_device", ctypes.c_int,
+     [c_p, c_p, i64, i32, i32, c_p, c_p, f64, c_p, i32, i64, c_p, c_p, c_p]),
     ("ds_synth_images_device", ctypes.c_int, [c_p, u64, u64, i64, i32, i32, c_p, c_p]),
     ("ds_generate_arrivals", ctypes.c_int, [c_p, c_p, i32, f64, u64, i32, c_p, i64,
                                             ctypes.POINTER(i64)]),
@@ -344,3 +346,11 @@ class Discriminator:
                      stream: int = 0):
         check(lib().ds_disc_score_device(self.handle, c_p(images_ptr), n, h, w, c_p(conf_ptr),
                                          c_p(stream)))
+
+    def batch_complete_device(self, images_ptr: int, n: int, h: int, w: int, conf_ptr: int,
+                              curve_ptr: int, decay: float, thr_ptr: int, nt: int,
+                              index_base: int, heavy_ptr: int, counts_ptr: int, stream: int = 0):
+        """One light batch (cluster.cpp:288-307): score, observe in order, defer."""
+        check(lib().ds_disc_batch_complete_device(
+            self.handle, c_p(images_ptr), n, h, w, c_p(conf_ptr), c_p(curve_ptr), decay,
+            c_p(thr_ptr), nt, index_base, c_p(heavy_ptr), c_p(counts_ptr), c_p(stream)))

@@ -154,3 +154,56 @@ def test_disc_pair_tile_edges(disc, weights, n, h, w):
 
 def test_disc_empty_batch(disc):
     assert disc.score(np.zeros((0, 512, 512, 3), np.uint8)).shape == (0,)
+
+
+@pytest.mark.parametrize("n,h,w,nt", [(1, 512, 512, 1), (32, 512, 512, 1), (32, 512, 512, 3),
+                                      (75, 128, 256, 101), (2048, 128, 256, 2),
+                                      (2100, 128, 256, 2)])
+def test_batch_complete_equals_separate_calls(disc, n, h, w, nt):
+    """ds_disc_batch_complete_device (one light batch, cluster.cpp:288-307:
+    score, observe in batch order, defer) gives the bits of the three separate
+    entry points -- fused tail for <= 2048 images, the separate path above."""
+    import torch
+    from paper_2411_15381_b200 import abi, workloads
+    ctx = disc.ctx
+    L = native.lib()
+    imgs = torch.from_numpy(disc_oracle.synth_images(11, 3, n, h, w).reshape(-1)).cuda()
+    thr = torch.tensor(np.linspace(0.0, 1.0, nt) if nt > 1 else [0.5], dtype=torch.float64,
+                       device="cuda")
+    prior = workloads.uniform_prior()
+    prior["bin_mass"][7] = -0.0
+    outs = []
+    for fused in (False, True):
+        conf = torch.empty(n, dtype=torch.float32, device="cuda")
+        cur = torch.from_numpy(prior.reshape(1).view(np.uint8).copy()).cuda()
+        heavy = torch.full((nt * n,), -1, dtype=torch.int64, device="cuda")
+        cnt = torch.empty(nt, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        if fused:
+            disc.batch_complete_device(imgs.data_ptr(), n, h, w, conf.data_ptr(), cur.data_ptr(),
+                                       0.999, thr.data_ptr(), nt, 1000, heavy.data_ptr(),
+                                       cnt.data_ptr())
+        else:
+            disc.score_device(imgs.data_ptr(), n, h, w, conf.data_ptr())
+            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(cur.data_ptr()),
+                                                   native.c_p(conf.data_ptr()), abi.CONF_F32, n,
+                                                   0.999, native.c_p(0)))
+            native.check(L.ds_route_device(ctx.handle, native.c_p(conf.data_ptr()), abi.CONF_F32,
+                                           n, native.c_p(thr.data_ptr()), nt, 1000,
+                                           native.c_p(heavy.data_ptr()),
+                                           native.c_p(cnt.data_ptr()), native.c_p(0)))
+        torch.cuda.synchronize()
+        c = cnt.cpu().numpy()
+        hv = heavy.cpu().numpy().reshape(nt, n)
+        outs.append((conf.cpu().numpy(), cur.cpu().numpy().tobytes(), c,
+                     [hv[k, :c[k]] for k in range(nt)]))
+    (c0, cv0, n0, h0), (c1, cv1, n1, h1) = outs
+    assert np.array_equal(c0.view(np.uint32), c1.view(np.uint32))
+    assert cv0 == cv1
+    assert np.array_equal(n0, n1)
+    for a, b in zip(h0, h1):
+        assert np.array_equal(a, b)
+    # and the lists are the ordered ids of c < t
+    for k in range(nt):
+        t = thr.cpu().numpy()[k]
+        assert np.array_equal(h1[k], np.flatnonzero(c1.astype(np.float64) < t) + 1000)
