@@ -94,6 +94,9 @@ constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (
 #endif
 constexpr int kAWStages = DS_AW ? 2 : 0; // W2_0 stages 0-1 land in the A ring (idle from GEMM1's
                                         // end until GEMM2_0 has read them)
+#ifndef DS_E1_PIPE
+#define DS_E1_PIPE 0
+#endif
 #ifndef DS_E1_SPLIT
 #define DS_E1_SPLIT 192
 #endif
@@ -175,6 +178,21 @@ __device__ __forceinline__ void e1_columns(uint32_t tmem_lane, int c_lo, uint32_
                          pk[3]);
         }
     };
+#if DS_E1_PIPE
+    // software-pipelined: block g+1's TMEM load is in flight while block g is
+    // activated (two 32-register buffers, as many as the unpipelined form)
+    uint32_t va[32], vb[32];
+    tmem_ld_x32_async(tmem_lane + c_lo, va);
+    tmem_wait_ld32(va);
+#pragma unroll
+    for (int g = 0; g < kN32; ++g) {
+        uint32_t (&cur)[32] = (g & 1) ? vb : va;
+        uint32_t (&nxt)[32] = (g & 1) ? va : vb;
+        if (g + 1 < kN32) tmem_ld_x32_async(tmem_lane + c_lo + 32 * (g + 1), nxt);
+        emit(cur, c_lo + 32 * g);
+        if (g + 1 < kN32) tmem_wait_ld32(nxt);
+    }
+#else
 #pragma unroll 1
     for (int g = 0; g + 1 < kN32; g += 2) {
         uint32_t v0[32], v1[32];
@@ -189,6 +207,7 @@ __device__ __forceinline__ void e1_columns(uint32_t tmem_lane, int c_lo, uint32_
         tmem_ld_x32_sync(tmem_lane + c0, v);
         emit(v, c0);
     }
+#endif
 }
 
 struct Bars {
