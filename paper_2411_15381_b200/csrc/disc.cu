@@ -94,6 +94,9 @@ constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (
 #endif
 constexpr int kAWStages = DS_AW ? 2 : 0; // W2_0 stages 0-1 land in the A ring (idle from GEMM1's
                                         // end until GEMM2_0 has read them)
+#ifndef DS_EXP_NO_WSTREAM
+#define DS_EXP_NO_WSTREAM 0
+#endif
 #ifndef DS_E1_PIPE
 #define DS_E1_PIPE 0
 #endif
@@ -514,6 +517,15 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     if (t < 16) DS_TRACE(6, ptile, t);
                     // both CTAs load their N-half; completion lands on the leader's
                     // barrier, which expects the whole stage
+#if DS_EXP_NO_WSTREAM
+                    // ENERGY EXPERIMENT ONLY (wrong results): after the first tile the
+                    // ring keeps its stale weights instead of re-streaming them from L2
+                    if (ptile > 0) {
+                        if (leader) mbar_arrive(&B.b_full[bs]);
+                        if (++bs == kBStages) { bs = 0; bp ^= 1; }
+                        continue;
+                    }
+#endif
                     if (leader) mbar_arrive_expect_tx(&B.b_full[bs], kBStage);
                     tma_2d_pair(sbase + kBRing + bs * kBHalf, &P.wmap, 0,
                                 t * 256 + static_cast<int>(rank) * 128,
