@@ -288,3 +288,36 @@ def test_curve_domain_errors(ctx):
         ctx.curve_observe(c, np.array([0.3, 1.5, 0.2]), 1.0)
     with pytest.raises(DomainError):
         ctx.curve_observe(c, np.array([0.3]), 0.0)
+
+
+def test_curve_segmented_replay_in_cuda_graph(ctx):
+    """The segmented replay (a cooperative launch) captured into a CUDA graph
+    and replayed gives the eager bits (scratch sized by an eager call first)."""
+    import torch
+    from paper_2411_15381_b200 import native
+    conf = ctx.score_latent(workloads.query_model(), 0, 200_000)
+    prior = workloads.uniform_prior()
+    dconf = torch.from_numpy(conf).cuda()
+    p_t = torch.from_numpy(prior.reshape(1).view(np.uint8).copy()).cuda()
+    cur = torch.empty_like(p_t)
+    s = torch.cuda.Stream()
+    L = native.lib()
+
+    def call():
+        cur.copy_(p_t)
+        native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(cur.data_ptr()),
+                                               native.c_p(dconf.data_ptr()), abi.CONF_F64,
+                                               len(conf), 0.999, native.c_p(s.cuda_stream)))
+    with torch.cuda.stream(s):
+        call()
+    torch.cuda.synchronize()
+    eager = cur.cpu().numpy().tobytes()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        call()
+    cur.zero_()
+    with torch.cuda.stream(s):
+        g.replay()
+    torch.cuda.synchronize()
+    assert cur.cpu().numpy().tobytes() == eager
+    _assert_same_bits(cur.cpu().numpy().view(abi.CURVE)[0], _port_curve(prior, conf, 0.999))
