@@ -94,6 +94,10 @@ constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (
 #endif
 constexpr int kAWStages = DS_AW ? 2 : 0; // W2_0 stages 0-1 land in the A ring (idle from GEMM1's
                                         // end until GEMM2_0 has read them)
+#ifndef DS_G33_IL
+#define DS_G33_IL 0   // >0: the previous tile's GEMM3_3 K-chunk q is issued after GEMM1 chunk DS_G33_IL + q
+#endif
+constexpr int kG33Il = DS_G33_IL;
 #ifndef DS_EXP_FAST_E1
 #define DS_EXP_FAST_E1 0
 #endif
@@ -545,8 +549,18 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             const int W1 = 0, W2 = kW1Stages, W3 = kW1Stages + 4 * kWChunkStages;
             for (long long tile = 0; tile < my_tiles; ++tile) {
                 ptile = tile;
-                put(W1 + kXStages, kW1Stages - kXStages);
-                if (tile > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
+                if (kG33Il > 0 && tile > 0) {
+                    // the MMA issuer's order: W1 stages 4-5 after GEMM1 chunks 4-5,
+                    // GEMM3_3(tile-1) K-chunk q after GEMM1 chunk kG33Il + q
+                    for (int c = 0; c < kW1Stages; ++c) {
+                        if (c >= kXStages) put(W1 + c, 1);
+                        const int q = c - kG33Il;
+                        if (q >= 0 && q < kWChunkStages) put(W3 + 3 * kWChunkStages + q, 1);
+                    }
+                } else {
+                    put(W1 + kXStages, kW1Stages - kXStages);
+                    if (tile > 0) put(W3 + 3 * kWChunkStages, kWChunkStages);
+                }
                 put(W2 + kAWStages, kWChunkStages - kAWStages);
                 for (int j = 1; j < 4; ++j) {
                     put(W2 + j * kWChunkStages, kWChunkStages);
@@ -645,10 +659,26 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     if (c >= kXStages) release_b();
                     umma_commit_pair(&B.a_empty[as], 0x3);
                     if (++as == kAStages) { as = 0; ap ^= 1; }
+                    if (c == kChunksPerTile - 1) umma_commit_pair(&B.acc12_full, 0x3);
+                    // GEMM3_3 of the previous tile between GEMM1 chunks: tensor work
+                    // while the next A chunk makes its round trip
+                    const int q = c - kG33Il;
+                    if (kG33Il > 0 && tile > 0 && q >= 0 && q < kWChunkStages) {
+                        if (q == 0) wait_bar(&B.h2_ready, prd);
+                        const uint64_t ad3 = desc_k_sw128(sbase + kR2 + q * kAChunk);
+                        const uint64_t bd3 = next_b();
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            umma_bf16_pair(acc3, ad3 + 2 * k, bd3 + 2 * k, kIdescF16, 1u);
+                        release_b();
+                        if (q == kWChunkStages - 1) {
+                            umma_commit_pair(&B.h2_free, 0x3);
+                            umma_commit_pair(&B.acc3_full, 0x3);
+                        }
+                    }
                 }
-                umma_commit_pair(&B.acc12_full, 0x3);
                 DS_TRACE(2, tile, 1);
-                if (tile > 0) {                      // G3_3 of the previous tile
+                if (kG33Il == 0 && tile > 0) {       // G3_3 of the previous tile
                     wait_bar(&B.h2_ready, prd);
                     gemm(sbase + kR2, 4, acc3, true);
                     umma_commit_pair(&B.h2_free, 0x3);
