@@ -94,6 +94,10 @@ constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (
 #endif
 constexpr int kAWStages = DS_AW ? 2 : 0; // W2_0 stages 0-1 land in the A ring (idle from GEMM1's
                                         // end until GEMM2_0 has read them)
+#ifndef DS_WARP_ARRIVE
+#define DS_WARP_ARRIVE 0   // 1: role groups signal the leader's barriers with one arrive per warp
+#endif
+constexpr bool kWarpArrive = DS_WARP_ARRIVE != 0;
 #ifndef DS_G33_IL
 #define DS_G33_IL 0   // >0: the previous tile's GEMM3_3 K-chunk q is issued after GEMM1 chunk DS_G33_IL + q
 #endif
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         // weight-stage barriers get both halves' bytes through cta_group::2 TMA.
         const uint32_t peer = leader ? 1u : 0u;
         for (int s = 0; s < kAStages; ++s) {
-            mbar_init(&B.a_full[s], 128 + peer);
+            mbar_init(&B.a_full[s], kWarpArrive ? 4 + 4 * peer : 128 + peer);
             mbar_init(&B.a_empty[s], 1);
         }
         for (int s = 0; s < kBStages; ++s) {
@@ -270,14 +274,14 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             mbar_init(&B.b_empty[s], 1);
         }
         mbar_init(&B.acc12_full, 1);
-        mbar_init(&B.drained, 256 + peer);
-        mbar_init(&B.h2_ready, 256 + peer);
+        mbar_init(&B.drained, kWarpArrive ? 8 + 8 * peer : 256 + peer);
+        mbar_init(&B.h2_ready, kWarpArrive ? 8 + 8 * peer : 256 + peer);
         mbar_init(&B.h2_free, 1);
         mbar_init(&B.acc3_full, 1);
-        mbar_init(&B.acc3_empty, 256 + peer);
+        mbar_init(&B.acc3_empty, kWarpArrive ? 8 + 8 * peer : 256 + peer);
         for (int s = 0; s < kXStages; ++s) mbar_init(&B.x_full[s], 1);
         mbar_init(&B.r1_free, 1);
-        mbar_init(&B.e1b_done, 128 + peer);
+        mbar_init(&B.e1b_done, kWarpArrive ? 4 + 4 * peer : 128 + peer);
         for (int s = 0; s < 2; ++s) mbar_init(&B.aw_full[s], 1);
         mbar_init(&B.aw_free, 1);
         fence_mbar_init();
@@ -293,7 +297,18 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     // locally; the peer's group syncs on a named barrier and one thread
     // forwards a single cluster-scope arrive.
     auto group_signal = [&](uint64_t* bar, uint32_t bar_id, uint32_t threads, bool first) {
-        if (leader) {
+        if (kWarpArrive) {
+            // one arrive per warp after __syncwarp (which orders the lanes'
+            // writes before lane 0's release arrive); the peer's go remote
+            __syncwarp();
+            if (lane == 0) {
+                if (leader) mbar_arrive(bar);
+                else mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+            }
+            (void)bar_id;
+            (void)threads;
+            (void)first;
+        } else if (leader) {
             mbar_arrive(bar);
         } else {
             named_bar_sync(bar_id, threads);
