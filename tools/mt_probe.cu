@@ -114,6 +114,85 @@ __global__ void __launch_bounds__(32) mt_b(uint64_t seed, int64_t n, uint64_t* r
     }
 }
 
+// (C) 160 threads, FOUR steps per barrier: thread t computes column t of
+// steps s+2..s+5 from the last two steps (A = step s, B = step s+1, shared),
+// recomputing the few neighbour words (column t+1 of steps s+2/s+3, column 0 of
+// the next step for t >= 154) it needs instead of waiting for their owners.
+template <int kStore>
+__global__ void __launch_bounds__(160) mt_c(uint64_t seed, int64_t n, uint64_t* raw) {
+    __shared__ uint64_t buf[2][2][156];   // [set][A/B][column]
+    __shared__ __align__(16) uint64_t stage[2][624];
+    const int t = threadIdx.x;
+    if (t == 0) {
+        uint64_t x = seed;
+        buf[0][0][0] = x;
+        for (int i = 1; i < 312; ++i) {
+            x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
+            buf[0][i / 156][i % 156] = x;
+        }
+    }
+    __syncthreads();
+    const int64_t steps = (n + 155) / 156;
+    int set = 0;
+    for (int64_t s = 0; s < steps; s += 4) {
+        const uint64_t* A = buf[set][0];
+        const uint64_t* B = buf[set][1];
+        if (t < 156) {
+            auto w2 = [&](int c) { return B[c] ^ mt_mix(A[c], c < 155 ? A[c + 1] : B[0]); };
+            const uint64_t w2_0 = (t >= 154) ? w2(0) : 0;
+            auto w3 = [&](int c, uint64_t w2c) {
+                return w2c ^ mt_mix(B[c], c < 155 ? B[c + 1] : w2_0);
+            };
+            const uint64_t W2 = w2(t);
+            const uint64_t W3 = w3(t, W2);
+            uint64_t n2, n3;   // column t+1 (or the next step's column 0) of steps s+2, s+3
+            if (t < 155) {
+                n2 = w2(t + 1);
+                n3 = w3(t + 1, n2);
+            } else {
+                n2 = w3(0, w2_0);                                  // W3(0)
+                const uint64_t w2_1 = w2(1);
+                n3 = n2 ^ mt_mix(w2_0, w2_1);                      // W4(0)
+            }
+            const uint64_t W4 = W3 ^ mt_mix(W2, n2);
+            const uint64_t W5 = W4 ^ mt_mix(W3, n3);
+            const int64_t k0 = s * 156 + t;
+            if (kStore == 0) {
+                if (k0 < n) raw[k0] = W2;
+                if (k0 + 156 < n) raw[k0 + 156] = W3;
+                if (k0 + 312 < n) raw[k0 + 312] = W4;
+                if (k0 + 468 < n) raw[k0 + 468] = W5;
+            } else if (kStore == 1) {
+                if ((k0 & 63) == 0 && k0 < n) raw[k0] = W2 ^ W3 ^ W4 ^ W5;
+            } else {
+                stage[set][t] = W2;
+                stage[set][t + 156] = W3;
+                stage[set][t + 312] = W4;
+                stage[set][t + 468] = W5;
+            }
+            buf[set ^ 1][0][t] = W4;
+            buf[set ^ 1][1][t] = W5;
+        }
+        if (kStore == 2) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncthreads();
+        if (kStore == 2 && t == 0) {
+            const int64_t first = s * 156;
+            const int64_t cnt = n - first < 624 ? n - first : 624;
+            if (cnt > 0) {
+                const uint32_t src = static_cast<uint32_t>(__cvta_generic_to_shared(&stage[set][0]));
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                             :: "l"(raw + first), "r"(src), "r"(static_cast<uint32_t>(cnt * 8)) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+        }
+        set ^= 1;
+    }
+    if (kStore == 2 && t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
     const int64_t n = 1000000;
     const uint64_t seed = 0x1234567887654321ULL;
@@ -151,6 +230,9 @@ int main() {
                cudaGetErrorString(cudaGetLastError()));
     };
     run("A 160 threads, ring", [&] { mt_a<<<1, 160>>>(seed, n, d); });
+    run("C 160 threads, 4 steps/barrier", [&] { mt_c<0><<<1, 160>>>(seed, n, d); });
+    run("C, stores off (compute only)", [&] { mt_c<1><<<1, 160>>>(seed, n, d); });
+    run("C, bulk stores from smem", [&] { mt_c<2><<<1, 160>>>(seed, n, d); });
     run("B one warp, direct stores", [&] { mt_b<0><<<1, 32>>>(seed, n, d); });
     run("B one warp, staged x4", [&] { mt_b<4><<<1, 32>>>(seed, n, d); });
     run("B one warp, staged x8", [&] { mt_b<8><<<1, 32>>>(seed, n, d); });
