@@ -209,7 +209,7 @@ def cpu_planner_leg(problems, cascades, grid, offs, threads):
                                   threads)
         kind = "port"
     dt = time.perf_counter() - t0
-    return len(problems) * CANDS_PER_PROBLEM / dt, kind, out
+    return len(problems) * CANDS_PER_PROBLEM / dt, kind, out, dt
 
 
 def cpu_latent_leg(n, threads):
@@ -260,9 +260,9 @@ def cpu_workload_leg(threads):
     return n / (t_arr + t_q), n / t_arr, ("reference" if use_ref else "port"), a
 
 
-def csv_records(n):
+def csv_records(n, seed=12):
     from tests import helpers
-    return helpers.random_query_records(np.random.default_rng(12), n)
+    return helpers.random_query_records(np.random.default_rng(seed), n)
 
 
 def cpu_csv_leg(records):
@@ -302,37 +302,28 @@ def host_weights():
 
 
 def planner_inputs():
-    from paper_2411_15381_b200 import abi, workloads
-    from oracle import lib  # noqa: F401  (curve via port below)
-    cas = np.zeros(3, abi.CASCADE)
-    for i, name in enumerate(["cascade1", "cascade2", "cascade3"]):
-        light, heavy, slo = workloads.fitted_tables(name)
-        cas[i] = workloads.make_cascade(light, heavy, slo)
-    probs = []
-    per = N_PLAN // 12
-    for ci in range(3):
-        for s in (16, 32, 64, 128):
-            p = workloads.c2_problems(cas[ci], s, per, seed=7 + 100 * ci + s)
-            p["cascade"] = ci
-            probs.append(p)
-    pro = np.concatenate(probs)
-    grid = workloads.make_grid(0.01)
-    offs = np.array([0, len(grid)], np.int32)
-    return pro, cas, grid, offs
+    """BASELINE.md's planner batch: 4,096 acceptance-C2-recipe problems
+    (mt19937_64(7)) over the three fitted 32x32 cascades x S in {16..128},
+    grid k/100 -- generated by the reference itself (oracle/make_golden.py
+    gen_config4_bench) and committed as a fixture with the reference's plans;
+    the CPU arm times diffserve::solve on exactly these problems."""
+    g = dict(np.load(os.path.join(ROOT, "tests", "golden", "config4_bench.npz")))
+    return (g["problems"], g["cascades"].copy(), g["grid_values"], g["grid_offsets"],
+            g["want_solve"])
 
 
-def sampled_curves(cas):
-    """Each config-4 cascade's curve = from_samples of 5K sample_query
-    confidences; computed with the C restatement."""
-    from oracle import lib
+def product_curves(ctx, cas):
+    """Each planner cascade's deferral curve = DeferralCurve::from_samples of
+    the 5K sample_query confidences (cascade cfg, seed 1)
+    built by the PRODUCT: K4 scores, K3 replays at decay 1 from the empty
+    curve. Returns whether they equal the fixture's (reference-built) curves."""
     from paper_2411_15381_b200 import abi, workloads
-    m = workloads.query_model()
-    conf = np.zeros(5000)
-    lib.port().dso_sample_queries(abi.ptr(m), 0, 5000, abi.ptr(conf), None, 8)
+    conf = ctx.score_latent(workloads.query_model(), 0, 5000)
+    curve = ctx.curve_observe(np.zeros((), abi.CURVE), conf, 1.0)
+    same = all(cas[i]["deferral"].tobytes() == curve.tobytes() for i in range(len(cas)))
     for i in range(len(cas)):
-        c = np.zeros((), abi.CURVE)
-        lib.port().dso_curve_observe(abi.ptr(c), abi.ptr(conf), 5000, 1.0)
-        cas[i]["deferral"] = c
+        cas[i]["deferral"] = curve
+    return same
 
 
 def run_reference(args):
@@ -376,17 +367,20 @@ def run_gpu(args):
 
     ws, rank, local = dist_env()
     # Test hooks for the multi-rank path on a 1-GPU box: BENCH_DIST_BACKEND=gloo
-    # and BENCH_SHARE_DEVICE=1 run every rank on cuda:0 (the driver uses NCCL,
-    # one rank per GPU).
+    # and BENCH_SHARE_DEVICE=1 run every rank on cuda:0 with the library's host
+    # transport (NCCL refuses two ranks on one device). The driver uses NCCL,
+    # one rank per GPU.
     backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     if os.environ.get("BENCH_SHARE_DEVICE") == "1":
         local = 0
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if ws > 1:
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+
     def allmax(vals):
         """Max over ranks (the contract: timings are the max over ranks)."""
         t = torch.tensor(vals, dtype=torch.float64)
@@ -395,60 +389,85 @@ def run_gpu(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return [float(x) for x in t.cpu()]
 
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
     ctx = native.Context(local)
     L = native.lib()
     stream = torch.cuda.ExternalStream(ctx.stream)
+    sp = native.c_p(ctx.stream)
     disc = native.Discriminator(ctx, WEIGHT_SEED)
-    if rank == 0:
-        # cache the exported weights so the CPU reference arm uses the same network
-        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    dev = torch.device("cuda", local)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    # The sharded hot path's collectives (include/ds_gpu.h "multi-GPU"): NCCL
+    # from the library itself, one communicator per rank
+    comm = None
+    if ws > 1:
+        comm = (ddist.nccl_comm(ctx) if backend == "nccl"
+                else native.Comm.host(ctx, ws, rank, ddist.TorchHostOps()))
 
     # ---- inputs resident in HBM ---------------------------------------------
     id0 = rank * N_IMG
+    NTOT = ws * N_IMG
     images = torch.empty(N_IMG * H * W * 3, dtype=torch.uint8, device=dev)
     native.check(L.ds_synth_images_device(ctx.handle, IMG_SEED, id0, N_IMG, H, W,
-                                          native.c_p(images.data_ptr()), native.c_p(ctx.stream)))
-    grid_t = torch.tensor(workloads.make_grid(0.01), dtype=torch.float64, device=dev)
+                                          native.c_p(images.data_ptr()), sp))
+    grid_np = workloads.make_grid(0.01)
+    grid_t = torch.tensor(grid_np, dtype=torch.float64, device=dev)
     NT = grid_t.numel()
     conf = torch.empty(N_IMG, dtype=torch.float32, device=dev)
     heavy = torch.empty(NT * N_IMG, dtype=torch.int64, device=dev)
     counts = torch.empty(NT, dtype=torch.int64, device=dev)
-    prior = np.zeros((), abi.CURVE)
-    from oracle import lib as _olib  # prior curve = from_samples(shipped samples)
-    s = np.asarray(workloads.SHIPPED_PRIOR_SAMPLES, np.float64)
-    _olib.port().dso_curve_observe(abi.ptr(prior), abi.ptr(s), len(s), 1.0)
+    offs = torch.empty(NT, dtype=torch.int64, device=dev)
+    totals = torch.empty(NT, dtype=torch.int64, device=dev)
+    # global heavy queues (rank 0, the load balancer's side) at N > 1
+    gq = torch.empty(NT * NTOT if (ws > 1 and rank == 0) else 1, dtype=torch.int64, device=dev)
+    gc = torch.empty(NT, dtype=torch.int64, device=dev)
+    # prior = DeferralCurve::from_samples(shipped samples) (cascades.profiles:20)
+    # through the product's K3 (observe at decay 1 from the empty curve)
+    prior = ctx.curve_observe(np.zeros((), abi.CURVE),
+                              np.asarray(workloads.SHIPPED_PRIOR_SAMPLES, np.float64), 1.0)
     prior_t = torch.from_numpy(prior.reshape(1).view(np.uint8).copy()).to(dev)
     curve_t = torch.empty_like(prior_t)
+    torch.cuda.synchronize()
 
     def step(ev=None):
         with torch.cuda.stream(stream):
             if ev is not None:
                 ev[0].record(stream)
             native.check(L.ds_disc_score_device(disc.handle, native.c_p(images.data_ptr()),
-                                                N_IMG, H, W, native.c_p(conf.data_ptr()),
-                                                native.c_p(ctx.stream)))
+                                                N_IMG, H, W, native.c_p(conf.data_ptr()), sp))
             if ev is not None:
                 ev[1].record(stream)
-            native.check(L.ds_route_device(ctx.handle, native.c_p(conf.data_ptr()), abi.CONF_F32,
-                                           N_IMG, native.c_p(grid_t.data_ptr()), NT, id0,
-                                           native.c_p(heavy.data_ptr()),
-                                           native.c_p(counts.data_ptr()), native.c_p(ctx.stream)))
             curve_t.copy_(prior_t)
-            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve_t.data_ptr()),
-                                                   native.c_p(conf.data_ptr()), abi.CONF_F32,
-                                                   N_IMG, DECAY, native.c_p(ctx.stream)))
-            if ws > 1:
-                # routed-count all-gather + exclusive scan over ranks: this
-                # rank's offset inside each of the 101 global heavy queues
-                ddist.global_offsets_device(counts)
+            if comm is None:
+                native.check(L.ds_route_device(ctx.handle, native.c_p(conf.data_ptr()),
+                                               abi.CONF_F32, N_IMG, native.c_p(grid_t.data_ptr()),
+                                               NT, id0, native.c_p(heavy.data_ptr()),
+                                               native.c_p(counts.data_ptr()), sp))
+                native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve_t.data_ptr()),
+                                                       native.c_p(conf.data_ptr()), abi.CONF_F32,
+                                                       N_IMG, DECAY, sp))
+            else:
+                # route this shard + routed-count all-gather (each rank's
+                # offset in every global queue), the ordered ids of every rank
+                # assembled into the 101 global heavy queues at rank 0, and the
+                # curve replayed over the GLOBAL id-ordered sequence on every
+                # rank (cluster.cpp:288-307 order)
+                comm.route(conf.data_ptr(), abi.CONF_F32, N_IMG, grid_t.data_ptr(), NT, id0,
+                           heavy.data_ptr(), counts.data_ptr(), offs.data_ptr(),
+                           totals.data_ptr(), stream=ctx.stream)
+                comm.gather_queues(0, heavy.data_ptr(), N_IMG, counts.data_ptr(), NT,
+                                   gq.data_ptr() if rank == 0 else 0, NTOT,
+                                   gc.data_ptr() if rank == 0 else 0, stream=ctx.stream)
+                comm.curve_observe(curve_t.data_ptr(), conf.data_ptr(), abi.CONF_F32,
+                                   [N_IMG] * ws, DECAY, stream=ctx.stream)
 
     # ---- warmup + timed region -------------------------------------------------
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -463,8 +482,7 @@ def run_gpu(args):
     t_end.record(stream)
     torch.cuda.synchronize()
     launches = ctx.launches() - n0
-    if ws > 1:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
     total_ms = t_start.elapsed_time(t_end)
@@ -473,24 +491,64 @@ def run_gpu(args):
     ms_per_step = total_ms / args.steps
     value = ws * N_IMG / (ms_per_step / 1000.0)
 
-    # ---- parity spot-check inside the benchmark: route vs confidences -------
+    # ---- parity inside the benchmark -------------------------------------------
+    # (1) this rank's routing vs its confidences (numpy)
     c_host = conf.cpu().numpy().astype(np.float64)
     cnt_host = counts.cpu().numpy()
-    want_cnt = np.array([(c_host < t).sum() for t in workloads.make_grid(0.01)])
+    want_cnt = np.array([(c_host < t).sum() for t in grid_np])
     parity_ok = bool(np.array_equal(cnt_host, want_cnt))
-    # K2 lists at t = 0.5 (grid index 50): the ordered ids of c < t, exactly
     heavy50 = heavy[50 * N_IMG: 50 * N_IMG + int(cnt_host[50])].cpu().numpy()
     lists_ok = bool(np.array_equal(heavy50, np.flatnonzero(c_host < 0.5) + id0))
-    # K3 curve after the step vs the C restatement on the same confidences, bit for bit
-    cw = prior.copy()
-    _olib.port().dso_curve_observe(abi.ptr(cw), abi.ptr(c_host), len(c_host), DECAY)
-    curve_ok = curve_t.cpu().numpy().tobytes() == cw.tobytes()
+    # (2) N ranks == 1 GPU: rank 0 redoes the whole world's work on one GPU
+    # (every rank's images scored here, routed in one call, one curve replay)
+    # and compares the global queues, counts and curve bits
+    parity_n1 = {}
+    conf_all = None
+    if rank == 0:
+        conf_all = torch.empty(NTOT, dtype=torch.float32, device=dev)
+        scratch_imgs = images if ws == 1 else torch.empty_like(images)
+        with torch.cuda.stream(stream):
+            for q in range(ws):
+                if ws > 1:
+                    native.check(L.ds_synth_images_device(
+                        ctx.handle, IMG_SEED, q * N_IMG, N_IMG, H, W,
+                        native.c_p(scratch_imgs.data_ptr()), sp))
+                native.check(L.ds_disc_score_device(
+                    disc.handle, native.c_p(scratch_imgs.data_ptr()), N_IMG, H, W,
+                    native.c_p(conf_all.data_ptr() + 4 * q * N_IMG), sp))
+            h1 = torch.empty(NT * NTOT, dtype=torch.int64, device=dev)
+            c1 = torch.empty(NT, dtype=torch.int64, device=dev)
+            native.check(L.ds_route_device(ctx.handle, native.c_p(conf_all.data_ptr()),
+                                           abi.CONF_F32, NTOT, native.c_p(grid_t.data_ptr()), NT,
+                                           0, native.c_p(h1.data_ptr()), native.c_p(c1.data_ptr()),
+                                           sp))
+            cur1 = prior_t.clone()
+            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(cur1.data_ptr()),
+                                                   native.c_p(conf_all.data_ptr()), abi.CONF_F32,
+                                                   NTOT, DECAY, sp))
+        torch.cuda.synchronize()
+        del scratch_imgs
+        g_cnt = (gc if ws > 1 else counts).cpu().numpy()
+        g_q = (gq if ws > 1 else heavy).cpu().numpy().reshape(NT, NTOT)
+        w_cnt = c1.cpu().numpy()
+        w_q = h1.cpu().numpy().reshape(NT, NTOT)
+        parity_n1 = {
+            "global_counts_equal_n1": bool(np.array_equal(g_cnt, w_cnt)),
+            "global_queues_equal_n1": bool(np.array_equal(g_cnt, w_cnt) and all(
+                np.array_equal(g_q[k, :w_cnt[k]], w_q[k, :w_cnt[k]]) for k in range(NT))),
+            "global_curve_bits_equal_n1": curve_t.cpu().numpy().tobytes() ==
+            cur1.cpu().numpy().tobytes(),
+            "confidences_equal_n1": bool(torch.equal(conf_all[:N_IMG], conf)),
+        }
+        del h1
+    step_curve = curve_t.cpu().numpy().view(abi.CURVE)[0].copy()
+    take_err = ctx.take_error()   # no invalid confidence met by any device call
+    barrier()
 
     # ---- e2e: the C-ABI calls with HOST buffers, copies inside the timed region
     pinned = torch.empty(N_IMG * H * W * 3, dtype=torch.uint8, pin_memory=True)
     pinned.copy_(images)
     host_imgs = pinned.numpy().reshape(N_IMG, H, W, 3)
-    grid_np = workloads.make_grid(0.01)
     e2e_steps = max(2, min(args.steps, 5))
 
     def e2e_step():
@@ -500,8 +558,7 @@ def run_gpu(args):
         return c, cnts
 
     e2e_step()
-    if ws > 1:
-        dist.barrier()
+    barrier()
     t0 = time.perf_counter()
     d2h = 0
     for _ in range(e2e_steps):
@@ -523,6 +580,7 @@ def run_gpu(args):
         pin_ms.append(a_.elapsed_time(b_))
     h2d_gbs = pinned.numel() / (min(pin_ms) / 1000.0) / 1e9
     e2e_gbs = N_IMG * H * W * 3 * (e2e_value / ws) / N_IMG / 1e9
+    del pinned, host_imgs
 
     # ---- image legs for the other configs ------------------------
     def timed(fn, reps):
@@ -535,15 +593,19 @@ def run_gpu(args):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
-    # config 5 (scale-out): 1M queries over the world, contiguous id shards of
-    # 1M/N per GPU scored in 5K chunks from the resident pool, routed at t = 0.5
-    # with global ids, then the routed-count all-gather -> global offsets
-    n5 = N_SCALE // ws
-    id5 = rank * n5
+    # config 5 (scale-out): 1M queries over the world, contiguous id shards
+    # scored in 5K chunks from each rank's resident pool (query i of rank q
+    # uses pool image (i - lo_q) mod 5K), routed at t = 0.5 with global ids;
+    # at N > 1 the routed-count all-gather and the global queue at rank 0
+    lo5, hi5 = ddist.shard_range(N_SCALE, ws, rank)
+    n5 = hi5 - lo5
     conf5 = torch.empty(n5, dtype=torch.float32, device=dev)
     heavy5 = torch.empty(n5, dtype=torch.int64, device=dev)
     count5 = torch.empty(1, dtype=torch.int64, device=dev)
     thr5 = torch.tensor([0.5], dtype=torch.float64, device=dev)
+    gq5 = torch.empty(N_SCALE if (ws > 1 and rank == 0) else 1, dtype=torch.int64, device=dev)
+    gc5 = torch.empty(1, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize()
 
     def scale_step():
         with torch.cuda.stream(stream):
@@ -551,42 +613,61 @@ def run_gpu(args):
                 m = min(N_IMG, n5 - off)
                 native.check(L.ds_disc_score_device(
                     disc.handle, native.c_p(images.data_ptr()), m, H, W,
-                    native.c_p(conf5.data_ptr() + 4 * off), native.c_p(ctx.stream)))
-            native.check(L.ds_route_device(ctx.handle, native.c_p(conf5.data_ptr()), abi.CONF_F32,
-                                           n5, native.c_p(thr5.data_ptr()), 1, id5,
-                                           native.c_p(heavy5.data_ptr()),
-                                           native.c_p(count5.data_ptr()), native.c_p(ctx.stream)))
-            if ws > 1:
-                ddist.global_offsets_device(count5)
+                    native.c_p(conf5.data_ptr() + 4 * off), sp))
+            if comm is None:
+                native.check(L.ds_route_device(ctx.handle, native.c_p(conf5.data_ptr()),
+                                               abi.CONF_F32, n5, native.c_p(thr5.data_ptr()), 1,
+                                               lo5, native.c_p(heavy5.data_ptr()),
+                                               native.c_p(count5.data_ptr()), sp))
+            else:
+                comm.route(conf5.data_ptr(), abi.CONF_F32, n5, thr5.data_ptr(), 1, lo5,
+                           heavy5.data_ptr(), count5.data_ptr(), stream=ctx.stream)
+                comm.gather_queues(0, heavy5.data_ptr(), n5, count5.data_ptr(), 1,
+                                   gq5.data_ptr() if rank == 0 else 0, N_SCALE,
+                                   gc5.data_ptr() if rank == 0 else 0, stream=ctx.stream)
     scale_step()
     torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
+    barrier()
     scale_ms = allmax([timed(scale_step, 1)])[0]
     scale_value = N_SCALE / (scale_ms / 1000.0)
-    scale_routed = int(count5.item())
+    if rank == 0:
+        # the 1M-query global queue vs one GPU's: pool confidences of every
+        # rank (conf_all above), expanded over each rank's id range
+        ca = conf_all.cpu().numpy().astype(np.float64)
+        want = []
+        for q in range(ws):
+            qlo, qhi = ddist.shard_range(N_SCALE, ws, q)
+            i = np.arange(qlo, qhi, dtype=np.int64)
+            want.append(i[ca[q * N_IMG + (i - qlo) % N_IMG] < 0.5])
+        want = np.concatenate(want)
+        got_n = int((gc5 if ws > 1 else count5).item())
+        got = (gq5 if ws > 1 else heavy5)[:got_n].cpu().numpy()
+        parity_n1["config5_global_queue_equal_n1"] = bool(
+            got_n == len(want) and np.array_equal(got, want))
+        scale_routed = got_n
+        del conf_all
+    del conf5, heavy5, gq5
 
     # config 1 (cascade 1): the same pool in light batches of 32 -- per batch:
     # score, observe the 32 confidences into the curve, route at the plan's
-    # threshold (cluster.cpp:288-307 order)
+    # threshold (cluster.cpp:288-307 order); independent per rank (each rank
+    # serves its own light batches)
     B1 = 32
     conf1 = torch.empty(N_IMG, dtype=torch.float32, device=dev)
     heavy1 = torch.empty(B1, dtype=torch.int64, device=dev)
     count1 = torch.empty(1, dtype=torch.int64, device=dev)
     curve1 = torch.empty_like(prior_t)
 
-    def batch32_step(sp=None):
-        sp = native.c_p(ctx.stream) if sp is None else sp
+    def batch32_step(spp=None):
+        spp = sp if spp is None else spp
         curve1.copy_(prior_t)
         for off in range(0, N_IMG, B1):
-            # one light batch (cluster.cpp:288-307): score, observe, defer --
-            # the discriminator plus one fused tail launch
             m = min(B1, N_IMG - off)
             native.check(L.ds_disc_batch_complete_device(
                 disc.handle, native.c_p(images.data_ptr() + off * H * W * 3), m, H, W,
                 native.c_p(conf1.data_ptr() + 4 * off), native.c_p(curve1.data_ptr()), DECAY,
                 native.c_p(thr5.data_ptr()), 1, id0 + off, native.c_p(heavy1.data_ptr()),
-                native.c_p(count1.data_ptr()), sp))
+                native.c_p(count1.data_ptr()), spp))
 
     def batch32_eager():
         with torch.cuda.stream(stream):
@@ -626,22 +707,21 @@ def run_gpu(args):
     N3, H3 = N_IMG, 1024
     images3 = torch.empty(N3 * H3 * H3 * 3, dtype=torch.uint8, device=dev)
     native.check(L.ds_synth_images_device(ctx.handle, 3, id0, N3, H3, H3,
-                                          native.c_p(images3.data_ptr()), native.c_p(ctx.stream)))
+                                          native.c_p(images3.data_ptr()), sp))
     conf3 = torch.empty(N3, dtype=torch.float32, device=dev)
 
     def c3_step():
         with torch.cuda.stream(stream):
             native.check(L.ds_disc_score_device(disc.handle, native.c_p(images3.data_ptr()), N3,
-                                                H3, H3, native.c_p(conf3.data_ptr()),
-                                                native.c_p(ctx.stream)))
+                                                H3, H3, native.c_p(conf3.data_ptr()), sp))
             native.check(L.ds_route_device(ctx.handle, native.c_p(conf3.data_ptr()), abi.CONF_F32,
                                            N3, native.c_p(grid_t.data_ptr()), NT, id0,
                                            native.c_p(heavy.data_ptr()),
-                                           native.c_p(counts.data_ptr()), native.c_p(ctx.stream)))
+                                           native.c_p(counts.data_ptr()), sp))
             curve_t.copy_(prior_t)
             native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(curve_t.data_ptr()),
                                                    native.c_p(conf3.data_ptr()), abi.CONF_F32,
-                                                   N3, DECAY, native.c_p(ctx.stream)))
+                                                   N3, DECAY, sp))
     c3_step()
     torch.cuda.synchronize()
     c3_ms = allmax([timed(c3_step, 3)])[0]
@@ -649,24 +729,37 @@ def run_gpu(args):
     c3_tflops = N3 * DISC_FLOP_BF16_EQ * 4 / (c3_ms / 1000.0) / 1e12
     del images3
 
-    # ---- planner leg (config 4) -------------------------------------------------
-    pro, cas, grid, offs = planner_inputs()
-    sampled_curves(cas)
+    # ---- planner leg (config 4): BASELINE.md's 4,096-problem batch -------------
+    # problem-sharded over the ranks (contiguous index ranges), plans gathered
+    # at rank 0 (the controller) at N > 1
+    pro, cas, grid, goffs, want_plans = planner_inputs()
+    curves_ok = product_curves(ctx, cas)
+    P_ALL = len(pro)
+    plo, phi = ddist.shard_range(P_ALL, ws, rank)
     d_pro = torch.from_numpy(pro.view(np.uint8).copy()).to(dev)
     d_cas = torch.from_numpy(cas.view(np.uint8).copy()).to(dev)
     d_grid = torch.from_numpy(grid.copy()).to(dev)
-    d_offs = torch.from_numpy(offs.copy()).to(dev)
-    d_out = torch.empty(len(pro) * abi.PLAN.itemsize, dtype=torch.uint8, device=dev)
+    d_offs = torch.from_numpy(goffs.copy()).to(dev)
+    PB = abi.PLAN.itemsize
+    d_out = torch.empty(max(phi - plo, 1) * PB, dtype=torch.uint8, device=dev)
+    d_all = torch.empty(P_ALL * PB, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
 
     def plan_step():
-        native.check(L.ds_plan_batch_device(ctx.handle, native.c_p(d_pro.data_ptr()), len(pro),
-                                            native.c_p(d_cas.data_ptr()), len(cas),
+        native.check(L.ds_plan_batch_device(ctx.handle,
+                                            native.c_p(d_pro.data_ptr() + plo * abi.PROBLEM.itemsize),
+                                            phi - plo, native.c_p(d_cas.data_ptr()), len(cas),
                                             native.c_p(d_grid.data_ptr()),
                                             native.c_p(d_offs.data_ptr()), 1,
-                                            native.c_p(d_out.data_ptr()), native.c_p(ctx.stream)))
+                                            native.c_p(d_out.data_ptr()), sp))
+        if comm is not None:
+            comm.gather(0, d_out.data_ptr(), (phi - plo) * PB,
+                        d_all.data_ptr() if rank == 0 else 0, d_all.numel() if rank == 0 else 0,
+                        stream=ctx.stream)
     for _ in range(args.warmup):
         plan_step()
     torch.cuda.synchronize()
+    barrier()
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(stream)
@@ -674,60 +767,54 @@ def run_gpu(args):
         plan_step()
     p1.record(stream)
     torch.cuda.synchronize()
-    plan_ms = p0.elapsed_time(p1) / args.steps
-    plan_ms = allmax([plan_ms])[0]
-    plan_value = ws * len(pro) * CANDS_PER_PROBLEM / (plan_ms / 1000.0)
-    gpu_plans = d_out.cpu().numpy().view(abi.PLAN)
-    # planner e2e through the host-buffer C-ABI call
-    ctx.plan_batch(pro, cas, grid, offs)
+    plan_ms = allmax([p0.elapsed_time(p1) / args.steps])[0]
+    plan_value = P_ALL * CANDS_PER_PROBLEM / (plan_ms / 1000.0)
+    plan_problems_s = P_ALL / (plan_ms / 1000.0)
+    plans_host = (d_all if comm is not None else d_out).cpu().numpy().view(abi.PLAN)
+    plans_ok = bool(rank != 0 or plans_host.tobytes() == want_plans.tobytes())
+    # planner e2e through the host-buffer C-ABI call (this rank's problems)
+    mine_pro = np.ascontiguousarray(pro[plo:phi])
+    ctx.plan_batch(mine_pro, cas, grid, goffs)
+    barrier()
     t0 = time.perf_counter()
     for _ in range(3):
-        ctx.plan_batch(pro, cas, grid, offs)
-    plan_e2e = ws * len(pro) * CANDS_PER_PROBLEM / allmax([(time.perf_counter() - t0) / 3])[0]
+        ctx.plan_batch(mine_pro, cas, grid, goffs)
+    plan_e2e_s = allmax([(time.perf_counter() - t0) / 3])[0]
+    plan_e2e = P_ALL * CANDS_PER_PROBLEM / plan_e2e_s
 
     # ---- planner, threshold-range sharded: every rank searches its slice of
-    # the 101-point grid for the SAME problems, then an all-reduce MIN of the
-    # packed selection keys (NCCL) and the decode (SURVEY 8(e) "by t-range")
+    # the 101-point grid for the SAME problems, the packed selection keys are
+    # MIN-all-reduced, every rank decodes (SURVEY 8(e) "by t-range";
+    # ds_plan_sharded_device -- NCCL from the library at N > 1)
     G_T = int(grid.size)
     t_lo, t_hi = ddist.shard_range(G_T, ws, rank)
-    d_keys = torch.empty(len(pro), dtype=torch.int64, device=dev)
-    d_out2 = torch.empty_like(d_out)
-    i64max = torch.iinfo(torch.int64).max
+    d_keys = torch.empty(P_ALL, dtype=torch.int64, device=dev)
+    d_out2 = torch.empty(P_ALL * PB, dtype=torch.uint8, device=dev)
 
     def tplan_step():
         with torch.cuda.stream(stream):
-            native.check(L.ds_plan_keys_device(ctx.handle, native.c_p(d_pro.data_ptr()), len(pro),
-                                               native.c_p(d_cas.data_ptr()), len(cas),
-                                               native.c_p(d_grid.data_ptr()),
-                                               native.c_p(d_offs.data_ptr()), 1, t_lo, t_hi,
-                                               native.c_p(d_keys.data_ptr()),
-                                               native.c_p(ctx.stream)))
-            if ws > 1:
-                # uint64 keys as int64 with "none" (all ones = -1) -> INT64_MAX
-                k = torch.where(d_keys == -1, torch.full_like(d_keys, i64max), d_keys)
-                if backend == "gloo":
-                    kc = k.cpu()
-                    dist.all_reduce(kc, op=dist.ReduceOp.MIN)
-                    k = kc.to(dev)
-                else:
-                    dist.all_reduce(k, op=dist.ReduceOp.MIN)
-                d_keys.copy_(torch.where(k == i64max, torch.full_like(k, -1), k))
-            native.check(L.ds_plan_from_keys_device(ctx.handle, native.c_p(d_pro.data_ptr()),
-                                                    len(pro), native.c_p(d_cas.data_ptr()),
-                                                    len(cas), native.c_p(d_grid.data_ptr()),
-                                                    native.c_p(d_offs.data_ptr()), 1,
-                                                    native.c_p(d_keys.data_ptr()),
-                                                    native.c_p(d_out2.data_ptr()),
-                                                    native.c_p(ctx.stream)))
+            if comm is not None:
+                comm.plan(d_pro.data_ptr(), P_ALL, d_cas.data_ptr(), len(cas), d_grid.data_ptr(),
+                          d_offs.data_ptr(), 1, t_lo, t_hi, d_out2.data_ptr(),
+                          stream=ctx.stream)
+                return
+            args_ = (ctx.handle, native.c_p(d_pro.data_ptr()), P_ALL,
+                     native.c_p(d_cas.data_ptr()), len(cas), native.c_p(d_grid.data_ptr()),
+                     native.c_p(d_offs.data_ptr()), 1)
+            native.check(L.ds_plan_keys_device(*args_, t_lo, t_hi,
+                                               native.c_p(d_keys.data_ptr()), sp))
+            native.check(L.ds_plan_from_keys_device(*args_, native.c_p(d_keys.data_ptr()),
+                                                    native.c_p(d_out2.data_ptr()), sp))
     tplan_step()
     torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
+    barrier()
     tplan_ms = allmax([timed(tplan_step, max(3, args.steps // 2))])[0]
-    tplan_value = len(pro) * CANDS_PER_PROBLEM / (tplan_ms / 1000.0)
-    tplan_parity = bool(torch.equal(d_out2, d_out))
+    tplan_value = P_ALL * CANDS_PER_PROBLEM / (tplan_ms / 1000.0)
+    tplan_parity = d_out2.cpu().numpy().tobytes() == want_plans.tobytes()
 
-    # ---- latent leg (config 5: 1M queries per GPU, reference-parity scorer) ------
+    # ---- latent leg (config 5 queries, the reference's own scorer): 1M per
+    # rank (distinct id ranges), route at t = 0.5, curve over the global
+    # sequence (at N > 1 the confidences all-gathered, every rank replays) ----
     lconf = torch.empty(N_LATENT, dtype=torch.float64, device=dev)
     lheavy = torch.empty(N_LATENT, dtype=torch.int64, device=dev)
     lcount = torch.empty(1, dtype=torch.int64, device=dev)
@@ -736,40 +823,62 @@ def run_gpu(args):
     qm = workloads.query_model()
     lat_id0 = rank * N_LATENT
     levs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    uprior = torch.from_numpy(workloads.uniform_prior().reshape(1).view(np.uint8).copy()).to(dev)
+    torch.cuda.synchronize()
 
     def latent_step(ev=False):
         with torch.cuda.stream(stream):
             if ev:
                 levs[0].record(stream)
             native.check(L.ds_score_latent_device(ctx.handle, abi.ptr(qm), lat_id0, N_LATENT,
-                                                  native.c_p(lconf.data_ptr()), native.c_p(0),
-                                                  native.c_p(ctx.stream)))
+                                                  native.c_p(lconf.data_ptr()), native.c_p(0), sp))
             if ev:
                 levs[1].record(stream)
-            native.check(L.ds_route_device(ctx.handle, native.c_p(lconf.data_ptr()), abi.CONF_F64,
-                                           N_LATENT, native.c_p(thr.data_ptr()), 1, lat_id0,
-                                           native.c_p(lheavy.data_ptr()),
-                                           native.c_p(lcount.data_ptr()), native.c_p(ctx.stream)))
+            if comm is None:
+                native.check(L.ds_route_device(ctx.handle, native.c_p(lconf.data_ptr()),
+                                               abi.CONF_F64, N_LATENT, native.c_p(thr.data_ptr()),
+                                               1, lat_id0, native.c_p(lheavy.data_ptr()),
+                                               native.c_p(lcount.data_ptr()), sp))
+            else:
+                comm.route(lconf.data_ptr(), abi.CONF_F64, N_LATENT, thr.data_ptr(), 1, lat_id0,
+                           lheavy.data_ptr(), lcount.data_ptr(), stream=ctx.stream)
             if ev:
                 levs[2].record(stream)
-            lcurve.copy_(prior_t)
-            native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(lcurve.data_ptr()),
-                                                   native.c_p(lconf.data_ptr()), abi.CONF_F64,
-                                                   N_LATENT, DECAY, native.c_p(ctx.stream)))
+            lcurve.copy_(uprior)
+            if comm is None:
+                native.check(L.ds_curve_observe_device(ctx.handle, native.c_p(lcurve.data_ptr()),
+                                                       native.c_p(lconf.data_ptr()), abi.CONF_F64,
+                                                       N_LATENT, DECAY, sp))
+            else:
+                comm.curve_observe(lcurve.data_ptr(), lconf.data_ptr(), abi.CONF_F64,
+                                   [N_LATENT] * ws, DECAY, stream=ctx.stream)
             if ev:
                 levs[3].record(stream)
     latent_step()
     torch.cuda.synchronize()
+    barrier()
     latent_step(ev=True)
     torch.cuda.synchronize()
     lat_ms = [levs[i].elapsed_time(levs[i + 1]) for i in range(3)]
     lconf_host = lconf.cpu().numpy()
     lheavy_host = lheavy[:int(lcount.item())].cpu().numpy()
+    lcurve_host = lcurve.cpu().numpy().view(abi.CURVE)[0].copy()
     latent_value = ws * N_LATENT / (allmax([sum(lat_ms)])[0] / 1000.0)
+    # K4 / K2 alone (kernel-level views for the rooflines below)
+    k4_ms = allmax([timed(lambda: native.check(L.ds_score_latent_device(
+        ctx.handle, abi.ptr(qm), lat_id0, N_LATENT, native.c_p(lconf.data_ptr()),
+        native.c_p(0), sp)), 10)])[0]
+    k2_ms = allmax([timed(lambda: native.check(L.ds_route_device(
+        ctx.handle, native.c_p(lconf.data_ptr()), abi.CONF_F64, N_LATENT,
+        native.c_p(thr.data_ptr()), 1, lat_id0, native.c_p(lheavy.data_ptr()),
+        native.c_p(lcount.data_ptr()), sp)), 20)])[0]
+    del lconf, lheavy
 
-    # ---- workload leg: arrivals (K8) + Query records (K4) --------------------
+    # ---- workload leg: arrivals (K8) + Query records (K4); every rank its own
+    # trace (seed WL_SEED + rank) and id range -- distinct work per rank -------
     wl_rates = np.asarray(WL_RATES, np.float64)
     wl_cap = 1_100_000
+    wl_seed = WL_SEED + rank
     wl_arr = torch.empty(wl_cap, dtype=torch.float64, device=dev)
     wl_rec = torch.empty(wl_cap * 6, dtype=torch.float64, device=dev)   # ds_query = 48 B
     wl_n = native.i64(0)
@@ -780,19 +889,19 @@ def run_gpu(args):
             if ev:
                 wevs[0].record(stream)
             native.check(L.ds_generate_arrivals_device(
-                ctx.handle, abi.ptr(wl_rates), len(wl_rates), 1.0, WL_SEED, abi.ARRIVALS_POISSON,
-                native.c_p(wl_arr.data_ptr()), wl_cap, native.ctypes.byref(wl_n),
-                native.c_p(ctx.stream)))
+                ctx.handle, abi.ptr(wl_rates), len(wl_rates), 1.0, wl_seed, abi.ARRIVALS_POISSON,
+                native.c_p(wl_arr.data_ptr()), wl_cap, native.ctypes.byref(wl_n), sp))
             if ev:
                 wevs[1].record(stream)
             native.check(L.ds_sample_queries_device(
-                ctx.handle, abi.ptr(qm), 0, native.c_p(wl_arr.data_ptr()), wl_n.value, 5.0,
-                native.c_p(wl_rec.data_ptr()), native.c_p(ctx.stream)))
+                ctx.handle, abi.ptr(qm), rank * wl_cap, native.c_p(wl_arr.data_ptr()), wl_n.value,
+                5.0, native.c_p(wl_rec.data_ptr()), sp))
             if ev:
                 wevs[2].record(stream)
     for _ in range(2):
         workload_step()
     torch.cuda.synchronize()
+    barrier()
     wl_ms = [0.0, 0.0]
     for _ in range(5):
         workload_step(ev=True)
@@ -800,16 +909,22 @@ def run_gpu(args):
         wl_ms[0] += wevs[0].elapsed_time(wevs[1]) / 5
         wl_ms[1] += wevs[1].elapsed_time(wevs[2]) / 5
     wl_count = wl_n.value
-    wl_value = ws * wl_count / (allmax([sum(wl_ms)])[0] / 1000.0)
-    wl_arr_value = ws * wl_count / (allmax([wl_ms[0]])[0] / 1000.0)
+    wl_counts = torch.tensor([float(wl_count)], dtype=torch.float64)
+    if ws > 1:
+        wl_counts = wl_counts if backend == "gloo" else wl_counts.to(dev)
+        dist.all_reduce(wl_counts)
+    wl_total = float(wl_counts.cpu()[0])
+    wl_value = wl_total / (allmax([sum(wl_ms)])[0] / 1000.0)
+    wl_arr_value = wl_total / (allmax([wl_ms[0]])[0] / 1000.0)
 
-    # ---- csv leg: queries.csv of 1M records (K9) ------------------------------
-    crec = csv_records(N_CSV)
+    # ---- csv leg: queries.csv of 1M records per rank (distinct records) -------
+    crec = csv_records(N_CSV, seed=12 + rank)
     drec = torch.from_numpy(crec.view(np.uint8).copy()).to(dev)
     csv_cap = N_CSV * 256 + 4096
     dcsv = torch.empty(csv_cap, dtype=torch.uint8, device=dev)
     csv_n = native.i64(0)
     cevs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
 
     def csv_step(ev=False):
         with torch.cuda.stream(stream):
@@ -817,31 +932,36 @@ def run_gpu(args):
                 cevs[0].record(stream)
             native.check(L.ds_format_queries_csv_device(
                 ctx.handle, native.c_p(drec.data_ptr()), N_CSV, native.c_p(dcsv.data_ptr()),
-                csv_cap, native.ctypes.byref(csv_n), native.c_p(ctx.stream)))
+                csv_cap, native.ctypes.byref(csv_n), sp))
             if ev:
                 cevs[1].record(stream)
     csv_step()
     torch.cuda.synchronize()
+    barrier()
     csv_ms = 0.0
     for _ in range(3):
         csv_step(ev=True)
         torch.cuda.synchronize()
         csv_ms += cevs[0].elapsed_time(cevs[1]) / 3
     csv_value = ws * N_CSV / (allmax([csv_ms])[0] / 1000.0)
+    barrier()
     t0 = time.perf_counter()
     csv_bytes = ctx.format_queries_csv(crec)
     csv_e2e = ws * N_CSV / allmax([time.perf_counter() - t0])[0]
+    csv_dev_ok = bool(dcsv[:csv_n.value].cpu().numpy().tobytes() == csv_bytes)
 
     if rank == 0:
         peaks, peak_src = load_peaks()
         achieved_tflops = N_IMG * DISC_FLOP_BF16_EQ / (disc_ms / 1000.0) / 1e12
         peak_burst = float(peaks["bf16_tflops"])
         peak_sus = float(peaks.get("bf16_tflops_sustained", peak_burst))
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "disc_ncu_summary.json")
-        if os.path.exists(prof):
-            with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch_5000img")
+        hbm = float(peaks["hbm_gbs"])
+        prof = load_profile_summaries()
+        traffic = prof.get("disc", {}).get("dram_bytes_per_launch_5000img")
+        # K2 at 1M f64 confidences, t = 0.5: algorithmic bytes = the confidences
+        # read once + one 8-byte id per deferred query + the count
+        k2_bytes = N_LATENT * 8 + int(lcount.item()) * 8 + 8
+        k2_gbs = k2_bytes / (k2_ms / 1000.0) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -851,6 +971,10 @@ def run_gpu(args):
             "config": {"workload": WORKLOAD,
                        "global_batch": ws * N_IMG, "image_hw": [H, W],
                        "thresholds": NT, "parallelism": f"dp{ws} (query shards)",
+                       "collectives": ("none (1 GPU)" if ws == 1 else
+                                       f"library {'NCCL' if backend == 'nccl' else 'host/gloo'}: "
+                                       "count all-gather, queue gather at rank 0, confidence "
+                                       "all-gather for the global curve"),
                        "l2": "inputs 3.9 GB/GPU > 126 MB L2, no flush"},
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": peak_burst,
                          "unit": "TFLOP/s (bf16-equivalent)", "frac": achieved_tflops / peak_burst,
@@ -871,12 +995,14 @@ def run_gpu(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "parity": {"route_counts_vs_confidences": parity_ok,
-                       "route_ids_at_0.5_vs_cpu": lists_ok,
-                       "curve_bits_vs_cpu": bool(curve_ok)},
+                       "route_ids_at_0.5_vs_confidences": lists_ok,
+                       "device_errors": take_err == -1,
+                       **parity_n1},
             "scaleout": {"value": scale_value, "unit": "images/s", "queries": N_SCALE,
-                         "queries_per_gpu": n5, "ms": scale_ms, "routed_at_0.5_rank0": scale_routed,
+                         "queries_per_gpu": n5, "ms": scale_ms, "routed_at_0.5": scale_routed,
                          "config": "config 5: 1M 512x512 queries, contiguous id shards, 5K "
-                                   "resident pool, route t=0.5, routed-count all-gather"},
+                                   "resident pool per GPU, route t=0.5; N > 1: routed-count "
+                                   "all-gather + global queue at rank 0"},
             "cascade1_batch32": {"value": b32_value, "unit": "images/s",
                                  "us_per_batch": b32_batch_us, "batch": B1,
                                  "parity_vs_full_batch": b32_parity,
@@ -884,98 +1010,183 @@ def run_gpu(args):
                                                 "unit": "images/s",
                                                 "us_per_batch": b32g_ms * 1000.0 / (
                                                     (N_IMG + B1 - 1) // B1),
+                                                "roofline_us_per_batch": 1e6 * B1 *
+                                                DISC_FLOP_BF16_EQ / (peak_burst * 1e12),
                                                 "parity_vs_full_batch": b32g_parity},
-                                 "config": "config 1: 5K 512x512 in light batches of 32 (ds_disc_batch_complete_device): score, "
-                                           "observe into the curve, route at t=0.5"},
+                                 "config": "config 1: 5K 512x512 in light batches of 32 "
+                                           "(ds_disc_batch_complete_device): score, observe "
+                                           "into the curve, route at t=0.5"},
             "cascade3": {"value": c3_value, "unit": "images/s", "image_hw": [H3, H3],
                          "images": N3, "ms_per_step": c3_ms,
                          "disc_bf16eq_tflops_step": c3_tflops,
                          "config": "config 3: 5K 1024x1024 (15.7 GB), score + route at 101 "
                                    "thresholds + curve replay"},
             "planner_t_sharded": {"value": tplan_value, "unit": "candidates/s",
-                                  "problems": len(pro), "grid_slice": [t_lo, t_hi],
+                                  "problems": P_ALL, "grid_slice": [t_lo, t_hi],
                                   "ms_per_batch": tplan_ms, "scaling": "strong",
-                                  "parity_vs_problem_sharded": tplan_parity,
-                                  "config": "config 4 problems, each rank a contiguous slice of "
-                                            "the threshold grid, all-reduce MIN of the packed "
-                                            "keys, decode"},
-            "planner": {"value": plan_value, "unit": "candidates/s", "problems": len(pro),
+                                  "parity_vs_reference": bool(tplan_parity),
+                                  "config": "config 4 batch, each rank a contiguous slice of "
+                                            "the threshold grid, MIN all-reduce of the packed "
+                                            "keys (ds_plan_sharded_device), decode"},
+            "planner": {"value": plan_value, "unit": "candidates/s", "problems": P_ALL,
+                        "problems_per_s": plan_problems_s,
                         "candidates_per_problem": CANDS_PER_PROBLEM, "ms_per_batch": plan_ms,
-                        "e2e": {"value": plan_e2e, "unit": "candidates/s"}},
+                        "scaling": "strong (one 4,096-problem batch split by problem index)",
+                        "inputs": "tests/golden/config4_bench.npz: 4,096 acceptance-C2 "
+                                  "problems (mt19937_64(7)) made by the reference",
+                        "curves_from_product_equal_reference": bool(curves_ok),
+                        "parity_vs_reference": plans_ok,
+                        "roofline": issue_roofline(prof.get("plan_sweep"), plan_ms,
+                                                   "plan_sweep_kernel"),
+                        "e2e": {"value": plan_e2e, "unit": "candidates/s",
+                                "ms_per_batch": plan_e2e_s * 1000.0}},
             "latent": {"value": latent_value, "unit": "queries/s", "queries_per_gpu": N_LATENT,
                        "ms_score_route_curve": lat_ms,
-                       "roofline": {"bound": "int/fp64 issue (no tensor/HBM bound)"}},
+                       "roofline": issue_roofline(prof.get("latent"), k4_ms, "latent_kernel"),
+                       "route_roofline": {"bound": "hbm", "kernel": "K2 route (1M f64, t=0.5)",
+                                          "achieved": k2_gbs, "peak": hbm, "unit": "GB/s",
+                                          "frac": k2_gbs / hbm, "ms": k2_ms,
+                                          "algorithmic_bytes": k2_bytes,
+                                          "traffic": prof.get("route", {}).get(
+                                              "dram_bytes_per_launch")}},
             "workload": {"value": wl_value, "unit": "queries/s",
-                         "arrivals_per_s": wl_arr_value, "arrivals_per_gpu": wl_count,
+                         "arrivals_per_s": wl_arr_value, "arrivals_rank0": wl_count,
+                         "arrivals_all_ranks": wl_total,
                          "ms_arrivals_records": wl_ms,
-                         "trace": "400 intervals x 2500 qps, Poisson, seed 3 (replica per GPU)"},
+                         "trace": "400 intervals x 2500 qps, Poisson, seed 3 + rank"},
             "csv": {"value": csv_value, "unit": "rows/s", "rows_per_gpu": N_CSV,
                     "bytes": csv_n.value, "ms": csv_ms,
                     "e2e": {"value": csv_e2e, "unit": "rows/s",
                             "note": "host records in, host bytes out (ds_format_queries_csv)"},
-                    "parity_device_vs_host": bool(
-                        dcsv[:csv_n.value].cpu().numpy().tobytes() == csv_bytes)},
+                    "parity_device_vs_host": csv_dev_ok},
         }
         if ws == 1 and not args.no_cpu:
-            threads = os.cpu_count() or 1
-            cv, ck, cpu_conf = cpu_images_leg(CPU_DISC_SAMPLE)
-            line["cpu_baseline"] = {"value": cv, "unit": "images/s", "cores": threads,
-                                    "kind": "port" if ck != "reference" else ck,
-                                    "sample": f"{CPU_DISC_SAMPLE} images 512x512: numpy port of "
-                                              "the discriminator (no reference network) + the "
-                                              "reference route loop at 101 thresholds"}
-            # image confidences of the same images (ids 0..95 of the pool) vs the
-            # CPU restatement, north_star's 1e-3 relative floored at 1e-2
-            g = c_host[:len(cpu_conf)]
-            rel = np.abs(g - cpu_conf) / np.maximum(np.abs(cpu_conf), 1e-2)
-            line["parity"]["disc_vs_cpu_port"] = {"images": int(len(cpu_conf)),
-                                                  "max_rel_err": float(rel.max()),
-                                                  "within_1e-3": bool(rel.max() <= 1e-3)}
-            sub = slice(0, CPU_PLAN_SAMPLE)
-            pv, pk, cpu_plans = cpu_planner_leg(np.ascontiguousarray(pro[sub]), cas, grid, offs,
-                                                threads)
-            line["planner"]["cpu_baseline"] = {
-                "value": pv, "unit": "candidates/s", "cores": threads, "kind": pk,
-                "sample": f"{CPU_PLAN_SAMPLE} config-4 problems, diffserve::solve on "
-                          f"{threads} threads"}
-            line["planner"]["parity_vs_cpu"] = bool(
-                gpu_plans[sub].tobytes() == cpu_plans.tobytes())
-            lv, lk, lconf_cpu, lidx_cpu = cpu_latent_leg(CPU_LATENT_SAMPLE, threads)
-            line["latent"]["cpu_baseline"] = {
-                "value": lv, "unit": "queries/s", "cores": threads, "kind": lk,
-                "sample": f"{CPU_LATENT_SAMPLE} queries: sample_query on {threads} threads + "
-                          "sequential observe/defers loop"}
-            # the same ids on the GPU: confidences (rel <= 1e-12) and the
-            # ordered heavy ids at t = 0.5 (the GPU list's prefix below the sample size)
-            g = lconf_host[:CPU_LATENT_SAMPLE]
-            rel = np.abs(g - lconf_cpu) / np.maximum(np.abs(lconf_cpu), 1e-2)
-            gl = lheavy_host[lheavy_host < CPU_LATENT_SAMPLE]
-            line["latent"]["parity_vs_cpu"] = {
-                "queries": CPU_LATENT_SAMPLE, "max_rel_err": float(rel.max()),
-                "within_1e-12": bool(rel.max() <= 1e-12),
-                "heavy_ids_equal": bool(np.array_equal(gl, lidx_cpu))}
-            wv, wav, wk, wa = cpu_workload_leg(threads)
-            line["workload"]["cpu_baseline"] = {
-                "value": wv, "unit": "queries/s", "arrivals_per_s": wav, "cores": threads,
-                "kind": wk, "sample": f"the full {len(wa)}-arrival trace: generate_arrivals "
-                                      f"(sequential) + sample_query on {threads} threads"}
-            cv2, ck2 = cpu_csv_leg(np.ascontiguousarray(crec[:CPU_CSV_SAMPLE]))
-            line["csv"]["cpu_baseline"] = {
-                "value": cv2, "unit": "rows/s", "cores": 1, "kind": ck2,
-                "sample": f"{CPU_CSV_SAMPLE} QueryRecords through write_csv (file in a tmp dir)"}
-            got = wl_arr[:wl_count].cpu().numpy()
-            line["workload"]["parity_vs_cpu"] = bool(
-                len(wa) == wl_count and got.tobytes() == wa.tobytes())
+            cpu_legs(line, args, c_host, prior, step_curve, pro, cas, grid, goffs, plans_host,
+                     lconf_host, lheavy_host, lcurve_host, wl_arr[:wl_count].cpu().numpy(), crec)
         print(json.dumps(line), flush=True)
         try:
             np.savez(os.path.join(ROOT, "gpurun_out", f"disc_weights_seed{WEIGHT_SEED}.npz"),
                      **disc.export())
         except Exception:
             pass
+    barrier()
+    if comm is not None:
+        comm.close()
     disc.close()
     ctx.close()
     if ws > 1:
         dist.destroy_process_group()
+
+
+def load_profile_summaries():
+    """ncu per-launch figures committed under profiles/ (fixed for these
+    inputs): dram bytes of disc_kernel and K2, executed warp-instructions of
+    K1 and K4 (their issue roofline)."""
+    out = {}
+    for key, name in (("disc", "disc_ncu_summary.json"), ("route", "route_ncu_summary.json"),
+                      ("plan_sweep", "plan_sweep_ncu_summary.json"),
+                      ("latent", "latent_ncu_summary.json")):
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            with open(p) as f:
+                out[key] = json.load(f)
+    return out
+
+
+def issue_roofline(summary, ms, kernel):
+    """Issue-bound kernels (no tensor or HBM bound): the launch's executed
+    warp-instructions (ncu, fixed for these inputs) at the SMs' issue peak of
+    4 warp-instructions per clock (148 SMs, max SM clock) is the floor;
+    frac = floor / measured time."""
+    if not summary or "warp_inst_per_launch" not in summary:
+        return {"bound": "issue (int/fp64)", "kernel": kernel, "frac": None,
+                "note": "no ncu instruction count committed"}
+    peaks, _ = load_peaks()
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = int(summary.get("sms", 148))
+    floor_ms = summary["warp_inst_per_launch"] / (sms * 4 * mhz * 1e6) * 1e3
+    achieved = summary["warp_inst_per_launch"] / (ms / 1000.0) / 1e9
+    peak = sms * 4 * mhz * 1e6 / 1e9
+    return {"bound": "issue (int/fp64)", "kernel": kernel, "unit": "G warp-inst/s",
+            "achieved": achieved, "peak": peak, "frac": floor_ms / ms, "ms": ms,
+            "traffic": summary.get("dram_bytes_per_launch"),
+            "source": summary.get("source")}
+
+
+def cpu_legs(line, args, c_host, prior, gpu_curve, pro, cas, grid, goffs, gpu_plans, lconf_host,
+             lheavy_host, lcurve_host, wl_arr, crec):
+    """The CPU reference path on this box's host cores (rank 0, N = 1), and
+    the parity checks that need it (the oracle/_ref checker)."""
+    from oracle import lib
+    from paper_2411_15381_b200 import abi, workloads
+    threads = os.cpu_count() or 1
+    cv, ck, cpu_conf = cpu_images_leg(CPU_DISC_SAMPLE)
+    line["cpu_baseline"] = {"value": cv, "unit": "images/s", "cores": threads,
+                            "kind": "port" if ck != "reference" else ck,
+                            "sample": f"{CPU_DISC_SAMPLE} images 512x512: numpy port of "
+                                      "the discriminator (no reference network) + the "
+                                      "reference route loop at 101 thresholds"}
+    g = c_host[:len(cpu_conf)]
+    rel = np.abs(g - cpu_conf) / np.maximum(np.abs(cpu_conf), 1e-2)
+    line["parity"]["disc_vs_cpu_port"] = {"images": int(len(cpu_conf)),
+                                          "max_rel_err": float(rel.max()),
+                                          "within_1e-3": bool(rel.max() <= 1e-3)}
+    # the step's curve vs the reference's observe loop on the same confidences
+    use_ref = lib.ref_available()
+    cw = prior.copy()
+    idx = np.zeros(len(c_host), np.int64)
+    cnt = np.zeros(1, np.int64)
+    (lib.ref().dsref_route_loop if use_ref else lib.port().dso_route_loop)(
+        abi.ptr(c_host), len(c_host), 0.5, 1, DECAY, abi.ptr(cw), abi.ptr(idx), abi.ptr(cnt))
+    line["parity"]["curve_bits_vs_reference_loop"] = bool(cw.tobytes() == gpu_curve.tobytes())
+    line["parity"]["route_ids_at_0.5_vs_reference_loop"] = bool(
+        np.array_equal(idx[:int(cnt[0])], np.flatnonzero(c_host < 0.5)))
+    # planner: diffserve::solve over the IDENTICAL 4,096-problem batch, all
+    # threads and one thread
+    pv, pk, cpu_plans, pt = cpu_planner_leg(pro, cas, grid, goffs, threads)
+    pv1, _, _, pt1 = cpu_planner_leg(pro, cas, grid, goffs, 1)
+    line["planner"]["cpu_baseline"] = {
+        "value": pv, "unit": "candidates/s", "cores": threads, "kind": pk,
+        "problems_per_s": len(pro) / pt, "seconds": pt,
+        "one_thread": {"value": pv1, "problems_per_s": len(pro) / pt1, "seconds": pt1},
+        "sample": f"the identical {len(pro)}-problem batch, diffserve::solve on "
+                  f"{threads} threads and on 1"}
+    line["planner"]["parity_cpu_vs_gpu"] = bool(cpu_plans.tobytes() == gpu_plans.tobytes())
+    line["planner"]["speedup_vs_cpu_all_threads"] = pt / (line["planner"]["ms_per_batch"] / 1e3)
+    lv, lk, lconf_cpu, lidx_cpu = cpu_latent_leg(CPU_LATENT_SAMPLE, threads)
+    line["latent"]["cpu_baseline"] = {
+        "value": lv, "unit": "queries/s", "cores": threads, "kind": lk,
+        "sample": f"{CPU_LATENT_SAMPLE} queries: sample_query on {threads} threads + "
+                  "sequential observe/defers loop"}
+    g = lconf_host[:CPU_LATENT_SAMPLE]
+    rel = np.abs(g - lconf_cpu) / np.maximum(np.abs(lconf_cpu), 1e-2)
+    gl = lheavy_host[lheavy_host < CPU_LATENT_SAMPLE]
+    # the latent leg's curve (1M observations, uniform prior) vs the
+    # reference's loop over the GPU's confidences
+    cl = workloads.uniform_prior()
+    li = np.zeros(len(lconf_host), np.int64)
+    (lib.ref().dsref_route_loop if use_ref else lib.port().dso_route_loop)(
+        abi.ptr(lconf_host), len(lconf_host), 0.5, 1, DECAY, abi.ptr(cl), abi.ptr(li),
+        abi.ptr(cnt))
+    line["latent"]["curve_bits_vs_reference_loop"] = bool(cl.tobytes() == lcurve_host.tobytes())
+    line["latent"]["heavy_ids_vs_reference_loop"] = bool(
+        np.array_equal(li[:int(cnt[0])], lheavy_host))
+    line["latent"]["parity_vs_cpu"] = {
+        "queries": CPU_LATENT_SAMPLE, "max_rel_err": float(rel.max()),
+        "bit_identical": int((g == lconf_cpu).sum()),
+        "within_1e-12": bool(rel.max() <= 1e-12),
+        "heavy_ids_equal": bool(np.array_equal(gl, lidx_cpu))}
+    wv, wav, wk, wa = cpu_workload_leg(threads)
+    line["workload"]["cpu_baseline"] = {
+        "value": wv, "unit": "queries/s", "arrivals_per_s": wav, "cores": threads,
+        "kind": wk, "sample": f"the full {len(wa)}-arrival trace: generate_arrivals "
+                              f"(sequential) + sample_query on {threads} threads"}
+    line["workload"]["parity_vs_cpu"] = bool(len(wa) == len(wl_arr) and
+                                             wl_arr.tobytes() == wa.tobytes())
+    cv2, ck2 = cpu_csv_leg(np.ascontiguousarray(crec[:CPU_CSV_SAMPLE]))
+    line["csv"]["cpu_baseline"] = {
+        "value": cv2, "unit": "rows/s", "cores": 1, "kind": ck2,
+        "sample": f"{CPU_CSV_SAMPLE} QueryRecords through write_csv (file in a tmp dir)"}
 
 
 def main():

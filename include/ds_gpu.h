@@ -56,7 +56,8 @@ typedef enum {
     DS_ERR_OUT_OF_RANGE = 4,     /* std::out_of_range (unprofiled batch)   */
     DS_ERR_CUDA = 5,             /* CUDA runtime / launch failure          */
     DS_ERR_NO_DEVICE = 6,        /* no sm_100 device visible               */
-    DS_ERR_CAPACITY = 7          /* input exceeds a compiled-in ABI limit  */
+    DS_ERR_CAPACITY = 7,         /* input exceeds a compiled-in ABI limit  */
+    DS_ERR_COMM = 8              /* collective transport (NCCL / host ops) */
 } ds_status;
 
 typedef enum {
@@ -145,6 +146,17 @@ ds_status ds_ctx_synchronize(ds_ctx* ctx);
 /* Number of device kernels this context launched so far (for bench audits). */
 int64_t ds_ctx_launch_count(const ds_ctx* ctx);
 void* ds_ctx_stream(ds_ctx* ctx); /* the context's cudaStream_t */
+/* The _device variants do not synchronize, so they cannot return the
+ * reference's std::domain_error for a confidence outside [0, 1]
+ * (profiles.cpp:108-112) at launch time. They stop the curve replay at the
+ * first invalid observation, as the reference's throw does (a light batch of
+ * <= 2048 images in ds_disc_batch_complete_device also routes only the
+ * queries before it, as the throw out of handle_batch_complete would), and
+ * record its index in the context. ds_ctx_take_error synchronizes `stream`
+ * (NULL: the context's stream), returns DS_ERR_DOMAIN with *first_bad = that
+ * index if any device call recorded one since the last call (and clears it),
+ * else DS_OK with *first_bad = -1. */
+ds_status ds_ctx_take_error(ds_ctx* ctx, void* stream, int64_t* first_bad);
 
 /* ---- planner (K1 plan_sweep) ---------------------------------------- */
 /* Validates every problem with the reference's checks (allocator.cpp:22-36,
@@ -215,7 +227,9 @@ ds_status ds_route(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t n,
 ds_status ds_route_device(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t n,
                           const double* thresholds, int32_t n_thresholds, int64_t index_base,
                           int64_t* heavy_idx, int64_t* counts, void* stream);
-/* Scratch bytes ds_route_device needs for n queries and nt thresholds. */
+/* Caller scratch ds_route_device needs for n queries and nt thresholds: 0
+ * (kept for ABI stability; K2 is one pass and keeps its look-back flags in
+ * the context). */
 size_t ds_route_scratch_bytes(int64_t n, int32_t n_thresholds);
 
 /* ---- deferral curve (K3 curve_observe) -------------------------------- */
@@ -394,6 +408,108 @@ ds_status ds_disc_batch_complete_device(ds_disc* disc, const uint8_t* nhwc, int6
  * function of (seed, image id, pixel index); generated on the device. */
 ds_status ds_synth_images_device(ds_ctx* ctx, uint64_t seed, uint64_t id0, int64_t n,
                                  int32_t h, int32_t w, uint8_t* out, void* stream);
+
+/* ---- multi-GPU: the sharded hot path (SURVEY.md 8(b) "NCCL-aware
+ * multi-GPU variant", 8(e)) ---------------------------------------------- */
+/* One rank per GPU. Queries shard by contiguous id range, planner problems by
+ * index or one batch by threshold range. The reference is single-process
+ * (SPEC.md:330); these entry points make an N-GPU run return exactly what one
+ * GPU -- and therefore the reference -- returns:
+ *   heavy queues : routed-count all-gather + exclusive scan (each rank's
+ *                  offset in every global queue), then the ordered ids of all
+ *                  ranks gathered into the global queues at a root rank
+ *                  (cluster.cpp:290-306 id order);
+ *   curve        : the ordered confidences all-gathered, every rank replays
+ *                  the whole sequence (observe_confidence is order-dependent
+ *                  through the decay, profiles.cpp:108-120);
+ *   planner      : packed selection keys MIN-all-reduced over threshold
+ *                  ranges (allocator.cpp:57-67,91-121).
+ * All calls below are COLLECTIVE: every rank of the communicator makes the
+ * same call with matching scalar arguments, in the same order. Device
+ * pointers, stream-ordered on `stream` (NULL: the context's stream); calls
+ * that must size a transfer from device counts synchronize `stream` once. */
+typedef struct ds_comm ds_comm;
+#define DS_NCCL_UNIQUE_ID_BYTES 128
+
+/* Host transport for callers without NCCL (and for tests that run several
+ * ranks on one GPU, which NCCL refuses): the library copies to host, calls
+ * these, copies back. Each returns 0 on success. */
+typedef struct {
+    /* recv gets nranks*bytes bytes: rank r's `bytes` bytes at offset r*bytes */
+    int (*allgather)(const void* send, void* recv, size_t bytes, void* user);
+    /* element-wise unsigned minimum over ranks, in place */
+    int (*allreduce_min_u64)(uint64_t* buf, size_t count, void* user);
+    /* rank r contributes bytes[r] bytes; root receives them back to back in
+     * rank order (recv is NULL on the other ranks) */
+    int (*gatherv)(const void* send, void* recv, const size_t* bytes, int32_t root, void* user);
+} ds_comm_ops;
+
+/* NCCL (loaded at run time: libnccl.so.2, the process's own if one is
+ * already loaded -- a host that links its own NCCL, e.g. torch, must load it
+ * before the first ds_comm call, or the system copy takes the soname). Rank 0 makes the id and distributes it out of band (MPI,
+ * torch.distributed, a file), then every rank calls ds_comm_init_nccl with
+ * its context -- ncclCommInitRank on the context's device. */
+ds_status ds_comm_nccl_unique_id(uint8_t id[DS_NCCL_UNIQUE_ID_BYTES]);
+ds_status ds_comm_init_nccl(ds_ctx* ctx, int32_t nranks, int32_t rank,
+                            const uint8_t id[DS_NCCL_UNIQUE_ID_BYTES], ds_comm** out);
+/* Wraps a caller's ncclComm_t (not owned; its device must be ctx's). */
+ds_status ds_comm_wrap_nccl(ds_ctx* ctx, void* nccl_comm, ds_comm** out);
+/* One process driving n GPUs (ncclCommInitAll over ctxs[i]'s devices): drive
+ * each comms[i] from its own host thread (the calls are collective and some
+ * synchronize, so one thread issuing all ranks' calls would deadlock). */
+ds_status ds_comm_init_all(ds_ctx* const* ctxs, int32_t n, ds_comm** comms);
+ds_status ds_comm_create_host(ds_ctx* ctx, int32_t nranks, int32_t rank, const ds_comm_ops* ops,
+                              void* user, ds_comm** out);
+ds_status ds_comm_destroy(ds_comm* comm);
+int32_t ds_comm_rank(const ds_comm* comm);
+int32_t ds_comm_size(const ds_comm* comm);
+/* [lo, hi) of a contiguous balanced split of n items: lo = n*rank/nranks. */
+void ds_shard_range(int64_t n, int32_t nranks, int32_t rank, int64_t* lo, int64_t* hi);
+
+/* Route this rank's shard (ds_route_device with index_base = its first global
+ * id), then all-gather the routed counts: rank_offsets[k] = this rank's start
+ * inside global heavy queue k (sum of lower ranks' counts), global_counts[k] =
+ * the global queue's length. Either output may be NULL. */
+ds_status ds_route_sharded_device(ds_ctx* ctx, ds_comm* comm, const void* conf, int32_t dtype,
+                                  int64_t n_local, const double* thresholds, int32_t n_thresholds,
+                                  int64_t index_base, int64_t* heavy_local, int64_t* counts_local,
+                                  int64_t* rank_offsets, int64_t* global_counts, void* stream);
+/* Assemble the global heavy queues at `root`: row k of global_heavy (stride
+ * global_stride >= the global count) receives every rank's counts_local[k]
+ * ids from heavy_local row k (stride n_local) at that rank's offset, i.e.
+ * rank order = global id order. global_heavy / global_counts are written on
+ * root only (may be NULL elsewhere). Synchronizes `stream` once (the
+ * transfer sizes come from the counts). */
+ds_status ds_queue_gather_device(ds_ctx* ctx, ds_comm* comm, int32_t root,
+                                 const int64_t* heavy_local, int64_t n_local,
+                                 const int64_t* counts_local, int32_t n_thresholds,
+                                 int64_t* global_heavy, int64_t global_stride,
+                                 int64_t* global_counts, void* stream);
+/* observe_confidence over the GLOBAL sequence: the ranks' shards (sizes
+ * shard_sizes[0..nranks), host memory, rank order = id order) are
+ * all-gathered and every rank replays all of them into its `curve`, so every
+ * rank ends with the curve one GPU (and the reference) computes. An invalid
+ * confidence is recorded as in ds_curve_observe_device (global index). */
+ds_status ds_curve_observe_sharded_device(ds_ctx* ctx, ds_comm* comm, ds_curve* curve,
+                                          const void* conf_local, int32_t dtype,
+                                          const int64_t* shard_sizes, double decay,
+                                          void* stream);
+/* Threshold-range sharded planning of ONE problem batch (every rank passes the
+ * same problems): this rank searches grid indices [t_lo, t_hi) (ds_plan_keys),
+ * the keys are MIN-all-reduced (uint64; "none" is UINT64_MAX), and every rank
+ * decodes the plans ds_plan_batch would return (ds_plan_from_keys). */
+ds_status ds_plan_sharded_device(ds_ctx* ctx, ds_comm* comm, const ds_problem* problems, int32_t n,
+                                 const ds_cascade* cascades, int32_t n_cascades,
+                                 const double* grid_values, const int32_t* grid_offsets,
+                                 int32_t n_grids, int32_t t_lo, int32_t t_hi, ds_plan* out,
+                                 void* stream);
+/* Generic ordered gather (problem-sharded plans, per-rank results): rank r
+ * contributes `bytes` bytes (may differ per rank); root receives all of them
+ * back to back in rank order and *total_bytes their sum (root only). recv
+ * needs room for the sum. Synchronizes `stream` once. */
+ds_status ds_comm_gather_device(ds_ctx* ctx, ds_comm* comm, int32_t root, const void* send,
+                                size_t bytes, void* recv, size_t recv_capacity,
+                                size_t* total_bytes, void* stream);
 
 #ifdef __cplusplus
 }

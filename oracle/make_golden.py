@@ -122,6 +122,37 @@ def gen_config4(per_combo=256):
     return int(want["feasible"].sum()), len(pro)
 
 
+def gen_config4_bench(total=4096):
+    """BASELINE.md's planner batch: P = 4,096 problems of the acceptance-C2
+    recipe (mt19937_64(7), acceptance_main.cpp:177-190) over the 3 fitted 32x32
+    cascades x S in {16, 32, 64, 128} (12 combos: 342 or 341 problems each),
+    the cascades' curves = from_samples of 5K sample_query confidences (cfg,
+    seed 1), grid k/100; want_solve = the reference's solve on each. The
+    batch bench.py times (GPU and the reference CPU arm) -- identical inputs."""
+    r = lib.ref()
+    cas = np.zeros(3, abi.CASCADE)
+    for i, name in enumerate(["cascade1", "cascade2", "cascade3"]):
+        light, heavy, slo = workloads.fitted_tables(name)
+        cas[i] = workloads.make_cascade(light, heavy, slo, sampled_curve(name))
+    grid = workloads.make_grid(0.01)
+    combos = [(ci, s) for ci in range(3) for s in (16, 32, 64, 128)]
+    probs = []
+    for j, (ci, s) in enumerate(combos):
+        n = total // len(combos) + (1 if j < total % len(combos) else 0)
+        p = np.zeros(n, abi.PROBLEM)
+        one = cas[ci:ci + 1].copy()
+        _check(r.dsref_gen_c2_recipe(P(one), s, 7, n, P(p)), "c2 recipe")
+        p["cascade"] = ci
+        probs.append(p)
+    pro = np.concatenate(probs)
+    assert len(pro) == total
+    offs = np.array([0, len(grid)], np.int32)
+    want = ref_plan(pro, cas, grid, offs)
+    np.savez_compressed(os.path.join(OUT, "config4_bench.npz"), cascades=cas, problems=pro,
+                        grid_values=grid, grid_offsets=offs, want_solve=want)
+    return int(want["feasible"].sum()), len(pro)
+
+
 def random_table(rng, base, max_sizes, contiguous):
     n = int(rng.integers(1, max_sizes + 1))
     t = {}
@@ -427,6 +458,7 @@ def main():
     print("alloc_random_2024: feasible", gen_alloc_random(), "of 60")
     print("accept_c1: feasible", gen_accept_c1(), "of 200")
     print("config4: feasible/total", gen_config4())
+    print("config4_bench: feasible/total", gen_config4_bench())
     print("wide_random: feasible/total", gen_wide())
     gen_latent()
     print("latent: ok")

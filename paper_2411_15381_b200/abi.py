@@ -23,6 +23,7 @@ ERR_OUT_OF_RANGE = 4
 ERR_CUDA = 5
 ERR_NO_DEVICE = 6
 ERR_CAPACITY = 7
+ERR_COMM = 8
 
 # ds_solve_mode
 SOLVE = 0

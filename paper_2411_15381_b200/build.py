@@ -25,7 +25,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-Xptxas"
 EXACT_FP64 = {"plan_sweep.cu", "latent.cu", "curve.cu", "route.cu", "arrivals.cu"}
 
 SOURCES = ["ds_ctx.cu", "plan_sweep.cu", "latent.cu", "route.cu", "curve.cu", "disc.cu",
-           "synth.cu", "arrivals.cu", "csv.cu"]
+           "synth.cu", "arrivals.cu", "csv.cu", "comm.cu"]
 HEADERS = ["ds_internal.h", "sm100.cuh", "fdlibm_log1p.h", "fmt6.h"]
 
 
@@ -57,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
     if force or not os.path.exists(LIB) or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
         if r.returncode != 0:

@@ -119,7 +119,7 @@ __device__ double total_run(double t, int64_t len, double d, bool& settled) {
 template <typename T, bool kScale>
 __global__ void __launch_bounds__(kThreads)
 curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int64_t n,
-                     double decay, int* __restrict__ bad) {
+                     double decay, int* __restrict__ bad, long long* __restrict__ err) {
     __shared__ __align__(16) unsigned char bins[kChunk];
     __shared__ int chunk_bad;
     const int tid = threadIdx.x;
@@ -187,6 +187,9 @@ curve_observe_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, i
     }
     if (tid < DS_CURVE_BINS) curve->bin_mass[tid] = m;
     else if (is_total) curve->total_mass = m;
+    // device variants: publish the first invalid observation to the context
+    // (every atomicMin on *bad precedes the last __syncthreads of the loop)
+    if (err && tid == 0 && *bad != 0x7fffffff) atomicMin(err, static_cast<long long>(*bad));
 }
 
 
@@ -245,6 +248,7 @@ struct Ws {
     int* changed;         // [kMaxPasses][kChains]
     unsigned* bar;        // grid barrier arrivals
     int* bad;             // first invalid observation (INT_MAX if none)
+    long long* err;       // the context's device error word (device variants), or nullptr
     unsigned long long* trace;   // debug (DS_CURVE_TRACE): phase timestamps, else nullptr
 };
 
@@ -567,6 +571,7 @@ curve_spec_kernel(ds_curve* __restrict__ curve, const T* __restrict__ conf, int6
     if (bad != 0x7fffffff) {
         // the reference throws at the first invalid confidence: replay up to it
         if (j == 0) sequential<kScale>(curve, ws.bins, bad, d);
+        if (j == 0 && tid == 0 && ws.err) atomicMin(ws.err, static_cast<long long>(bad));
         return;
     }
 
@@ -725,7 +730,8 @@ SpecPlan spec_plan(ds_ctx* ctx, int64_t n, int32_t dtype, double decay) {
 
 // `ws` is a device area of spec_plan(...).bytes (unused by the single-CTA path).
 ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype, int64_t n,
-                 double decay, int* dbad, const SpecPlan& plan, char* ws, cudaStream_t st) {
+                 double decay, int* dbad, const SpecPlan& plan, char* ws, cudaStream_t st,
+                 long long* err) {
     const bool scale = decay != 1.0;
     if (plan.bytes) {
         const size_t rows = static_cast<size_t>(plan.S) * spec::kChains;
@@ -747,6 +753,7 @@ ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype,
         q += dsi::align_up(spec::kMaxPasses * spec::kChains * 4, 256);
         w.bar = reinterpret_cast<unsigned*>(q);
         w.bad = dbad;
+        w.err = err;
         static unsigned long long* trace_buf = nullptr;
         static const bool want_trace = getenv("DS_CURVE_TRACE") != nullptr;
         if (want_trace && !trace_buf) cudaMalloc(&trace_buf, 32 * sizeof(unsigned long long));
@@ -799,12 +806,12 @@ ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype,
     }
     if (dtype == DS_CONF_F64) {
         const double* c = static_cast<const double*>(conf);
-        if (scale) curve_observe_kernel<double, true><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);
-        else curve_observe_kernel<double, false><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);
+        if (scale) curve_observe_kernel<double, true><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad, err);
+        else curve_observe_kernel<double, false><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad, err);
     } else {
         const float* c = static_cast<const float*>(conf);
-        if (scale) curve_observe_kernel<float, true><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);
-        else curve_observe_kernel<float, false><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad);
+        if (scale) curve_observe_kernel<float, true><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad, err);
+        else curve_observe_kernel<float, false><<<1, kThreads, 0, st>>>(dcurve, c, n, decay, dbad, err);
     }
     DS_LAUNCH_CHECK(ctx, "curve_observe_kernel");
     return DS_OK;
@@ -813,8 +820,9 @@ ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype,
 } // namespace
 
 // Device variant: `curve` is a device ds_curve updated in place. A confidence
-// outside [0, 1] stops the replay where the reference would throw; the
-// host-buffer variant reports it as DS_ERR_DOMAIN.
+// outside [0, 1] stops the replay where the reference would throw and is
+// recorded in the context (ds_ctx_take_error); the host-buffer variant
+// reports it as DS_ERR_DOMAIN directly.
 extern "C" ds_status ds_curve_observe_device(ds_ctx* ctx, ds_curve* curve, const void* conf,
                                              int32_t dtype, int64_t n, double decay,
                                              void* stream) {
@@ -830,7 +838,7 @@ extern "C" ds_status ds_curve_observe_device(ds_ctx* ctx, ds_curve* curve, const
     ds_status s = dsi::ensure_scratch(ctx, 256 + plan.bytes, &scratch);
     if (s != DS_OK) return s;
     return launch(ctx, curve, conf, dtype, n, decay, static_cast<int*>(scratch), plan,
-                  static_cast<char*>(scratch) + 256, st);
+                  static_cast<char*>(scratch) + 256, st, ctx->d_err);
 }
 
 extern "C" ds_status ds_curve_observe(ds_ctx* ctx, ds_curve* curve, const void* conf,
@@ -861,7 +869,7 @@ extern "C" ds_status ds_curve_observe(ds_ctx* ctx, ds_curve* curve, const void* 
         return dsi::fail(DS_ERR_DOMAIN, "curve decay must lie in (0, 1]");
     }
     s = launch(ctx, reinterpret_cast<ds_curve*>(d + bc), d, dtype, n, decay, dbad, plan,
-               d + bc + bv + 256, ctx->stream);
+               d + bc + bv + 256, ctx->stream, nullptr);
     if (s != DS_OK) return s;
     int bad = 0;
     DS_CUDA_TRY(cudaMemcpyAsync(curve, d + bc, sizeof(ds_curve), cudaMemcpyDeviceToHost,

@@ -784,12 +784,17 @@ __global__ void finalize_kernel(const float* __restrict__ part, long long n, int
 // bins on warps 0-3, the total alone on warp 4, explicit _rn fp64), then
 // Policy::defers (strict <) at every threshold into ordered heavy lists (as
 // route.cu). Bit-identical to finalize + ds_curve_observe + ds_route.
+// A confidence outside [0, 1] (a NaN from the network) is where the reference
+// throws out of handle_batch_complete: the curve stops before it, only the
+// queries before it are routed, and its index goes to the context's device
+// error word (ds_ctx_take_error).
 constexpr int kTailThreads = 160, kTailTotalTid = 128, kTailMax = 2048;
 __global__ void __launch_bounds__(kTailThreads)
 batch_tail_kernel(const float* __restrict__ part, int n, int tpi, int tokens, float hb,
                   float* __restrict__ conf, ds_curve* __restrict__ curve, double decay,
                   const double* __restrict__ thr, int nt, long long index_base,
-                  long long* __restrict__ heavy, long long* __restrict__ counts) {
+                  long long* __restrict__ heavy, long long* __restrict__ counts,
+                  long long* __restrict__ err) {
     __shared__ float sc[kTailMax];
     __shared__ __align__(16) unsigned char sbin[kTailMax];
     __shared__ int s_bad, wcnt[kTailThreads / 32];
@@ -812,6 +817,7 @@ batch_tail_kernel(const float* __restrict__ part, int n, int tpi, int tokens, fl
     }
     __syncthreads();
     const int n_eff = s_bad;
+    if (tid == 0 && n_eff < n) atomicMin(err, static_cast<long long>(n_eff));
     const bool scale = decay != 1.0;
     if (tid < DS_CURVE_BINS) {
         double m = curve->bin_mass[tid];
@@ -829,9 +835,9 @@ batch_tail_kernel(const float* __restrict__ part, int n, int tpi, int tokens, fl
         const double t = thr[k];
         long long off = 0;
         long long* out = heavy + static_cast<long long>(k) * n;
-        for (int base = 0; base < n; base += kTailThreads) {
+        for (int base = 0; base < n_eff; base += kTailThreads) {
             const int i = base + tid;
-            const bool p = i < n && static_cast<double>(sc[i]) < t;
+            const bool p = i < n_eff && static_cast<double>(sc[i]) < t;
             const unsigned bal = __ballot_sync(0xffffffffu, p);
             __syncthreads();   // wcnt of the previous chunk consumed
             if (lane == 0) wcnt[warp] = __popc(bal);
@@ -1047,7 +1053,7 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     if (tail) {
         batch_tail_kernel<<<1, kTailThreads, 0, st>>>(
             part, static_cast<int>(n), p.tiles_per_img, tokens, d->hb, out, tail->curve, tail->decay,
-            tail->thr, tail->nt, tail->index_base, tail->heavy, tail->counts);
+            tail->thr, tail->nt, tail->index_base, tail->heavy, tail->counts, d->ctx->d_err);
         DS_LAUNCH_CHECK(d->ctx, "batch_tail_kernel");
     } else {
         finalize_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(

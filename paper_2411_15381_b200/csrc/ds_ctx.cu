@@ -27,7 +27,9 @@ ds_status cuda_fail(cudaError_t e, const char* what) {
 ds_status ensure_scratch(ds_ctx* ctx, size_t bytes, void** out) {
     if (bytes > ctx->scratch_bytes) {
         if (ctx->scratch) {
-            DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+            // the _device entry points use this scratch on the CALLER's stream:
+            // drain the whole device, not only ctx->stream, before freeing it
+            DS_CUDA_TRY(cudaDeviceSynchronize());
             DS_CUDA_TRY(cudaFree(ctx->scratch));
             ctx->scratch = nullptr;
             ctx->scratch_bytes = 0;
@@ -53,6 +55,13 @@ ds_status ensure_pinned(ds_ctx* ctx, size_t bytes, void** out) {
         ctx->pinned_bytes = want;
     }
     *out = ctx->pinned;
+    return DS_OK;
+}
+
+ds_status reset_device_error(ds_ctx* ctx, cudaStream_t st) {
+    static const long long kNone = 0x7fffffffffffffffLL;
+    // pageable source: staged before the call returns
+    DS_CUDA_TRY(cudaMemcpyAsync(ctx->d_err, &kNone, sizeof(kNone), cudaMemcpyHostToDevice, st));
     return DS_OK;
 }
 
@@ -104,6 +113,18 @@ ds_status ds_ctx_create(int device, ds_ctx** out) {
         delete ctx;
         return dsi::cuda_fail(e, "cudaStreamCreate");
     }
+    e = cudaMalloc(&ctx->d_err, sizeof(long long));
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+        return dsi::cuda_fail(e, "cudaMalloc");
+    }
+    if (dsi::reset_device_error(ctx, ctx->stream) != DS_OK) {
+        cudaFree(ctx->d_err);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+        return DS_ERR_CUDA;
+    }
     *out = ctx;
     return DS_OK;
 }
@@ -113,6 +134,8 @@ ds_status ds_ctx_destroy(ds_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->d_err) cudaFree(ctx->d_err);
+    if (ctx->route_flags) cudaFree(ctx->route_flags);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);
@@ -133,6 +156,21 @@ ds_status ds_ctx_synchronize(ds_ctx* ctx) {
 
 int64_t ds_ctx_launch_count(const ds_ctx* ctx) {
     return ctx ? ctx->launches.load(std::memory_order_relaxed) : 0;
+}
+
+ds_status ds_ctx_take_error(ds_ctx* ctx, void* stream, int64_t* first_bad) {
+    if (!ctx) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null ctx");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    DS_CUDA_TRY(cudaSetDevice(ctx->device));
+    long long v = 0;
+    DS_CUDA_TRY(cudaMemcpyAsync(&v, ctx->d_err, sizeof(v), cudaMemcpyDeviceToHost, st));
+    DS_CUDA_TRY(cudaStreamSynchronize(st));
+    if (first_bad) *first_bad = v == 0x7fffffffffffffffLL ? -1 : v;
+    if (v == 0x7fffffffffffffffLL) return DS_OK;
+    ds_status s = dsi::reset_device_error(ctx, st);
+    if (s != DS_OK) return s;
+    return dsi::fail(DS_ERR_DOMAIN, "confidence must lie in [0, 1] (observation " +
+                                        std::to_string(v) + " of a device call)");
 }
 
 void* ds_ctx_stream(ds_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }

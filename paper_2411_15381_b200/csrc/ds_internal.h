@@ -23,6 +23,14 @@ struct ds_ctx {
     // second stream + events for copy/compute overlap in host-buffer calls
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // first invalid confidence a device variant met (LLONG_MAX if none): the
+    // _device calls cannot return the reference's domain_error at launch time
+    // (ds_ctx_take_error reads and clears it)
+    long long* d_err = nullptr;
+    // K2's decoupled look-back flags ([thresholds][tiles] epoch-tagged words)
+    void* route_flags = nullptr;
+    size_t route_flags_bytes = 0;
+    unsigned route_epoch = 0;
 };
 
 namespace dsi {
@@ -37,6 +45,9 @@ ds_status cuda_fail(cudaError_t e, const char* what);
 ds_status ensure_scratch(ds_ctx* ctx, size_t bytes, void** out);
 ds_status ensure_pinned(ds_ctx* ctx, size_t bytes, void** out);
 ds_status ensure_copy_stream(ds_ctx* ctx);
+
+// Stream-ordered reset of ctx->d_err to LLONG_MAX.
+ds_status reset_device_error(ds_ctx* ctx, cudaStream_t st);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -6,12 +6,23 @@
 // test_policies.cpp:46-48), and deferred ids enter the heavy queue in id
 // order. For every threshold t_k the output is that ordered id list.
 //
-// Two passes over tiles of kTile confidences (HBM-bound: 4-8 B read + 8 B
-// written per deferred query; the second pass re-reads the tile from L2):
-//   count  : per (tile, threshold) number of deferrals (warp ballot + popc)
-//   scatter: block-exclusive prefix of earlier tiles' counts, then a warp
-//            ballot/popc prefix inside the tile gives each deferred query its
-//            slot; indices are written coalesced-in-order.
+// ONE pass, one launch (HBM-bound: the confidences are read once, 8 B are
+// written per deferred query). Grid (tiles, thresholds); a CTA owns a tile of
+// kTile confidences for one threshold:
+//   * ingest: 128-bit loads (double2 / float4), striped so a warp reads 512
+//     contiguous bytes per instruction; element e of row r, thread t, slot j
+//     is tile_base + r*kThreads*V + t*V + j;
+//   * count: warp ballots per (row, slot), popc -> per-warp row counts in
+//     shared memory -> the tile's deferral count;
+//   * decoupled look-back (single-pass scan): the tile publishes its count
+//     (status A), warp 0 walks the predecessors' flags 32 at a time back to
+//     the nearest inclusive prefix (status P), then publishes its own P. A
+//     flag word is [epoch:20 | status:2 | value:42]; the epoch is bumped per
+//     launch, so stale words from earlier launches read as "not ready" and no
+//     memset is needed between launches. Tiles of a threshold are blockIdx.x
+//     in dispatch order, so every predecessor is running or done;
+//   * scatter: exclusive prefix + rows before + warps before + the lane's rank
+//     among the warp's deferrals of that row: ordered, coalesced id writes.
 #include <cuda_runtime.h>
 
 #include "ds_internal.h"
@@ -19,151 +30,213 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kPerThread = 8;
-constexpr int kTile = kThreads * kPerThread;   // 2048 queries per tile
+constexpr int kPerThread = 16;                 // confidences per thread
+constexpr int kTile = kThreads * kPerThread;   // 4096 per tile
+constexpr int kWarps = kThreads / 32;
+constexpr unsigned long long kValBits = 42, kValMask = (1ull << kValBits) - 1;
+constexpr unsigned kEpochBits = 20;
+constexpr unsigned long long kStatusA = 1, kStatusP = 2;
 
-template <typename T>
-__device__ __forceinline__ double load_conf(const T* c, int64_t i) {
-    return static_cast<double>(__ldg(c + i));
+template <typename T> struct Vec;
+template <> struct Vec<double> {
+    using type = double2;
+    static constexpr int V = 2;
+    __device__ static void get(const type& v, double (&o)[2]) { o[0] = v.x; o[1] = v.y; }
+};
+template <> struct Vec<float> {
+    using type = float4;
+    static constexpr int V = 4;
+    __device__ static void get(const type& v, double (&o)[4]) {
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+};
+
+__device__ __forceinline__ unsigned long long flag_word(unsigned epoch, unsigned long long st,
+                                                        long long v) {
+    return (static_cast<unsigned long long>(epoch) << (kValBits + 2)) | (st << kValBits) |
+           (static_cast<unsigned long long>(v) & kValMask);
+}
+__device__ __forceinline__ void flag_store(unsigned long long* p, unsigned long long w) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long flag_load(const unsigned long long* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
 }
 
-// Grid (tiles, thresholds). counts[k * tiles + tile]
-template <typename T>
-__global__ void __launch_bounds__(kThreads)
-route_count_kernel(const T* __restrict__ conf, int64_t n, const double* __restrict__ thr,
-                   int32_t* __restrict__ counts) {
-    const int tile = blockIdx.x, k = blockIdx.y, tiles = gridDim.x;
-    const double t = thr[k];
-    const int64_t base = static_cast<int64_t>(tile) * kTile;
-    int mine = 0;
+// Exclusive prefix of this tile's count over tiles [0, tile) of one threshold
+// (warp 0 only; every lane returns it).
+__device__ long long look_back(const unsigned long long* flags, int tile, unsigned epoch) {
+    const int lane = threadIdx.x & 31;
+    long long excl = 0;
+    for (int base = tile - 1;; base -= 32) {
+        const int idx = base - lane;   // lane 0: the nearest predecessor
+        unsigned long long st = kStatusP, val = 0;
+        if (idx >= 0) {
+            unsigned long long w;
+            do {
+                w = flag_load(flags + idx);
+            } while ((w >> (kValBits + 2)) != epoch || ((w >> kValBits) & 3ull) == 0);
+            st = (w >> kValBits) & 3ull;
+            val = w & kValMask;
+        }
+        const unsigned pmask = __ballot_sync(0xffffffffu, st == kStatusP);
+        const int stop = pmask ? __ffs(pmask) - 1 : 32;
+        long long v = lane <= stop ? static_cast<long long>(val) : 0;
 #pragma unroll
-    for (int r = 0; r < kPerThread; ++r) {
-        const int64_t i = base + r * kThreads + threadIdx.x;
-        if (i < n && load_conf(conf, i) < t) ++mine;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    __shared__ int warp_sum[kThreads / 32];
-    if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = mine;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-#pragma unroll
-        for (int w = 0; w < kThreads / 32; ++w) s += warp_sum[w];
-        counts[static_cast<int64_t>(k) * tiles + tile] = s;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pmask) return excl;
     }
 }
 
-// kSingle: n fits one tile (n <= kTile, the light batches): no count pass, the
-// prefix of earlier tiles is 0 and the tile's own count is the total.
-template <typename T, bool kSingle = false>
+template <typename T>
 __global__ void __launch_bounds__(kThreads)
-route_scatter_kernel(const T* __restrict__ conf, int64_t n, const double* __restrict__ thr,
-                     const int32_t* __restrict__ counts, int64_t index_base,
-                     int64_t* __restrict__ heavy_idx, int64_t* __restrict__ total_out) {
+route_kernel(const T* __restrict__ conf, long long n, const double* __restrict__ thr,
+             unsigned long long* __restrict__ flags, unsigned epoch, long long index_base,
+             long long* __restrict__ heavy_idx, long long* __restrict__ total_out) {
+    using VT = Vec<T>;
+    constexpr int V = VT::V, R = kPerThread / V;
     const int tile = blockIdx.x, k = blockIdx.y, tiles = gridDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double t = thr[k];
-    const int32_t* ck = counts + static_cast<int64_t>(k) * tiles;
-    __shared__ long long s_prefix;
-    __shared__ int warp_cnt[kPerThread][kThreads / 32];
-    // exclusive prefix of earlier tiles (warp 0), and the grand total (last tile)
-    if (kSingle) {
-        if (threadIdx.x == 0) s_prefix = 0;
-    } else if (warp == 0) {
-        long long acc = 0;
-        for (int b = lane; b < tile; b += 32) acc += ck[b];
+    const long long base = static_cast<long long>(tile) * kTile;
+    __shared__ int warp_cnt[R][kWarps];
+    __shared__ long long s_excl;
+    // ingest (128-bit, striped) and the predicate
+    unsigned pred = 0;   // bit r*V + j
+    const bool full = base + kTile <= n && (reinterpret_cast<uintptr_t>(conf) % 16) == 0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-            s_prefix = acc;
-            if (tile == tiles - 1) total_out[k] = acc + ck[tile];
+    for (int r = 0; r < R; ++r) {
+        const long long e0 = base + static_cast<long long>(r) * kThreads * V + threadIdx.x * V;
+        double c[V];
+        if (full) {
+            VT::get(__ldg(reinterpret_cast<const typename VT::type*>(conf + e0)), c);
+        } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                c[j] = e0 + j < n ? static_cast<double>(__ldg(conf + e0 + j)) : 2.0;
         }
-    }
-    // Element order inside the tile: row r (kThreads wide), then thread.
-    const int64_t base = static_cast<int64_t>(tile) * kTile;
-    unsigned ballots[kPerThread];
 #pragma unroll
-    for (int r = 0; r < kPerThread; ++r) {
-        const int64_t i = base + r * kThreads + threadIdx.x;
-        const bool p = i < n && load_conf(conf, i) < t;
-        ballots[r] = __ballot_sync(0xffffffffu, p);
-        if (lane == 0) warp_cnt[r][warp] = __popc(ballots[r]);
+        for (int j = 0; j < V; ++j) pred |= (c[j] < t ? 1u : 0u) << (r * V + j);
+    }
+    // ballots -> per-warp row counts; the lane's rank inside its warp row
+    unsigned char rank_in_row[R][V];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        int before = 0, all = 0;
+        unsigned b[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            b[j] = __ballot_sync(0xffffffffu, (pred >> (r * V + j)) & 1u);
+            before += __popc(b[j] & lt);
+            all += __popc(b[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            rank_in_row[r][j] = static_cast<unsigned char>(before);
+            before += (pred >> (r * V + j)) & 1u;
+        }
+        if (lane == 0) warp_cnt[r][warp] = all;
     }
     __syncthreads();
-    // Offsets: all rows before r (all warps), then warps before `warp` in row r.
-    long long off = s_prefix;
-    int64_t* out = heavy_idx + static_cast<int64_t>(k) * n;
+    unsigned long long* fk = flags + static_cast<long long>(k) * tiles;
+    if (warp == 0) {
+        long long cnt = 0;
+        for (int i = lane; i < R * kWarps; i += 32) cnt += (&warp_cnt[0][0])[i];
 #pragma unroll
-    for (int r = 0; r < kPerThread; ++r) {
-        int before = 0, row = 0;
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        long long excl = 0;
+        if (tile == 0) {
+            if (lane == 0 && tiles > 1) flag_store(fk, flag_word(epoch, kStatusP, cnt));
+        } else {
+            if (lane == 0) flag_store(fk + tile, flag_word(epoch, kStatusA, cnt));
+            excl = look_back(fk, tile, epoch);
+            if (lane == 0 && tile < tiles - 1)
+                flag_store(fk + tile, flag_word(epoch, kStatusP, excl + cnt));
+        }
+        if (lane == 0) {
+            s_excl = excl;
+            if (tile == tiles - 1) total_out[k] = excl + cnt;
+        }
+    }
+    __syncthreads();
+    // scatter in id order
+    long long off = s_excl;
+    long long* out = heavy_idx + static_cast<long long>(k) * n;
 #pragma unroll
-        for (int w = 0; w < kThreads / 32; ++w) {
+    for (int r = 0; r < R; ++r) {
+        int wb = 0, row = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
             const int c = warp_cnt[r][w];
-            before += w < warp ? c : 0;
+            wb += w < warp ? c : 0;
             row += c;
         }
-        const unsigned b = ballots[r];
-        if ((b >> lane) & 1u) {
-            const int within = __popc(b & ((1u << lane) - 1u));
-            out[off + before + within] = index_base + base + r * kThreads + threadIdx.x;
-        }
+        const long long e0 = base + static_cast<long long>(r) * kThreads * V + threadIdx.x * V;
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            if ((pred >> (r * V + j)) & 1u) out[off + wb + rank_in_row[r][j]] = index_base + e0 + j;
         off += row;
     }
-    if (kSingle && threadIdx.x == 0) total_out[k] = off;
 }
 
 } // namespace
 
 extern "C" size_t ds_route_scratch_bytes(int64_t n, int32_t n_thresholds) {
-    const int64_t tiles = (n + kTile - 1) / kTile;
-    return dsi::align_up(sizeof(int32_t) * tiles * (n_thresholds > 0 ? n_thresholds : 1), 256);
+    (void)n;
+    (void)n_thresholds;
+    return 0;   // the look-back flags live in the context (epoch-tagged, reused)
 }
 
 namespace {
 
 ds_status route_launch(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t n,
                        const double* thresholds, int32_t nt, int64_t index_base,
-                       int64_t* heavy_idx, int64_t* counts, int32_t* scratch, cudaStream_t st) {
+                       int64_t* heavy_idx, int64_t* counts, cudaStream_t st) {
     const int64_t tiles = (n + kTile - 1) / kTile;
-    if (tiles > 0x7fffffff || nt > 65535)
-        return dsi::fail(DS_ERR_CAPACITY, "ds_route: too many tiles or thresholds");
+    if (tiles > 0x7fffffff || nt > 65535 || n >= (1ll << kValBits))
+        return dsi::fail(DS_ERR_CAPACITY, "ds_route: too many queries, tiles or thresholds");
+    // look-back flags: [nt][tiles] words in a context buffer, reused across
+    // launches through the epoch tag; zeroed on growth and on epoch wrap
+    const size_t need = sizeof(unsigned long long) * static_cast<size_t>(tiles) * nt;
+    if (need > ctx->route_flags_bytes || ctx->route_epoch + 1 >= (1u << kEpochBits)) {
+        if (need > ctx->route_flags_bytes) {
+            if (ctx->route_flags) {
+                DS_CUDA_TRY(cudaDeviceSynchronize());
+                DS_CUDA_TRY(cudaFree(ctx->route_flags));
+                ctx->route_flags = nullptr;
+                ctx->route_flags_bytes = 0;
+            }
+            const size_t want = dsi::align_up(need < (1u << 16) ? (1u << 16) : need, 1u << 16);
+            DS_CUDA_TRY(cudaMalloc(&ctx->route_flags, want));
+            ctx->route_flags_bytes = want;
+        }
+        DS_CUDA_TRY(cudaMemsetAsync(ctx->route_flags, 0, ctx->route_flags_bytes, st));
+        ctx->route_epoch = 0;
+    }
+    const unsigned epoch = ++ctx->route_epoch;
     dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nt));
-    if (tiles == 1) {   // one launch for a light batch
-        if (dtype == DS_CONF_F64)
-            route_scatter_kernel<double, true><<<grid, kThreads, 0, st>>>(
-                static_cast<const double*>(conf), n, thresholds, nullptr, index_base, heavy_idx,
-                counts);
-        else
-            route_scatter_kernel<float, true><<<grid, kThreads, 0, st>>>(
-                static_cast<const float*>(conf), n, thresholds, nullptr, index_base, heavy_idx,
-                counts);
-        DS_LAUNCH_CHECK(ctx, "route_scatter_kernel");
-        return DS_OK;
-    }
-    if (dtype == DS_CONF_F64) {
-        route_count_kernel<double><<<grid, kThreads, 0, st>>>(
-            static_cast<const double*>(conf), n, thresholds, scratch);
-        DS_LAUNCH_CHECK(ctx, "route_count_kernel");
-        route_scatter_kernel<double><<<grid, kThreads, 0, st>>>(
-            static_cast<const double*>(conf), n, thresholds, scratch, index_base, heavy_idx,
-            counts);
-    } else {
-        route_count_kernel<float><<<grid, kThreads, 0, st>>>(
-            static_cast<const float*>(conf), n, thresholds, scratch);
-        DS_LAUNCH_CHECK(ctx, "route_count_kernel");
-        route_scatter_kernel<float><<<grid, kThreads, 0, st>>>(
-            static_cast<const float*>(conf), n, thresholds, scratch, index_base, heavy_idx,
-            counts);
-    }
-    DS_LAUNCH_CHECK(ctx, "route_scatter_kernel");
+    auto* flags = static_cast<unsigned long long*>(ctx->route_flags);
+    if (dtype == DS_CONF_F64)
+        route_kernel<double><<<grid, kThreads, 0, st>>>(
+            static_cast<const double*>(conf), n, thresholds, flags, epoch, index_base,
+            reinterpret_cast<long long*>(heavy_idx), reinterpret_cast<long long*>(counts));
+    else
+        route_kernel<float><<<grid, kThreads, 0, st>>>(
+            static_cast<const float*>(conf), n, thresholds, flags, epoch, index_base,
+            reinterpret_cast<long long*>(heavy_idx), reinterpret_cast<long long*>(counts));
+    DS_LAUNCH_CHECK(ctx, "route_kernel");
     return DS_OK;
 }
 
 } // namespace
 
-// Device variant: `counts` must be device memory; scratch comes from the ctx
-// (stream-ordered, so callers on other streams must not overlap two calls).
+// Device variant: `counts` must be device memory. The look-back flags come
+// from the ctx (stream-ordered: calls on one ctx from several streams must not
+// overlap).
 extern "C" ds_status ds_route_device(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t n,
                                      const double* thresholds, int32_t nt, int64_t index_base,
                                      int64_t* heavy_idx, int64_t* counts, void* stream) {
@@ -176,11 +249,7 @@ extern "C" ds_status ds_route_device(ds_ctx* ctx, const void* conf, int32_t dtyp
         DS_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int64_t) * nt, st));
         return DS_OK;
     }
-    void* scratch = nullptr;
-    ds_status s = dsi::ensure_scratch(ctx, ds_route_scratch_bytes(n, nt), &scratch);
-    if (s != DS_OK) return s;
-    return route_launch(ctx, conf, dtype, n, thresholds, nt, index_base, heavy_idx, counts,
-                        static_cast<int32_t*>(scratch), st);
+    return route_launch(ctx, conf, dtype, n, thresholds, nt, index_base, heavy_idx, counts, st);
 }
 
 extern "C" ds_status ds_route(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t n,
@@ -199,19 +268,17 @@ extern "C" ds_status ds_route(ds_ctx* ctx, const void* conf, int32_t dtype, int6
     const size_t bc = dsi::align_up(esz * n, 256);
     const size_t bt = dsi::align_up(sizeof(double) * nt, 256);
     const size_t bk = dsi::align_up(sizeof(int64_t) * nt, 256);
-    const size_t bs = ds_route_scratch_bytes(n, nt);
     const size_t bi = dsi::align_up(sizeof(int64_t) * n * nt, 256);
     char* d = nullptr;
-    ds_status s = dsi::ensure_scratch(ctx, bc + bt + bk + bs + bi, reinterpret_cast<void**>(&d));
+    ds_status s = dsi::ensure_scratch(ctx, bc + bt + bk + bi, reinterpret_cast<void**>(&d));
     if (s != DS_OK) return s;
     DS_CUDA_TRY(cudaMemcpyAsync(d, conf, esz * n, cudaMemcpyHostToDevice, ctx->stream));
     DS_CUDA_TRY(cudaMemcpyAsync(d + bc, thresholds, sizeof(double) * nt, cudaMemcpyHostToDevice,
                                 ctx->stream));
     int64_t* dcounts = reinterpret_cast<int64_t*>(d + bc + bt);
-    int32_t* dscr = reinterpret_cast<int32_t*>(d + bc + bt + bk);
-    int64_t* didx = reinterpret_cast<int64_t*>(d + bc + bt + bk + bs);
+    int64_t* didx = reinterpret_cast<int64_t*>(d + bc + bt + bk);
     s = route_launch(ctx, d, dtype, n, reinterpret_cast<double*>(d + bc), nt, index_base, didx,
-                     dcounts, dscr, ctx->stream);
+                     dcounts, ctx->stream);
     if (s != DS_OK) return s;
     DS_CUDA_TRY(cudaMemcpyAsync(counts, dcounts, sizeof(int64_t) * nt, cudaMemcpyDeviceToHost,
                                 ctx->stream));

@@ -60,24 +60,21 @@ def global_offsets_device(counts, group=None):
 
 
 KEY_NONE = np.uint64(0xFFFFFFFFFFFFFFFF)
-_I64_MAX = np.int64(0x7FFFFFFFFFFFFFFF)
+_SIGN = np.uint64(0x8000000000000000)
 
 
 def keys_to_i64(keys: np.ndarray) -> np.ndarray:
-    """uint64 selection keys -> int64 with the same order for the reduction
-    (real keys are < 2^63: the threshold field is at most 2^23 wide; "none" =
-    2^64-1 maps to INT64_MAX)."""
+    """uint64 selection keys -> int64 with the same order for a signed MIN
+    reduction: flipping bit 63 maps unsigned order onto signed order for
+    every key (including keys >= 2^63 on grids longer than 2^23 points);
+    "none" = 2^64-1 lands on INT64_MAX."""
     k = np.asarray(keys, np.uint64)
-    out = k.astype(np.int64)
-    out[k == KEY_NONE] = _I64_MAX
-    return out
+    return (k ^ _SIGN).view(np.int64)
 
 
 def keys_from_i64(keys: np.ndarray) -> np.ndarray:
-    k = np.asarray(keys, np.int64)
-    out = k.astype(np.uint64)
-    out[k == _I64_MAX] = KEY_NONE
-    return out
+    k = np.ascontiguousarray(keys, np.int64)
+    return k.view(np.uint64) ^ _SIGN
 
 
 def plan_t_sharded(keys_fn, decode_fn, grid_len: int, group=None, device=None):
@@ -96,3 +93,59 @@ def plan_t_sharded(keys_fn, decode_fn, grid_len: int, group=None, device=None):
         mine = mine.to(device)
     dist.all_reduce(mine, op=dist.ReduceOp.MIN, group=group)
     return decode_fn(keys_from_i64(mine.cpu().numpy()))
+
+
+class TorchHostOps:
+    """ds_comm_ops over a torch.distributed process group (host tensors; gloo).
+
+    The host transport of native.Comm.host: the library stages device data
+    through pinned host memory and calls these. Used where NCCL cannot run --
+    several ranks sharing one GPU in the tests (NCCL refuses duplicate
+    devices), or hosts without NCCL."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def allgather(self, send: np.ndarray) -> np.ndarray:
+        import torch
+        import torch.distributed as dist
+        t = torch.from_numpy(np.ascontiguousarray(send, np.uint8))
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(parts, t, group=self.group)
+        return torch.cat(parts).numpy()
+
+    def allreduce_min_u64(self, buf: np.ndarray) -> np.ndarray:
+        import torch
+        import torch.distributed as dist
+        t = torch.from_numpy(keys_to_i64(buf).copy())
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return keys_from_i64(t.numpy())
+
+    def gatherv(self, send: np.ndarray, sizes, root: int):
+        import torch
+        import torch.distributed as dist
+        m = max(max(sizes), 1)
+        t = torch.zeros(m, dtype=torch.uint8)
+        if len(send):
+            t[:len(send)] = torch.from_numpy(np.ascontiguousarray(send, np.uint8))
+        if self.rank == root:
+            parts = [torch.empty(m, dtype=torch.uint8) for _ in range(self.world)]
+            dist.gather(t, parts, dst=root, group=self.group)
+            return np.concatenate([p.numpy()[:sizes[r]] for r, p in enumerate(parts)])
+        dist.gather(t, None, dst=root, group=self.group)
+        return None
+
+
+def nccl_comm(ctx, group=None):
+    """A native.Comm over NCCL for this process's rank of `group`: rank 0 makes
+    the unique id, torch.distributed broadcasts it, every rank initialises
+    (ncclCommInitRank on its context's device)."""
+    import torch.distributed as dist
+    from . import native
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    box = [native.Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return native.Comm.nccl(ctx, world, rank, box[0])

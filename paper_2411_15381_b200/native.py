@@ -54,8 +54,12 @@ class CapacityError(DsError):
     status = abi.ERR_CAPACITY
 
 
+class CommError(DsError):
+    status = abi.ERR_COMM
+
+
 _EXC = {c.status: c for c in (InvalidArgument, DomainError, InvariantError, OutOfRange,
-                              CudaError, NoDevice, CapacityError)}
+                              CudaError, NoDevice, CapacityError, CommError)}
 
 _lib = None
 c_p = ctypes.c_void_p
@@ -73,6 +77,7 @@ SIGNATURES = [
     ("ds_ctx_synchronize", ctypes.c_int, [c_p]),
     ("ds_ctx_launch_count", i64, [c_p]),
     ("ds_ctx_stream", c_p, [c_p]),
+    ("ds_ctx_take_error", ctypes.c_int, [c_p, c_p, ctypes.POINTER(i64)]),
     ("ds_plan_batch", ctypes.c_int, [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, c_p]),
     ("ds_plan_batch_device", ctypes.c_int, [c_p, c_p, i32, c_p, i32, c_p, c_p, i32, c_p, c_p]),
     ("ds_plan_validate", ctypes.c_int, [c_p, i32, c_p, i32, c_p, c_p, i32]),
@@ -109,7 +114,39 @@ SIGNATURES = [
     ("ds_format_queries_csv_device", ctypes.c_int, [c_p, c_p, i64, c_p, i64,
                                                     ctypes.POINTER(i64), c_p]),
     ("ds_format_g6", ctypes.c_int, [c_p, c_p, i64, c_p]),
+    # multi-GPU (ds_comm)
+    ("ds_comm_nccl_unique_id", ctypes.c_int, [c_p]),
+    ("ds_comm_init_nccl", ctypes.c_int, [c_p, i32, i32, c_p, ctypes.POINTER(c_p)]),
+    ("ds_comm_wrap_nccl", ctypes.c_int, [c_p, c_p, ctypes.POINTER(c_p)]),
+    ("ds_comm_init_all", ctypes.c_int, [c_p, i32, c_p]),
+    ("ds_comm_create_host", ctypes.c_int, [c_p, i32, i32, c_p, c_p, ctypes.POINTER(c_p)]),
+    ("ds_comm_destroy", ctypes.c_int, [c_p]),
+    ("ds_comm_rank", i32, [c_p]),
+    ("ds_comm_size", i32, [c_p]),
+    ("ds_shard_range", None, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+    ("ds_route_sharded_device", ctypes.c_int,
+     [c_p, c_p, c_p, i32, i64, c_p, i32, i64, c_p, c_p, c_p, c_p, c_p]),
+    ("ds_queue_gather_device", ctypes.c_int,
+     [c_p, c_p, i32, c_p, i64, c_p, i32, c_p, i64, c_p, c_p]),
+    ("ds_curve_observe_sharded_device", ctypes.c_int, [c_p, c_p, c_p, c_p, i32, c_p, f64, c_p]),
+    ("ds_plan_sharded_device", ctypes.c_int,
+     [c_p, c_p, c_p, i32, c_p, i32, c_p, c_p, i32, i32, i32, c_p, c_p]),
+    ("ds_comm_gather_device", ctypes.c_int,
+     [c_p, c_p, i32, c_p, ctypes.c_size_t, c_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t),
+      c_p]),
 ]
+
+# ds_comm_ops (include/ds_gpu.h): host-transport callbacks
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_p, c_p, ctypes.c_size_t, c_p)
+ALLREDUCE_MIN_U64_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
+                                        ctypes.c_size_t, c_p)
+GATHERV_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_p, c_p, ctypes.POINTER(ctypes.c_size_t),
+                              ctypes.c_int32, c_p)
+
+
+class CommOps(ctypes.Structure):
+    _fields_ = [("allgather", ALLGATHER_FN), ("allreduce_min_u64", ALLREDUCE_MIN_U64_FN),
+                ("gatherv", GATHERV_FN)]
 
 
 def lib():
@@ -164,6 +201,13 @@ class Context:
 
     def synchronize(self):
         check(lib().ds_ctx_synchronize(self.handle))
+
+    def take_error(self, stream: int = 0) -> int:
+        """Raises DomainError if a _device call met a confidence outside
+        [0, 1] since the last call (ds_ctx_take_error); returns -1 otherwise."""
+        v = i64(-1)
+        check(lib().ds_ctx_take_error(self.handle, c_p(stream), ctypes.byref(v)))
+        return int(v.value)
 
     # ---- planner ------------------------------------------------------
     def plan_batch(self, problems: np.ndarray, cascades: np.ndarray, grid_values: np.ndarray,
@@ -354,3 +398,150 @@ class Discriminator:
         check(lib().ds_disc_batch_complete_device(
             self.handle, c_p(images_ptr), n, h, w, c_p(conf_ptr), c_p(curve_ptr), decay,
             c_p(thr_ptr), nt, index_base, c_p(heavy_ptr), c_p(counts_ptr), c_p(stream)))
+
+
+class Comm:
+    """A ds_comm: the collectives of the sharded hot path (include/ds_gpu.h
+    "multi-GPU"). Made by Comm.nccl (one rank per GPU over NCCL; rank 0's
+    unique_id() distributed out of band) or Comm.host (caller callbacks: the
+    tests' several ranks on one GPU over gloo, dist.TorchHostOps)."""
+
+    def __init__(self, ctx: Context, handle, keepalive=None):
+        self.ctx = ctx
+        self.handle = handle
+        self._keep = keepalive
+        L = lib()
+        self.rank = int(L.ds_comm_rank(handle))
+        self.size = int(L.ds_comm_size(handle))
+
+    @staticmethod
+    def _nccl_first():
+        # The library dlopens "libnccl.so.2" and takes the process's copy if
+        # one is loaded. torch links its own (newer) NCCL under that soname:
+        # import it first, else the system NCCL would be loaded and torch's
+        # import would then bind to it (missing symbols).
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
+
+    @staticmethod
+    def unique_id() -> bytes:
+        Comm._nccl_first()
+        buf = (ctypes.c_uint8 * 128)()
+        check(lib().ds_comm_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, ctx: Context, nranks: int, rank: int, uid: bytes) -> "Comm":
+        if len(uid) != 128:
+            raise InvalidArgument("an NCCL unique id is 128 bytes")
+        cls._nccl_first()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        h = c_p()
+        check(lib().ds_comm_init_nccl(ctx.handle, nranks, rank, buf, ctypes.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def host(cls, ctx: Context, nranks: int, rank: int, impl) -> "Comm":
+        """impl.allgather(u8 array) -> u8 array of nranks*len; impl.allreduce_min_u64(u64
+        array) in place; impl.gatherv(u8 array, sizes, root) -> u8 array at root."""
+        import traceback
+
+        def view(ptr, n, ty=ctypes.c_uint8):
+            return np.ctypeslib.as_array((ty * n).from_address(ptr)) if n else \
+                np.zeros(0, np.uint8)
+
+        def ag(send, recv, nbytes, user):
+            try:
+                out = np.ascontiguousarray(impl.allgather(view(send, nbytes).copy()), np.uint8)
+                if out.nbytes != nbytes * nranks:
+                    return 1
+                ctypes.memmove(recv, out.ctypes.data, out.nbytes)
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        def ar(buf, count, user):
+            try:
+                a = np.ctypeslib.as_array(buf, shape=(count,))
+                a[:] = impl.allreduce_min_u64(a.copy())
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        def gv(send, recv, sizes, root, user):
+            try:
+                sz = [int(sizes[r]) for r in range(nranks)]
+                out = impl.gatherv(view(send, sz[rank]).copy(), sz, int(root))
+                if rank == root:
+                    out = np.ascontiguousarray(out, np.uint8)
+                    if out.nbytes != sum(sz):
+                        return 1
+                    if out.nbytes:
+                        ctypes.memmove(recv, out.ctypes.data, out.nbytes)
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 1
+
+        ops = CommOps(ALLGATHER_FN(ag), ALLREDUCE_MIN_U64_FN(ar), GATHERV_FN(gv))
+        h = c_p()
+        check(lib().ds_comm_create_host(ctx.handle, nranks, rank, ctypes.byref(ops), None,
+                                        ctypes.byref(h)))
+        return cls(ctx, h, keepalive=ops)
+
+    def close(self):
+        if self.handle:
+            lib().ds_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def shard_range(n: int, nranks: int, rank: int):
+        lo, hi = i64(0), i64(0)
+        lib().ds_shard_range(n, nranks, rank, ctypes.byref(lo), ctypes.byref(hi))
+        return int(lo.value), int(hi.value)
+
+    # ---- collective calls on device pointers (ints), stream-ordered -----------
+    def route(self, conf_ptr, dtype, n_local, thr_ptr, nt, index_base, heavy_ptr, counts_ptr,
+              offsets_ptr=0, totals_ptr=0, stream=0):
+        check(lib().ds_route_sharded_device(
+            self.ctx.handle, self.handle, c_p(conf_ptr), dtype, n_local, c_p(thr_ptr), nt,
+            index_base, c_p(heavy_ptr), c_p(counts_ptr), c_p(offsets_ptr or None),
+            c_p(totals_ptr or None), c_p(stream or None)))
+
+    def gather_queues(self, root, heavy_ptr, n_local, counts_ptr, nt, global_ptr=0,
+                      global_stride=0, global_counts_ptr=0, stream=0):
+        check(lib().ds_queue_gather_device(
+            self.ctx.handle, self.handle, root, c_p(heavy_ptr or None), n_local, c_p(counts_ptr),
+            nt, c_p(global_ptr or None), global_stride, c_p(global_counts_ptr or None),
+            c_p(stream or None)))
+
+    def curve_observe(self, curve_ptr, conf_ptr, dtype, shard_sizes, decay, stream=0):
+        sizes = np.ascontiguousarray(shard_sizes, np.int64)
+        if len(sizes) != self.size:
+            raise InvalidArgument("one shard size per rank")
+        check(lib().ds_curve_observe_sharded_device(
+            self.ctx.handle, self.handle, c_p(curve_ptr), c_p(conf_ptr or None), dtype,
+            abi.ptr(sizes), decay, c_p(stream or None)))
+
+    def plan(self, problems_ptr, n, cascades_ptr, n_cascades, grid_ptr, offs_ptr, n_grids, t_lo,
+             t_hi, out_ptr, stream=0):
+        check(lib().ds_plan_sharded_device(
+            self.ctx.handle, self.handle, c_p(problems_ptr), n, c_p(cascades_ptr), n_cascades,
+            c_p(grid_ptr), c_p(offs_ptr), n_grids, t_lo, t_hi, c_p(out_ptr), c_p(stream or None)))
+
+    def gather(self, root, send_ptr, nbytes, recv_ptr=0, capacity=0, stream=0) -> int:
+        total = ctypes.c_size_t(0)
+        check(lib().ds_comm_gather_device(
+            self.ctx.handle, self.handle, root, c_p(send_ptr or None), nbytes,
+            c_p(recv_ptr or None), capacity, ctypes.byref(total), c_p(stream or None)))
+        return int(total.value)

@@ -11,6 +11,8 @@
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 from . import abi
@@ -94,8 +96,18 @@ def full_grid(step: float = 0.01) -> np.ndarray:
 
 
 def make_grid(step: float = 0.01) -> np.ndarray:
-    """Simulation's grid (cluster.cpp:20-28): k/n with n = lround(1/step)."""
-    n = int(np.round(1.0 / step))
+    """Simulation's grid (cluster.cpp:20-28): k/n with n = lround(1/step).
+
+    std::lround rounds halves away from zero (np.round would round them to
+    even: step 0.4 gives n = 3 here as in the reference, not 2); a step
+    outside (0, 1] raises like the reference's std::invalid_argument."""
+    if not (step > 0.0) or step > 1.0:
+        raise ValueError("threshold grid step must be in (0, 1]")
+    x = 1.0 / step
+    n = math.floor(x)
+    if x - n >= 0.5:     # exact for x >= 1
+        n += 1
+    n = int(n)
     return np.asarray([k / n for k in range(n + 1)], np.float64)
 
 

@@ -209,6 +209,60 @@ def test_t_sharded_planner_argmin_equals_reference(world, name):
     assert np.array_equal(got != ddist.KEY_NONE, grid_mode & (want["feasible"] == 1))
     assert found >= 5
     # keys in int64 for the reduction keep the unsigned order
-    k = np.array([0, 5, 2**62, int(ddist.KEY_NONE)], np.uint64)
+    # (keys at and above 2^63 arise on grids longer than 2^23 points)
+    k = np.array([0, 5, 2**62, 2**63 - 1, 2**63, 2**63 + 7, 2**64 - 2, int(ddist.KEY_NONE)],
+                 np.uint64)
     assert np.array_equal(ddist.keys_from_i64(ddist.keys_to_i64(k)), k)
-    assert list(np.argsort(ddist.keys_to_i64(k))) == [0, 1, 2, 3]
+    assert list(np.argsort(ddist.keys_to_i64(k))) == list(range(len(k)))
+    assert ddist.keys_to_i64(k)[-1] == np.iinfo(np.int64).max
+
+
+def _host_ops_worker(rank, world, port, q):
+    """dist.TorchHostOps -- the ds_comm_ops host transport of native.Comm.host --
+    over gloo: the byte/key semantics the C library relies on."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ops = ddist.TorchHostOps()
+        mine = np.arange(6, dtype=np.uint8) + 10 * rank
+        ag = ops.allgather(mine)
+        keys = np.array([2**64 - 1, 2**63 + rank, 5 + (world - rank), 2**62 * (rank + 1) % 2**64,
+                         2**63 - 1 - rank], np.uint64)
+        mn = ops.allreduce_min_u64(keys.copy())
+        sizes = [3 * r for r in range(world)]          # rank 0 sends nothing
+        send = np.full(sizes[rank], rank + 1, np.uint8)
+        gv = ops.gatherv(send, sizes, world - 1)
+        q.put((rank, ag, mn, gv))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_torch_host_ops(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_host_ops_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, ag, mn, gv = q.get(timeout=120)
+        res[r] = (ag, mn, gv)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_ag = np.concatenate([np.arange(6, dtype=np.uint8) + 10 * r for r in range(world)])
+    keys = [np.array([2**64 - 1, 2**63 + r, 5 + (world - r), 2**62 * (r + 1) % 2**64,
+                      2**63 - 1 - r], np.uint64) for r in range(world)]
+    want_mn = np.minimum.reduce(keys)
+    want_gv = np.concatenate([np.full(3 * r, r + 1, np.uint8) for r in range(world)])
+    for r in range(world):
+        ag, mn, gv = res[r]
+        assert np.array_equal(ag, want_ag)
+        assert np.array_equal(mn, want_mn) and mn.dtype == np.uint64
+        if r == world - 1:
+            assert np.array_equal(gv, want_gv)
+        else:
+            assert gv is None

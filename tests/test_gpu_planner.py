@@ -29,6 +29,7 @@ def ctx():
                                       ("alloc_random_2024", "want_solve"),
                                       ("accept_c1", "want_solve"),
                                       ("config4", "want_solve"),
+                                      ("config4_bench", "want_solve"),
                                       ("wide_random", "want")])
 def test_planner_matches_reference_goldens(ctx, golden, name, key):
     g = golden(name)

@@ -265,6 +265,31 @@ def test_curve_segmented_invalid_confidence_stops_at_it(ctx):
     torch.cuda.synchronize()
     got = dcur.cpu().numpy().view(abi.CURVE)[0]
     _assert_same_bits(got, _port_curve(curve, conf[:123_457], 0.999))
+    # the device call recorded where the reference would have thrown
+    with pytest.raises(DomainError, match="123457"):
+        ctx.take_error()
+    assert ctx.take_error() == -1   # cleared
+
+
+@pytest.mark.parametrize("n,bad", [(40, 17), (5_000, 0), (5_000, 4_999)])
+def test_curve_device_invalid_confidence_recorded(ctx, n, bad):
+    """Short sequences (single-CTA replay): same stop point, same record."""
+    import torch
+    from paper_2411_15381_b200 import native
+    conf = np.random.default_rng(n + bad).random(n)
+    conf[bad] = -0.25
+    curve = workloads.uniform_prior()
+    dconf = torch.from_numpy(conf).cuda()
+    dcur = torch.from_numpy(curve.reshape(1).view(np.uint8).copy()).cuda()
+    torch.cuda.synchronize()
+    assert ctx.take_error() == -1
+    native.check(native.lib().ds_curve_observe_device(
+        ctx.handle, native.c_p(dcur.data_ptr()), native.c_p(dconf.data_ptr()), abi.CONF_F64,
+        n, 0.999, None))
+    torch.cuda.synchronize()
+    _assert_same_bits(dcur.cpu().numpy().view(abi.CURVE)[0], _port_curve(curve, conf[:bad], 0.999))
+    with pytest.raises(DomainError, match=f"observation {bad} "):
+        ctx.take_error()
 
 
 @pytest.mark.parametrize("n", [5_000, 40_000])

@@ -26,6 +26,7 @@ def port_plan(problems, cascades, gvals, goffs, threads=4):
                                       ("alloc_random_2024", "want_solve"),
                                       ("accept_c1", "want_solve"),
                                       ("config4", "want_solve"),
+                                      ("config4_bench", "want_solve"),
                                       ("wide_random", "want")])
 def test_port_planner_matches_reference_goldens(golden, name, key):
     g = golden(name)
