@@ -27,10 +27,11 @@ struct ds_ctx {
     // _device calls cannot return the reference's domain_error at launch time
     // (ds_ctx_take_error reads and clears it)
     long long* d_err = nullptr;
-    // K2's decoupled look-back flags ([thresholds][tiles] epoch-tagged words)
+    // K2's decoupled look-back flags ([thresholds][tiles] words + a done
+    // counter; every launch leaves them zero)
     void* route_flags = nullptr;
     size_t route_flags_bytes = 0;
-    unsigned route_epoch = 0;
+    unsigned route_attr_set = 0;   // bit per tile size: smem attribute set
 };
 
 namespace dsi {
