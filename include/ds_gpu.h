@@ -404,6 +404,26 @@ ds_status ds_disc_batch_complete_device(ds_disc* disc, const uint8_t* nhwc, int6
                                         int32_t n_thresholds, int64_t index_base,
                                         int64_t* heavy_idx, int64_t* counts, void* stream);
 
+/* A backlog of light batches in one call: batch b is images
+ * [batch_offsets[b], batch_offsets[b+1]) (device array of n_batches + 1
+ * nondecreasing offsets, 0 .. n_images), completed in order as
+ * handle_batch_complete (cluster.cpp:288-307) completes them one by one:
+ * every confidence observed into the curve in order, batch b routed at ITS
+ * threshold thresholds[b] (device, one per batch: the plan in force when it
+ * completes) into heavy_idx[batch_offsets[b] .. + counts[b]) (global ids
+ * index_base + image index). Bit-identical to n_batches calls of
+ * ds_disc_batch_complete_device (the discriminator's confidences do not
+ * depend on the batch split), but one discriminator launch streams all the
+ * batches' tiles, so small batches keep every SM busy (config 1: batches of
+ * 32). A confidence outside [0, 1] stops the curve and the routing at that
+ * query (later batches: counts 0) and is recorded as in ds_ctx_take_error. */
+ds_status ds_disc_batches_complete_device(ds_disc* disc, const uint8_t* nhwc, int64_t n_images,
+                                          const int64_t* batch_offsets, int32_t n_batches,
+                                          int32_t h, int32_t w, float* conf, ds_curve* curve,
+                                          double decay, const double* thresholds,
+                                          int64_t index_base, int64_t* heavy_idx,
+                                          int64_t* counts, void* stream);
+
 /* Synthetic image pool: pixel bytes are a pure
  * function of (seed, image id, pixel index); generated on the device. */
 ds_status ds_synth_images_device(ds_ctx* ctx, uint64_t seed, uint64_t id0, int64_t n,

@@ -823,22 +823,48 @@ ds_status launch(ds_ctx* ctx, ds_curve* dcurve, const void* conf, int32_t dtype,
 // outside [0, 1] stops the replay where the reference would throw and is
 // recorded in the context (ds_ctx_take_error); the host-buffer variant
 // reports it as DS_ERR_DOMAIN directly.
+namespace dsi {
+
+// ds_curve_observe_device that also hands back the device word holding the
+// first invalid observation's index (INT_MAX if none): valid until the next
+// use of the context scratch (ds_disc_batches_complete_device reads it in
+// the very next launch to stop routing where the reference would throw).
+ds_status curve_observe_device_bad(ds_ctx* ctx, ds_curve* curve, const void* conf, int32_t dtype,
+                                   int64_t n, double decay, cudaStream_t st, const int** bad) {
+    if (!ctx || !curve) return fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (dtype != DS_CONF_F64 && dtype != DS_CONF_F32)
+        return fail(DS_ERR_INVALID_ARGUMENT, "unknown confidence dtype");
+    if (!(decay > 0.0) || !(decay <= 1.0))
+        return fail(DS_ERR_DOMAIN, "curve decay must lie in (0, 1]");
+    const SpecPlan plan = spec_plan(ctx, n > 0 ? n : 1, dtype, decay);
+    void* scratch = nullptr;
+    ds_status s = ensure_scratch(ctx, 256 + plan.bytes, &scratch);
+    if (s != DS_OK) return s;
+    if (bad) *bad = static_cast<const int*>(scratch);
+    if (n <= 0) {   // nothing observed: no invalid index
+        static const int kNone = 0x7fffffff;
+        DS_CUDA_TRY(cudaMemcpyAsync(scratch, &kNone, sizeof(int), cudaMemcpyHostToDevice, st));
+        return DS_OK;
+    }
+    return launch(ctx, curve, conf, dtype, n, decay, static_cast<int*>(scratch), plan,
+                  static_cast<char*>(scratch) + 256, st, ctx->d_err);
+}
+
+} // namespace dsi
+
 extern "C" ds_status ds_curve_observe_device(ds_ctx* ctx, ds_curve* curve, const void* conf,
                                              int32_t dtype, int64_t n, double decay,
                                              void* stream) {
     if (!ctx || !curve) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
-    if (dtype != DS_CONF_F64 && dtype != DS_CONF_F32)
-        return dsi::fail(DS_ERR_INVALID_ARGUMENT, "unknown confidence dtype");
-    if (!(decay > 0.0) || !(decay <= 1.0))
-        return dsi::fail(DS_ERR_DOMAIN, "curve decay must lie in (0, 1]");
-    if (n <= 0) return DS_OK;
+    if (n <= 0) {
+        if (dtype != DS_CONF_F64 && dtype != DS_CONF_F32)
+            return dsi::fail(DS_ERR_INVALID_ARGUMENT, "unknown confidence dtype");
+        if (!(decay > 0.0) || !(decay <= 1.0))
+            return dsi::fail(DS_ERR_DOMAIN, "curve decay must lie in (0, 1]");
+        return DS_OK;
+    }
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-    const SpecPlan plan = spec_plan(ctx, n, dtype, decay);
-    void* scratch = nullptr;
-    ds_status s = dsi::ensure_scratch(ctx, 256 + plan.bytes, &scratch);
-    if (s != DS_OK) return s;
-    return launch(ctx, curve, conf, dtype, n, decay, static_cast<int*>(scratch), plan,
-                  static_cast<char*>(scratch) + 256, st, ctx->d_err);
+    return dsi::curve_observe_device_bad(ctx, curve, conf, dtype, n, decay, st, nullptr);
 }
 
 extern "C" ds_status ds_curve_observe(ds_ctx* ctx, ds_curve* curve, const void* conf,

@@ -748,16 +748,25 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 umma_commit_pair(&B.h2_free, 0x3);
                 umma_commit_pair(&B.acc3_full, 0x3);
             }
+            if (P.trace && blockIdx.x == 0)   // debug: the MMA issuer is done
+                P.trace[(0 * kTraceTiles + 7) * 16 + 0] = static_cast<long long>(globaltimer());
         }
     }
+    __syncwarp();   // single-lane roles (warps 12-14) rejoin their warps
     tc_fence_before();
     __syncthreads();
-    if (P.trace && threadIdx.x == 0)
-        P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
     cluster_sync();     // both CTAs done with TMEM / remote barriers
+    if (P.trace && threadIdx.x == 0 && blockIdx.x == 0)
+        P.trace[(0 * kTraceTiles + 7) * 16 + 1] = static_cast<long long>(globaltimer());
     if (warp == 13) {
         tc_fence_after();
         tmem_dealloc2<512>(tmem);
+        // debug: this CTA's end (a stamp after the CTA barrier by thread 0 is
+        // not one: bar.sync counts a warp as arrived when any of its lanes
+        // arrives, and lanes 1-31 of the MMA warp get there while lane 0 is
+        // still issuing the last tile)
+        if (P.trace && lane == 0)
+            P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
     }
 }
 
@@ -853,6 +862,45 @@ batch_tail_kernel(const float* __restrict__ part, int n, int tpi, int tokens, fl
         }
         if (tid == 0) counts[k] = off;
     }
+}
+
+// A backlog of light batches after one discriminator launch and one curve
+// replay over all their confidences (ds_disc_batches_complete_device): batch
+// b = queries [off[b], off[b+1]) routed at ITS threshold thr[b]
+// (Policy::defers, strict <) into heavy[off[b] ..], counts[b] -- one CTA per
+// batch. Queries at or after the first invalid confidence (*bad, from the
+// replay) are not routed, as the reference's throw out of
+// handle_batch_complete would leave them.
+constexpr int kSegThreads = 128;
+__global__ void __launch_bounds__(kSegThreads)
+segmented_route_kernel(const float* __restrict__ conf, const long long* __restrict__ off,
+                       const double* __restrict__ thr, const int* __restrict__ bad,
+                       long long index_base, long long* __restrict__ heavy,
+                       long long* __restrict__ counts) {
+    __shared__ int wcnt[kSegThreads / 32];
+    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long lo = off[b], first_bad = static_cast<long long>(*bad);
+    long long hi = off[b + 1];
+    if (hi > first_bad) hi = first_bad > lo ? first_bad : lo;
+    const double t = thr[b];
+    long long pos = 0;
+    for (long long base = lo; base < hi; base += kSegThreads) {
+        const long long i = base + tid;
+        const bool p = i < hi && static_cast<double>(conf[i]) < t;
+        const unsigned bal = __ballot_sync(0xffffffffu, p);
+        __syncthreads();   // wcnt of the previous chunk consumed
+        if (lane == 0) wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int before = 0, all = 0;
+#pragma unroll
+        for (int w = 0; w < kSegThreads / 32; ++w) {
+            before += w < warp ? wcnt[w] : 0;
+            all += wcnt[w];
+        }
+        if (p) heavy[lo + pos + before + __popc(bal & ((1u << lane) - 1u))] = index_base + i;
+        pos += all;
+    }
+    if (tid == 0) counts[b] = pos;
 }
 
 // ---- deterministic weights ---------------------------------------------------------
@@ -1214,6 +1262,35 @@ extern "C" ds_status ds_disc_batch_complete_device(ds_disc* d, const uint8_t* nh
     BatchTail tail{curve, decay, thresholds, nt, static_cast<long long>(index_base),
                    reinterpret_cast<long long*>(heavy_idx), reinterpret_cast<long long*>(counts)};
     return launch_disc(d, nhwc, n, h, w, conf, 0, st, nullptr, &tail);
+}
+
+extern "C" ds_status ds_disc_batches_complete_device(ds_disc* d, const uint8_t* nhwc,
+                                                     int64_t n_images, const int64_t* batch_offsets,
+                                                     int32_t n_batches, int32_t h, int32_t w,
+                                                     float* conf, ds_curve* curve, double decay,
+                                                     const double* thresholds, int64_t index_base,
+                                                     int64_t* heavy_idx, int64_t* counts,
+                                                     void* stream) {
+    if (!d || !curve || n_batches < 0 || n_images < 0 ||
+        (n_images > 0 && (!nhwc || !conf || !heavy_idx)) ||
+        (n_batches > 0 && (!batch_offsets || !thresholds || !counts)))
+        return dsi::fail(DS_ERR_INVALID_ARGUMENT, "null argument");
+    if (!(decay > 0.0) || !(decay <= 1.0))
+        return dsi::fail(DS_ERR_DOMAIN, "curve decay must lie in (0, 1]");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+    ds_status s = DS_OK;
+    if (n_images > 0) s = launch_disc(d, nhwc, n_images, h, w, conf, 0, st);
+    const int* bad = nullptr;
+    if (s == DS_OK)
+        s = dsi::curve_observe_device_bad(d->ctx, curve, conf, DS_CONF_F32, n_images, decay, st,
+                                          &bad);
+    if (s != DS_OK || n_batches == 0) return s;
+    segmented_route_kernel<<<static_cast<unsigned>(n_batches), kSegThreads, 0, st>>>(
+        conf, reinterpret_cast<const long long*>(batch_offsets), thresholds, bad,
+        static_cast<long long>(index_base), reinterpret_cast<long long*>(heavy_idx),
+        reinterpret_cast<long long*>(counts));
+    DS_LAUNCH_CHECK(d->ctx, "segmented_route_kernel");
+    return DS_OK;
 }
 
 // Host-buffer entry: the image upload is pipelined with scoring -- chunks of

@@ -50,6 +50,11 @@ ds_status ensure_copy_stream(ds_ctx* ctx);
 // Stream-ordered reset of ctx->d_err to LLONG_MAX.
 ds_status reset_device_error(ds_ctx* ctx, cudaStream_t st);
 
+// ds_curve_observe_device + the device word with the first invalid index
+// (curve.cu).
+ds_status curve_observe_device_bad(ds_ctx* ctx, ds_curve* curve, const void* conf, int32_t dtype,
+                                   int64_t n, double decay, cudaStream_t st, const int** bad);
+
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 } // namespace dsi

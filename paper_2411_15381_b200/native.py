@@ -101,6 +101,8 @@ SIGNATURES = [
     ("ds_disc_score_device", ctypes.c_int, [c_p, c_p, i64, i32, i32, c_p, c_p]),
     ("ds_disc_batch_complete_device", ctypes.c_int,
      [c_p, c_p, i64, i32, i32, c_p, c_p, f64, c_p, i32, i64, c_p, c_p, c_p]),
+    ("ds_disc_batches_complete_device", ctypes.c_int,
+     [c_p, c_p, i64, c_p, i32, i32, i32, c_p, c_p, f64, c_p, i64, c_p, c_p, c_p]),
     ("ds_synth_images_device", ctypes.c_int, [c_p, u64, u64, i64, i32, i32, c_p, c_p]),
     ("ds_generate_arrivals", ctypes.c_int, [c_p, c_p, i32, f64, u64, i32, c_p, i64,
                                             ctypes.POINTER(i64)]),
@@ -390,6 +392,16 @@ class Discriminator:
                      stream: int = 0):
         check(lib().ds_disc_score_device(self.handle, c_p(images_ptr), n, h, w, c_p(conf_ptr),
                                          c_p(stream)))
+
+    def batches_complete_device(self, images_ptr: int, n_images: int, offsets_ptr: int,
+                                n_batches: int, h: int, w: int, conf_ptr: int, curve_ptr: int,
+                                decay: float, thr_ptr: int, index_base: int, heavy_ptr: int,
+                                counts_ptr: int, stream: int = 0):
+        """A backlog of light batches in order (ds_disc_batches_complete_device)."""
+        check(lib().ds_disc_batches_complete_device(
+            self.handle, c_p(images_ptr), n_images, c_p(offsets_ptr), n_batches, h, w,
+            c_p(conf_ptr), c_p(curve_ptr), decay, c_p(thr_ptr), index_base, c_p(heavy_ptr),
+            c_p(counts_ptr), c_p(stream)))
 
     def batch_complete_device(self, images_ptr: int, n: int, h: int, w: int, conf_ptr: int,
                               curve_ptr: int, decay: float, thr_ptr: int, nt: int,

@@ -207,3 +207,57 @@ def test_batch_complete_equals_separate_calls(disc, n, h, w, nt):
     for k in range(nt):
         t = thr.cpu().numpy()[k]
         assert np.array_equal(h1[k], np.flatnonzero(c1.astype(np.float64) < t) + 1000)
+
+
+@pytest.mark.parametrize("sizes_seed", [1, 2])
+def test_batches_complete_equals_batch_by_batch(disc, sizes_seed):
+    """ds_disc_batches_complete_device (a backlog of light batches in one call)
+    gives the bits of one ds_disc_batch_complete_device call per batch, in
+    order, each at its own threshold: confidences, the curve after every
+    observation (cluster.cpp:288-307 order) and each batch's heavy ids."""
+    import torch
+    from paper_2411_15381_b200 import workloads
+    rng = np.random.default_rng(sizes_seed)
+    sizes = rng.integers(1, 41, size=23)
+    sizes[5] = 0   # an empty batch in the middle
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(offs[-1])
+    thr = rng.random(len(sizes))
+    thr[3] = 0.0
+    thr[4] = 1.0
+    imgs = torch.from_numpy(disc_oracle.synth_images(5, 17, n, 512, 512).reshape(-1)).cuda()
+    prior = workloads.uniform_prior()
+    dthr = torch.from_numpy(thr).cuda()
+    results = []
+    for backlog in (False, True):
+        conf = torch.empty(n, dtype=torch.float32, device="cuda")
+        cur = torch.from_numpy(prior.reshape(1).view(np.uint8).copy()).cuda()
+        heavy = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+        cnt = torch.full((len(sizes),), -1, dtype=torch.int64, device="cuda")
+        doffs = torch.from_numpy(offs).cuda()
+        torch.cuda.synchronize()
+        if backlog:
+            disc.batches_complete_device(imgs.data_ptr(), n, doffs.data_ptr(), len(sizes), 512,
+                                         512, conf.data_ptr(), cur.data_ptr(), 0.999,
+                                         dthr.data_ptr(), 500, heavy.data_ptr(), cnt.data_ptr())
+        else:
+            for b in range(len(sizes)):
+                o = int(offs[b])
+                disc.batch_complete_device(imgs.data_ptr() + o * 512 * 512 * 3, int(sizes[b]),
+                                           512, 512, conf.data_ptr() + 4 * o, cur.data_ptr(),
+                                           0.999, dthr.data_ptr() + 8 * b, 1, 500 + o,
+                                           heavy.data_ptr() + 8 * o, cnt.data_ptr() + 8 * b)
+        torch.cuda.synchronize()
+        c = cnt.cpu().numpy()
+        hv = heavy.cpu().numpy()
+        results.append((conf.cpu().numpy(), cur.cpu().numpy().tobytes(), c,
+                        [hv[offs[b]:offs[b] + c[b]] for b in range(len(sizes))]))
+    (c0, v0, n0, h0), (c1, v1, n1, h1) = results
+    assert np.array_equal(c0.view(np.uint32), c1.view(np.uint32))
+    assert v0 == v1
+    assert np.array_equal(n0, n1)
+    for b in range(len(sizes)):
+        assert np.array_equal(h0[b], h1[b]), b
+        want = 500 + offs[b] + np.flatnonzero(c0[offs[b]:offs[b + 1]].astype(np.float64) < thr[b])
+        assert np.array_equal(h1[b], want), b
+    assert n1[3] == 0 and n1[5] == 0 and n1[4] == sizes[4]
