@@ -1242,8 +1242,8 @@ def cpu_legs(line, args, c_host, prior, gpu_curve, pro, cas, grid, goffs, gpu_pl
         np.array_equal(li[:int(cnt[0])], lheavy_host))
     line["latent"]["parity_vs_cpu"] = {
         "queries": CPU_LATENT_SAMPLE, "max_rel_err": float(rel.max()),
-        "bit_identical": int((g == lconf_cpu).sum()),
-        "within_1e-12": bool(rel.max() <= 1e-12),
+        "bit_identical": int((g.view(np.uint64) == lconf_cpu.view(np.uint64)).sum()),
+        "all_bit_identical": bool(np.array_equal(g.view(np.uint64), lconf_cpu.view(np.uint64))),
         "heavy_ids_equal": bool(np.array_equal(gl, lidx_cpu))}
     wv, wav, wk, wa = cpu_workload_leg(threads)
     line["workload"]["cpu_baseline"] = {

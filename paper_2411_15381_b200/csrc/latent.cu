@@ -12,12 +12,13 @@
 //
 // fp64 arithmetic is written with explicit _rn intrinsics in the reference's
 // evaluation order (no FMA contraction). sqrt is correctly rounded on both
-// sides; log and cos are CUDA's (<= 1-2 ulp vs glibc), so confidences match
-// the reference to a few ulp and routing/binning decisions are identical
-// except inside that band (tests/test_gpu_score_route.py counts both).
+// sides; log and cos are glibc's FMA builds restated operation by operation
+// (glibc_libm.h), so every confidence and quality value is bit-identical to
+// the reference's (tests/test_gpu_score_route.py requires all of them).
 #include <cuda_runtime.h>
 
 #include "ds_internal.h"
+#include "glibc_libm.h"
 
 namespace {
 
@@ -83,7 +84,10 @@ __device__ __forceinline__ double box_muller(uint64_t r1, uint64_t r2) { // rng.
     const double u2 = uniform53(r2);
     if (u1 <= 0.0) u1 = 0x1.0p-53;
     // 2.0 * M_PI * u2 == (2.0 * M_PI) * u2; 2*pi is exact in double
-    return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
+    // log and cos exactly as glibc's FMA builds compute them (glibc_libm.h):
+    // the draw is bit-identical to the reference's
+    return __dmul_rn(__dsqrt_rn(__dmul_rn(-2.0, glibc_log(u1))),
+                     glibc_cos(__dmul_rn(6.283185307179586, u2)));
 }
 
 // kRecords: write full Query records (workload.cpp:121-128) instead of the
