@@ -77,6 +77,8 @@ def ref():
         lib.dsref_gen_accept_c1.argtypes = [u64, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p,
                                             c_p]
         lib.dsref_gen_c2_recipe.argtypes = [c_p, ctypes.c_int, u64, ctypes.c_int, c_p]
+        lib.dsref_policy_run.argtypes = [i32, f64, f64, i32, f64, c_p, i32, c_p, c_p, i32, c_p,
+                                         c_p, u64, c_p, c_p, c_p]
         _ref = lib
     return _ref
 

@@ -202,6 +202,43 @@ int dsref_plan_batch(const ds_problem* problems, int32_t n, const ds_cascade* ca
     return 0;
 }
 
+// One run of a Policy from make_policy (policies.cpp:198-219) -- the
+// reference's per-kind control logic -- over n ticks: tick i calls
+// plan(problems[i]) -> out[i], then observe_batch(ev_model[i] (0 light,
+// 1 heavy), ev_timeout[i]) and records live_batch(light/heavy) ->
+// live[2i], live[2i+1], and entry_stage(out[i], rng) -> entry[i] (0 light,
+// 1 heavy) from RandomStream(seed, "entry").
+int dsref_policy_run(int32_t kind, double peak, double fixed_t, int32_t add_step, double mult,
+                     const ds_problem* problems, int32_t n, const ds_cascade* cascade,
+                     const double* grid, int32_t g, const int32_t* ev_model,
+                     const int32_t* ev_timeout, uint64_t seed, ds_plan* out, int32_t* live,
+                     int32_t* entry) {
+    try {
+        PolicyParams pp;
+        pp.kind = static_cast<PolicyKind>(kind);
+        pp.peak_demand_qps = peak;
+        pp.fixed_threshold = fixed_t;
+        pp.aimd_add_step = add_step;
+        pp.aimd_mult_factor = mult;
+        std::unique_ptr<Policy> pol = make_policy(pp);
+        CascadeProfile c = to_cascade(*cascade);
+        RandomStream rng(seed, "entry");
+        for (int i = 0; i < n; ++i) {
+            AllocationProblem p = to_problem(problems[i], &c, grid, g);
+            AllocationPlan pl = pol->plan(p);
+            out[i] = from_plan(pl);
+            pol->observe_batch(ev_model[i] ? ModelKind::heavy : ModelKind::light,
+                               ev_timeout[i] != 0);
+            live[2 * i] = pol->live_batch(ModelKind::light);
+            live[2 * i + 1] = pol->live_batch(ModelKind::heavy);
+            entry[i] = pol->entry_stage(pl, rng) == ModelKind::heavy ? 1 : 0;
+        }
+        return 0;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 // Predicates, for property tests (allocator.cpp:129-151).
 int dsref_latency_feasible(const ds_problem* dp, const ds_cascade* c, const double* grid, int g,
                            int b1, int b2, int* out) {

@@ -24,7 +24,8 @@ __all__ = ["ModelProfile", "DeferralCurve", "CascadeProfile", "QueueState", "All
            "solve_even_split", "solve_batch", "sample_query", "sample_queries",
            "observe_confidences", "route", "InvalidArgument", "DomainError", "InvariantError",
            "OutOfRange", "CapacityError", "default_context", "Policy", "make_policy",
-           "PolicyParams", "Trace", "POISSON", "UNIFORM", "generate_arrivals",
+           "PolicyParams", "POLICY_KINDS", "LIGHT", "HEAVY", "aimd_update", "Trace",
+           "POISSON", "UNIFORM", "generate_arrivals",
            "sample_query_records", "fmt6", "write_csv"]
 
 _ctx: Context | None = None
@@ -301,17 +302,67 @@ class PolicyParams:                        # policies.hpp:62-68
     aimd_mult_factor: float = 0.5
 
 
+LIGHT, HEAVY = "light", "heavy"            # ModelKind, policies.hpp:25
+POLICY_KINDS = ("diffserve", "diffserve_static", "clipper_light", "clipper_heavy",
+                "proteus_like", "abl_static_threshold", "abl_aimd_batching",
+                "abl_no_queuing_model")     # PolicyKind, policies.hpp:11-20
+
+
+def aimd_update(m: ModelProfile, current_batch: int, slo_timeout: bool, add_step: int,
+                mult_factor: float) -> int:
+    """aimd_update (policies.cpp:45-59): multiplicative decrease to the largest
+    profiled batch <= b * mult on an SLO timeout, else additive increase to the
+    smallest profiled batch >= b + add (capped at the largest)."""
+    sizes = m.batch_sizes()
+    if slo_timeout:
+        target = current_batch * mult_factor
+        nxt = sizes[0]
+        for b in sizes:
+            if b <= target:
+                nxt = b
+        return nxt
+    want = current_batch + add_step
+    for b in sizes:
+        if b >= want:
+            return b
+    return sizes[-1]
+
+
 class Policy:
-    """The reference's plugin API; plan() runs on the GPU planner."""
+    """The reference's plugin API (policies.hpp:30-60) for every PolicyKind
+    make_policy knows (policies.cpp:63-219); plan() runs on the GPU planner
+    (K1), the per-kind control logic -- Clipper's one frozen solve, Proteus'
+    fix-ups and random entry stage, AIMD's batch state -- is the reference's."""
 
     def __init__(self, params: PolicyParams):
+        if params.kind not in POLICY_KINDS:
+            raise InvalidArgument(f"unknown policy kind '{params.kind}'")
         self.params = params
+        self._frozen = None            # Clipper: the one solve, frozen (policies.cpp:98-110)
+        self._cascade = None           # AIMD state (policies.cpp:157-183)
+        self._b1 = self._b2 = 0
 
     def kind(self) -> str:
         return self.params.kind
 
+    def entry_stage(self, plan: AllocationPlan, rng=None) -> str:
+        """policies.cpp:31-35 (light), 92-94 (Clipper), 123-128 (Proteus:
+        uniform over hosted variants via rng.bernoulli(0.5))."""
+        k = self.params.kind
+        if k == "clipper_light":
+            return LIGHT
+        if k == "clipper_heavy":
+            return HEAVY
+        if k == "proteus_like":
+            if plan.x1 > 0 and plan.x2 > 0:
+                if rng is None:
+                    raise InvalidArgument("proteus_like entry_stage needs a random stream")
+                return HEAVY if rng.bernoulli(0.5) else LIGHT
+            return HEAVY if plan.x2 > 0 else LIGHT
+        return LIGHT
+
     def defers(self, confidence: float, threshold: float) -> bool:     # policies.cpp:37-39
-        if self.params.kind in ("clipper_light", "clipper_heavy", "proteus_like"):
+        if not self.uses_discriminator():
             return False
         return confidence < threshold
 
@@ -324,10 +375,18 @@ class Policy:
             return solve(p)
         if k == "diffserve_static":
             return solve_static_peak(p, self.params.peak_demand_qps)
-        if k == "abl_static_threshold":
-            return solve_pinned_threshold(p, self.params.fixed_threshold)
-        if k == "abl_no_queuing_model":
-            return solve(dataclasses.replace(p, queuing="twice_exec"))
+        if k in ("clipper_light", "clipper_heavy"):
+            if self._frozen is None:
+                light = k == "clipper_light"
+                m = p.cascade.light if light else p.cascade.heavy
+                out = solve_single_model(m, light, p.total_servers, self.params.peak_demand_qps,
+                                         p.overprovision_lambda, p.cascade.slo_seconds)
+                if light:
+                    out.b2 = p.cascade.heavy.min_batch()
+                else:
+                    out.b1 = p.cascade.light.min_batch()
+                self._frozen = out
+            return dataclasses.replace(self._frozen)
         if k == "proteus_like":
             out = solve_even_split(p)
             if out.b1 == 0:
@@ -335,7 +394,31 @@ class Policy:
             if out.b2 == 0:
                 out.b2 = p.cascade.heavy.min_batch()
             return out
-        raise InvalidArgument(f"policy '{k}' has no GPU plan() in this build")
+        if k == "abl_static_threshold":
+            return solve_pinned_threshold(p, self.params.fixed_threshold)
+        if k == "abl_aimd_batching":
+            self._cascade = p.cascade
+            if self._b1 == 0:          # slow start at the smallest profiled batches
+                self._b1 = p.cascade.light.min_batch()
+                self._b2 = p.cascade.heavy.min_batch()
+            return solve_fixed_batches(p, self._b1, self._b2)
+        # abl_no_queuing_model (policies.cpp:188-192)
+        return solve(dataclasses.replace(p, queuing="twice_exec"))
+
+    def observe_batch(self, model: str, slo_timeout: bool) -> None:    # policies.cpp:166-172
+        if self.params.kind != "abl_aimd_batching" or self._cascade is None or self._b1 == 0:
+            return
+        if model == LIGHT:
+            self._b1 = aimd_update(self._cascade.light, self._b1, slo_timeout,
+                                   self.params.aimd_add_step, self.params.aimd_mult_factor)
+        else:
+            self._b2 = aimd_update(self._cascade.heavy, self._b2, slo_timeout,
+                                   self.params.aimd_add_step, self.params.aimd_mult_factor)
+
+    def live_batch(self, model: str) -> int:                           # policies.cpp:175-177
+        if self.params.kind != "abl_aimd_batching":
+            return 0
+        return self._b1 if model == LIGHT else self._b2
 
 
 def make_policy(params: PolicyParams) -> Policy:                       # policies.cpp:198

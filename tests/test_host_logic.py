@@ -26,3 +26,14 @@ def test_make_grid_uses_lround(step):
 def test_make_grid_rejects_bad_step(step):
     with pytest.raises(ValueError):
         workloads.make_grid(step)
+
+
+def test_aimd_update_rule():
+    """aimd_update (policies.cpp:45-59), host side of api.Policy."""
+    from paper_2411_15381_b200 import api
+    m = api.ModelProfile("l", {1: 0.1, 2: 0.13, 4: 0.18, 8: 0.3, 16: 0.52})
+    assert api.aimd_update(m, 16, True, 1, 0.5) == 8
+    assert api.aimd_update(m, 1, True, 1, 0.5) == 1
+    assert api.aimd_update(m, 4, False, 1, 0.5) == 8
+    assert api.aimd_update(m, 16, False, 1, 0.5) == 16
+    assert api.aimd_update(m, 2, False, 3, 0.5) == 8
