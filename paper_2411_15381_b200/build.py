@@ -26,7 +26,7 @@ EXACT_FP64 = {"plan_sweep.cu", "latent.cu", "curve.cu", "route.cu", "arrivals.cu
 
 SOURCES = ["ds_ctx.cu", "plan_sweep.cu", "latent.cu", "route.cu", "curve.cu", "disc.cu",
            "synth.cu", "arrivals.cu", "csv.cu", "comm.cu"]
-HEADERS = ["ds_internal.h", "sm100.cuh", "fdlibm_log1p.h", "fmt6.h", "glibc_libm.h",
+HEADERS = ["ds_internal.h", "sm100.cuh", "lookback.cuh", "fdlibm_log1p.h", "fmt6.h", "glibc_libm.h",
            "glibc_libm_data.h"]
 
 

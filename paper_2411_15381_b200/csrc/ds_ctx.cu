@@ -58,6 +58,26 @@ ds_status ensure_pinned(ds_ctx* ctx, size_t bytes, void** out) {
     return DS_OK;
 }
 
+ds_status lookback_flags(ds_ctx* ctx, size_t words, unsigned long long** flags, unsigned** done) {
+    const size_t need = sizeof(unsigned long long) * words + 256;
+    if (need > ctx->route_flags_bytes) {
+        if (ctx->route_flags) {
+            DS_CUDA_TRY(cudaDeviceSynchronize());
+            DS_CUDA_TRY(cudaFree(ctx->route_flags));
+            ctx->route_flags = nullptr;
+            ctx->route_flags_bytes = 0;
+        }
+        const size_t want = align_up(need < (1u << 16) ? (1u << 16) : need, 1u << 16);
+        DS_CUDA_TRY(cudaMalloc(&ctx->route_flags, want));
+        DS_CUDA_TRY(cudaMemset(ctx->route_flags, 0, want));
+        ctx->route_flags_bytes = want;
+    }
+    *flags = static_cast<unsigned long long*>(ctx->route_flags);
+    *done = reinterpret_cast<unsigned*>(static_cast<char*>(ctx->route_flags) +
+                                        ctx->route_flags_bytes - 256);
+    return DS_OK;
+}
+
 ds_status reset_device_error(ds_ctx* ctx, cudaStream_t st) {
     static const long long kNone = 0x7fffffffffffffffLL;
     // pageable source: staged before the call returns

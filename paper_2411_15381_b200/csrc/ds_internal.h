@@ -27,8 +27,8 @@ struct ds_ctx {
     // _device calls cannot return the reference's domain_error at launch time
     // (ds_ctx_take_error reads and clears it)
     long long* d_err = nullptr;
-    // K2's decoupled look-back flags ([thresholds][tiles] words + a done
-    // counter; every launch leaves them zero)
+    // decoupled look-back flags of K2 / K9 (lookback.cuh): words + a done
+    // counter, zero at allocation and left zero by every launch
     void* route_flags = nullptr;
     size_t route_flags_bytes = 0;
     unsigned route_attr_set = 0;   // bit per tile size: smem attribute set
@@ -46,6 +46,10 @@ ds_status cuda_fail(cudaError_t e, const char* what);
 ds_status ensure_scratch(ds_ctx* ctx, size_t bytes, void** out);
 ds_status ensure_pinned(ds_ctx* ctx, size_t bytes, void** out);
 ds_status ensure_copy_stream(ds_ctx* ctx);
+
+// At least `words` zeroed look-back flag words and the done counter
+// (lookback.cuh; grow-only, shared by the launches of one context).
+ds_status lookback_flags(ds_ctx* ctx, size_t words, unsigned long long** flags, unsigned** done);
 
 // Stream-ordered reset of ctx->d_err to LLONG_MAX.
 ds_status reset_device_error(ds_ctx* ctx, cudaStream_t st);

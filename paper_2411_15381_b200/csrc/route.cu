@@ -38,16 +38,16 @@
 #include <vector>
 
 #include "ds_internal.h"
+#include "lookback.cuh"
 
 namespace {
+
+using namespace dslb;
 
 constexpr int kThreads = 256;                  // element threads (8 warps)
 constexpr int kBlock = kThreads + 32;          // + one control warp: count, look-back
 constexpr int kPerThreadMax = 32;              // confidences per thread (<= 32: one bit each)
 constexpr int kWarps = kThreads / 32;
-constexpr unsigned long long kValBits = 62, kValMask = (1ull << kValBits) - 1;
-constexpr unsigned long long kStatusA = 1, kStatusP = 2;
-
 template <typename T> struct Vec;
 template <> struct Vec<double> {
     using type = double2;
@@ -61,83 +61,6 @@ template <> struct Vec<float> {
         o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
     }
 };
-
-__device__ __forceinline__ unsigned long long flag_word(unsigned long long st, long long v) {
-    return (st << kValBits) | (static_cast<unsigned long long>(v) & kValMask);
-}
-__device__ __forceinline__ void flag_store(unsigned long long* p, unsigned long long w) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
-}
-__device__ __forceinline__ unsigned long long flag_load(const unsigned long long* p) {
-    unsigned long long w;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
-    return w;
-}
-
-// Exclusive prefix of this tile's count over tiles [0, tile) of one threshold
-// (warp 0 only; every lane returns it). Each round reads the 128 nearest
-// unread predecessors (4 per lane, all loads in flight together) and stops at
-// the nearest inclusive prefix (P); tiles without one contribute their count.
-__device__ long long look_back(const unsigned long long* flags, int tile) {
-    const int lane = threadIdx.x & 31;
-    long long excl = 0;
-    for (int base = tile - 1;; base -= 128) {
-        unsigned long long st[4], val[4];
-        unsigned ready = 0;   // bit q: flag q read (all four loads in flight together)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            st[q] = kStatusP;
-            val[q] = 0;
-            if (base - (4 * lane + q) < 0) ready |= 1u << q;   // before tile 0: P of 0
-        }
-        while (ready != 0xFu) {
-            unsigned long long w[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (!((ready >> q) & 1u)) w[q] = flag_load(flags + (base - (4 * lane + q)));
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (!((ready >> q) & 1u) && (w[q] >> kValBits) != 0) {
-                    st[q] = (w[q] >> kValBits) & 3ull;
-                    val[q] = w[q] & kValMask;
-                    ready |= 1u << q;
-                }
-        }
-        int first_p = 4;
-#pragma unroll
-        for (int q = 3; q >= 0; --q)
-            if (st[q] == kStatusP) first_p = q;
-        const unsigned pmask = __ballot_sync(0xffffffffu, first_p < 4);
-        const int stop = pmask ? __ffs(pmask) - 1 : 32;
-        long long v = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (lane < stop || (lane == stop && q <= first_p)) v += static_cast<long long>(val[q]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += v;
-        if (pmask) return excl;
-    }
-}
-
-// Every CTA's look-back reads are done when it retires; the last of the
-// launch zeroes the [nt][tiles] flags and the counter for the next launch.
-__device__ __forceinline__ void retire(unsigned long long* flags, unsigned* done, int tiles) {
-    if (tiles == 1) return;   // a single tile per threshold uses no flags
-    __shared__ bool s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned total = gridDim.x * gridDim.y;
-        s_last = atomicAdd(done, 1u) == total - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const long long words = static_cast<long long>(tiles) * gridDim.y;
-    for (long long i = threadIdx.x; i < words; i += blockDim.x) flags[i] = 0ull;
-    if (threadIdx.x == 0) *done = 0u;
-}
 
 template <typename T, int kPerThread>
 __global__ void __launch_bounds__(kBlock)
@@ -328,26 +251,12 @@ ds_status route_launch_pt(ds_ctx* ctx, const void* conf, int32_t dtype, int64_t 
     const int64_t tiles = (n + kTile - 1) / kTile;
     if (tiles > 0x7fffffff || nt > 65535)
         return dsi::fail(DS_ERR_CAPACITY, "ds_route: too many tiles or thresholds");
-    // look-back flags: [nt][tiles] words + the done counter in a context
-    // buffer; zero at allocation, left zero by every launch (retire)
-    const size_t need = sizeof(unsigned long long) * static_cast<size_t>(tiles) * nt + 256;
-    if (need > ctx->route_flags_bytes) {
-        if (ctx->route_flags) {
-            DS_CUDA_TRY(cudaDeviceSynchronize());
-            DS_CUDA_TRY(cudaFree(ctx->route_flags));
-            ctx->route_flags = nullptr;
-            ctx->route_flags_bytes = 0;
-        }
-        const size_t want = dsi::align_up(need < (1u << 16) ? (1u << 16) : need, 1u << 16);
-        DS_CUDA_TRY(cudaMalloc(&ctx->route_flags, want));
-        DS_CUDA_TRY(cudaMemset(ctx->route_flags, 0, want));
-        ctx->route_flags_bytes = want;
-    }
+    unsigned long long* flags = nullptr;
+    unsigned* done = nullptr;
+    ds_status s = dsi::lookback_flags(ctx, static_cast<size_t>(tiles) * nt, &flags, &done);
+    if (s != DS_OK) return s;
     static const int exp = getenv("DS_ROUTE_EXP") ? atoi(getenv("DS_ROUTE_EXP")) : 0;
-    auto* done = reinterpret_cast<unsigned*>(static_cast<char*>(ctx->route_flags) +
-                                             ctx->route_flags_bytes - 256);
     dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(nt));
-    auto* flags = static_cast<unsigned long long*>(ctx->route_flags);
     constexpr int kSmem = (kTile + 32) * sizeof(long long);   // + one dummy slot per lane
     if (kSmem > 48 * 1024 && !(ctx->route_attr_set & (1u << (PT / 8)))) {   // once per device
         DS_CUDA_TRY(cudaFuncSetAttribute(route_kernel<double, PT>,
