@@ -171,13 +171,9 @@ ds_status check_comm(ds_ctx* ctx, ds_comm* c) {
 // ---- the three transport primitives ------------------------------------------
 
 // recv[r * bytes .. ] = rank r's send (device buffers; send may alias nothing in recv)
+// (NCCL is called even with one rank, so the one-GPU tests run the NCCL path.)
 ds_status allgather(ds_comm* c, const void* send, void* recv, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return DS_OK;
-    if (c->nranks == 1) {
-        if (send != recv)
-            DS_CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
-        return DS_OK;
-    }
     if (c->use_nccl) {
         DS_NCCL_TRY(nccl().AllGather(send, recv, bytes, ncclUint8, c->nc, st), "ncclAllGather");
         return DS_OK;
@@ -185,6 +181,11 @@ ds_status allgather(ds_comm* c, const void* send, void* recv, size_t bytes, cuda
     char* h = nullptr;
     ds_status s = comm_host(c, bytes * (c->nranks + 1), &h);
     if (s != DS_OK) return s;
+    if (c->nranks == 1) {
+        if (send != recv)
+            DS_CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
+        return DS_OK;
+    }
     DS_CUDA_TRY(cudaMemcpyAsync(h, send, bytes, cudaMemcpyDeviceToHost, st));
     DS_CUDA_TRY(cudaStreamSynchronize(st));
     if (c->ops.allgather(h, h + bytes, bytes, c->user) != 0)
@@ -195,12 +196,13 @@ ds_status allgather(ds_comm* c, const void* send, void* recv, size_t bytes, cuda
 }
 
 ds_status allreduce_min_u64(ds_comm* c, uint64_t* buf, size_t count, cudaStream_t st) {
-    if (count == 0 || c->nranks == 1) return DS_OK;
+    if (count == 0) return DS_OK;
     if (c->use_nccl) {
         DS_NCCL_TRY(nccl().AllReduce(buf, buf, count, ncclUint64, ncclMin, c->nc, st),
                     "ncclAllReduce");
         return DS_OK;
     }
+    if (c->nranks == 1) return DS_OK;
     char* h = nullptr;
     ds_status s = comm_host(c, count * 8, &h);
     if (s != DS_OK) return s;
