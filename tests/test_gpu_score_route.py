@@ -338,3 +338,84 @@ def test_curve_segmented_replay_in_cuda_graph(ctx):
     torch.cuda.synchronize()
     assert cur.cpu().numpy().tobytes() == eager
     _assert_same_bits(cur.cpu().numpy().view(abi.CURVE)[0], _port_curve(prior, conf, 0.999))
+
+
+def _port_route(conf, thr, base):
+    n = len(conf)
+    c64 = np.ascontiguousarray(conf, np.float64)
+    idx = np.zeros(len(thr) * max(n, 1), np.int64)
+    cnt = np.zeros(len(thr), np.int64)
+    lib.port().dso_route(abi.ptr(c64), n, abi.ptr(thr), len(thr), base, abi.ptr(idx),
+                         abi.ptr(cnt))
+    return cnt, [idx[k * n: k * n + cnt[k]] for k in range(len(thr))]
+
+
+@pytest.mark.parametrize("n", [8191, 8192, 8193, 3 * 8192 + 5, 1_048_583, 2_100_001])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_route_single_pass_tiles_vs_port(ctx, n, dtype):
+    """K2's single pass around its 8,192-query tiles and past 128 tiles (more
+    than one look-back round), NaN and boundary confidences included."""
+    rng = np.random.default_rng(n + 3)
+    conf = rng.random(n).astype(dtype)
+    conf[::5] = 0.5
+    conf[3::17] = np.nan                    # NaN < t is false: never deferred
+    thr = np.array([0.5, 0.0, 1.0, 0.731], np.float64)
+    counts, lists = ctx.route(conf, thr, index_base=7)
+    want_cnt, want = _port_route(conf, thr, 7)
+    assert np.array_equal(counts, want_cnt)
+    for k in range(len(thr)):
+        assert np.array_equal(lists[k], want[k]), k
+
+
+def test_route_many_thresholds_many_tiles(ctx):
+    conf = np.random.default_rng(9).random(50_000)
+    thr = workloads.make_grid(0.01)
+    counts, lists = ctx.route(conf, thr, index_base=123)
+    want_cnt, want = _port_route(conf, thr, 123)
+    assert np.array_equal(counts, want_cnt)
+    assert all(np.array_equal(a, b) for a, b in zip(lists, want))
+
+
+def test_route_device_misaligned_and_graph_replays(ctx):
+    """A confidence pointer that is not 16-byte aligned (scalar loads), and
+    the same launch replayed from a CUDA graph on changing data: the look-back
+    flags are left clean by every launch."""
+    import torch
+    from paper_2411_15381_b200 import native
+    L = native.lib()
+    n = 70_001
+    base = torch.from_numpy(np.random.default_rng(1).random(n + 1).astype(np.float32)).cuda()
+    thr = torch.tensor([0.5, 0.25], dtype=torch.float64, device="cuda")
+    heavy = torch.empty(2 * n, dtype=torch.int64, device="cuda")
+    cnt = torch.empty(2, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+
+    def launch(stream):
+        native.check(L.ds_route_device(ctx.handle, native.c_p(base.data_ptr() + 4), abi.CONF_F32,
+                                       n, native.c_p(thr.data_ptr()), 2, 0,
+                                       native.c_p(heavy.data_ptr()), native.c_p(cnt.data_ptr()),
+                                       native.c_p(stream)))
+
+    def check():
+        c = base[1:].cpu().numpy()
+        want_cnt, want = _port_route(c, np.array([0.5, 0.25]), 0)
+        got = cnt.cpu().numpy()
+        assert np.array_equal(got, want_cnt)
+        h = heavy.cpu().numpy().reshape(2, n)
+        for k in range(2):
+            assert np.array_equal(h[k, :got[k]], want[k])
+
+    s = torch.cuda.Stream()
+    launch(s.cuda_stream)
+    torch.cuda.synchronize()
+    check()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        launch(s.cuda_stream)
+    for seed in range(3):
+        base.copy_(torch.from_numpy(np.random.default_rng(seed + 10).random(n + 1)
+                                    .astype(np.float32)))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        check()
