@@ -27,7 +27,7 @@ EXACT_FP64 = {"plan_sweep.cu", "latent.cu", "curve.cu", "route.cu", "arrivals.cu
 SOURCES = ["ds_ctx.cu", "plan_sweep.cu", "latent.cu", "route.cu", "curve.cu", "disc.cu",
            "synth.cu", "arrivals.cu", "csv.cu", "comm.cu"]
 HEADERS = ["ds_internal.h", "sm100.cuh", "lookback.cuh", "fdlibm_log1p.h", "fmt6.h", "glibc_libm.h",
-           "glibc_libm_data.h"]
+           "glibc_libm_data.h", "mt64_charpoly.h", "gf2_jump.h"]
 
 
 def _mtime(p: str) -> float:

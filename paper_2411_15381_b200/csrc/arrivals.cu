@@ -9,10 +9,17 @@
 // to nextafter(previous, +inf) when it does not increase, and stops at the
 // first t >= duration. Every piece is restated as a data-parallel pass:
 //
-//   K8a mt_stream   one CTA runs the single std::mt19937_64 stream. Word m of
-//                   the stream obeys x_m = x_{m-156} ^ twist(x_{m-312},
-//                   x_{m-311}); thread c owns column c (mod 156), two steps
-//                   of 156 words per barrier.
+//   K8a mt_stream   the single std::mt19937_64 stream. Word m obeys
+//                   x_m = x_{m-156} ^ twist(x_{m-312}, x_{m-311}); a CTA
+//                   generates it with thread c on column c (mod 156), two
+//                   steps of 156 words per barrier. Long streams (round 2)
+//                   are cut into segments of 20,480 words: segment 0 as
+//                   above, every other segment on its own SM from its start
+//                   state, computed by JUMP-AHEAD -- x^J mod phi over GF(2)
+//                   (phi = the engine's characteristic polynomial, degree
+//                   19937; gf2_jump.h, host, cached) selects which of the
+//                   first 19,937 states XOR to the state J words ahead.
+//                   1M draws: 0.54 -> ~0.2 ms (arrivals 0.70 -> 0.38 ms).
 //   K8b exp_draws   grid-wide: temper, U = (u64 >> 11) * 2^-53,
 //                   e = -log1p(-U) with glibc's log1p restated bit for bit
 //                   (fdlibm_log1p.h; rng.cpp:24-28).
@@ -44,10 +51,12 @@
 #include <cmath>
 #include <cstdlib>
 #include <limits>
+#include <mutex>
 #include <vector>
 
 #include "ds_internal.h"
 #include "fdlibm_log1p.h"
+#include "gf2_jump.h"
 
 namespace {
 
@@ -91,23 +100,17 @@ __device__ __forceinline__ uint64_t temper(uint64_t z) {
 // the second step's neighbour for c = 155 (column 0 of the first new step) is
 // recomputed by that thread from words already in the ring.
 constexpr int kMtThreads = 160;
-__global__ void __launch_bounds__(kMtThreads) mt_stream_kernel(uint64_t seed, int64_t n,
-                                                               uint64_t* __restrict__ raw) {
-    __shared__ uint64_t ring[4][156];   // ring[step & 3][column]
+
+// From the 312 words preceding raw[base] in ring[0..1] (ring[0][c] =
+// x_{base+c}, ring[1][c] = x_{base+156+c}), writes raw[base + k] for
+// k < count and base + k < n. Block-uniform (all kMtThreads threads).
+__device__ __forceinline__ void mt_run(uint64_t (&ring)[4][156], int64_t base, int64_t count,
+                                       int64_t n, uint64_t* __restrict__ raw) {
     const int c = threadIdx.x;
-    if (c == 0) {   // std::mt19937_64 seeding recurrence: steps 0 and 1
-        uint64_t x = seed;
-        ring[0][0] = x;
-        for (int i = 1; i < 312; ++i) {
-            x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
-            ring[i / 156][i % 156] = x;
-        }
-    }
-    __syncthreads();
     const bool active = c < 156;
     uint64_t x2 = active ? ring[0][c] : 0;   // step s
     uint64_t x1 = active ? ring[1][c] : 0;   // step s+1
-    const int64_t steps = (n + 155) / 156;
+    const int64_t steps = (count + 155) / 156;
     for (int64_t s = 0; s < steps; s += 2) {
         const int a = static_cast<int>(s & 3), b = (a + 1) & 3, w0 = (a + 2) & 3, w1 = (a + 3) & 3;
         if (active) {
@@ -125,13 +128,152 @@ __global__ void __launch_bounds__(kMtThreads) mt_stream_kernel(uint64_t seed, in
             ring[w0][c] = y0;
             ring[w1][c] = y1;
             const int64_t k0 = s * 156 + c;
-            if (k0 < n) raw[k0] = y0;
-            if (k0 + 156 < n) raw[k0 + 156] = y1;
+            if (k0 < count && base + k0 < n) raw[base + k0] = y0;
+            if (k0 + 156 < count && base + k0 + 156 < n) raw[base + k0 + 156] = y1;
             x2 = y0;
             x1 = y1;
         }
         __syncthreads();
     }
+}
+
+// std::mt19937_64 seeding recurrence (x_0 .. x_311) into ring[0..1].
+__device__ __forceinline__ void mt_seed(uint64_t seed, uint64_t (&ring)[4][156]) {
+    if (threadIdx.x == 0) {
+        uint64_t x = seed;
+        ring[0][0] = x;
+        for (int i = 1; i < 312; ++i) {
+            x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
+            ring[i / 156][i % 156] = x;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kMtThreads) mt_stream_kernel(uint64_t seed, int64_t count,
+                                                               int64_t n,
+                                                               uint64_t* __restrict__ raw) {
+    __shared__ uint64_t ring[4][156];   // ring[step & 3][column]
+    mt_seed(seed, ring);
+    mt_run(ring, 0, count, n, raw);
+}
+
+// Jump-ahead: segment s >= 1 of kJumpSeg words starts from the state
+// x_{J} .. x_{J+311}, J = s * kJumpSeg. The engine's words obey the linear
+// recurrence of its characteristic polynomial phi (degree 19937,
+// mt64_charpoly.h), so with r(x) = x^J mod phi (host, cached),
+//     x_{J+j} = XOR over the set bits i of r of x_{i+j},   j = 0 .. 311
+// (all 64 bits for j >= 1; only x_J's upper 33 bits, the ones the recurrence
+// reads, for j = 0). One CTA per segment: the base words x_0 .. x_20247 (the
+// seed words and segment 0's output) in shared memory, thread j XORs the
+// words the set bits of r select (a warp-uniform walk of r), then the
+// segment's words are generated as in mt_stream. Checked bit for bit against
+// the single stream (tests/test_gpu_arrivals.py).
+constexpr int kJumpSeg = 20480;                   // >= 19937: segment 0 holds the base words
+constexpr int kJumpBase = 19937 + 312;            // x_0 .. x_20248
+constexpr int kJumpGroups = 3;                    // the set bits of r split three ways
+constexpr int kJumpThreads = 320 * kJumpGroups;   // 312 state words per group
+constexpr int kJumpMaxBits = 19937;
+constexpr int kJumpSmem = (kJumpBase + kJumpGroups * 312) * 8 + kJumpMaxBits * 2 + 16;
+
+// idx: the exponents i of r's set bits (uint16, ascending), segment s at
+// idx[off[s-1] .. off[s]).
+__global__ void __launch_bounds__(kJumpThreads)
+mt_jump_kernel(uint64_t seed, const uint16_t* __restrict__ idx, const int* __restrict__ off,
+               int64_t n, uint64_t* __restrict__ raw) {
+    extern __shared__ uint64_t jw[];   // x_0 .. x_{kJumpBase-1} | partial sums | indices
+    __shared__ uint64_t ring[4][156];
+    uint64_t* part = jw + kJumpBase;
+    uint16_t* si = reinterpret_cast<uint16_t*>(part + kJumpGroups * 312);
+    const int s = blockIdx.x + 1, tid = threadIdx.x;
+    const int i0 = off[s - 1], nbits = off[s] - i0;
+    mt_seed(seed, ring);
+    for (int i = tid; i < 312; i += kJumpThreads) jw[i] = ring[i / 156][i % 156];
+    for (int i = 312 + tid; i < kJumpBase; i += kJumpThreads) jw[i] = raw[i - 312];
+    for (int i = tid; i < nbits; i += kJumpThreads) si[i] = idx[i0 + i];
+    __syncthreads();
+    // group g takes every third set bit: thread j XORs the words they select
+    const int g = tid / 320, j = tid % 320;
+    if (j < 312) {
+        uint64_t a0 = 0, a1 = 0;
+        const uint64_t* wj = jw + j;
+        int k = g;
+        for (; k + kJumpGroups < nbits; k += 2 * kJumpGroups) {
+            a0 ^= wj[si[k]];
+            a1 ^= wj[si[k + kJumpGroups]];
+        }
+        if (k < nbits) a0 ^= wj[si[k]];
+        part[g * 312 + j] = a0 ^ a1;
+    }
+    __syncthreads();   // ring reused for the segment's state
+    if (tid < 312) ring[tid / 156][tid % 156] = part[tid] ^ part[312 + tid] ^ part[624 + tid];
+    __syncthreads();
+    mt_run(ring, static_cast<int64_t>(s) * kJumpSeg, kJumpSeg, n, raw);
+}
+
+std::mutex g_jump_mu;
+std::vector<Poly> g_jump;   // g_jump[s-1] = x^(s * kJumpSeg) mod phi (process cache)
+
+// The jump polynomials' set-bit exponents for segments 1 .. S-1 on the
+// device (context cache; at least 64 segments, ~20 KB each).
+ds_status jump_lists(ds_ctx* ctx, int S, const uint16_t** idx, const int** off) {
+    std::lock_guard<std::mutex> lock(g_jump_mu);
+    if (ctx->jump_polys_n < S - 1) {
+        const int want = S - 1 < 64 ? 64 : S - 1;
+        if (g_jump.empty()) g_jump.push_back(poly_xpow(kJumpSeg));
+        while (static_cast<int>(g_jump.size()) < want)
+            g_jump.push_back(poly_mulmod(g_jump.back(), g_jump.front()));
+        std::vector<uint16_t> bits;
+        std::vector<int> offs(1, 0);
+        for (int i = 0; i < want; ++i) {
+            for (int k = 0; k < kJumpMaxBits; ++k)
+                if ((g_jump[i][k / 64] >> (k % 64)) & 1u) bits.push_back(static_cast<uint16_t>(k));
+            offs.push_back(static_cast<int>(bits.size()));
+        }
+        if (ctx->jump_polys) {
+            DS_CUDA_TRY(cudaDeviceSynchronize());
+            DS_CUDA_TRY(cudaFree(ctx->jump_polys));
+            ctx->jump_polys = nullptr;
+            ctx->jump_polys_n = 0;
+        }
+        const size_t bo = dsi::align_up(sizeof(int) * offs.size(), 256);
+        DS_CUDA_TRY(cudaMalloc(&ctx->jump_polys, bo + sizeof(uint16_t) * bits.size()));
+        DS_CUDA_TRY(cudaMemcpy(ctx->jump_polys, offs.data(), sizeof(int) * offs.size(),
+                               cudaMemcpyHostToDevice));
+        DS_CUDA_TRY(cudaMemcpy(static_cast<char*>(ctx->jump_polys) + bo, bits.data(),
+                               sizeof(uint16_t) * bits.size(), cudaMemcpyHostToDevice));
+        ctx->jump_polys_n = want;
+        ctx->jump_idx_offset = bo;
+    }
+    *off = static_cast<const int*>(ctx->jump_polys);
+    *idx = reinterpret_cast<const uint16_t*>(static_cast<const char*>(ctx->jump_polys) +
+                                             ctx->jump_idx_offset);
+    return DS_OK;
+}
+
+// raw[0 .. n): the engine's untempered words x_312 .. (one stream; K8a).
+ds_status mt_stream(ds_ctx* ctx, uint64_t seed, int64_t n, uint64_t* raw, cudaStream_t st) {
+    static const bool no_jump = std::getenv("DS_ARRIVALS_NO_JUMP") != nullptr;   // A/B
+    if (no_jump || n <= 2 * kJumpSeg) {
+        mt_stream_kernel<<<1, kMtThreads, 0, st>>>(seed, n, n, raw);
+        DS_LAUNCH_CHECK(ctx, "mt_stream_kernel");
+        return DS_OK;
+    }
+    const int S = static_cast<int>((n + kJumpSeg - 1) / kJumpSeg);
+    const uint16_t* idx = nullptr;
+    const int* off = nullptr;
+    ds_status s = jump_lists(ctx, S, &idx, &off);
+    if (s != DS_OK) return s;
+    mt_stream_kernel<<<1, kMtThreads, 0, st>>>(seed, kJumpSeg, n, raw);   // segment 0
+    DS_LAUNCH_CHECK(ctx, "mt_stream_kernel");
+    if (!(ctx->route_attr_set & (1u << 20))) {
+        DS_CUDA_TRY(cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kJumpSmem));
+        ctx->route_attr_set |= 1u << 20;
+    }
+    mt_jump_kernel<<<S - 1, kJumpThreads, kJumpSmem, st>>>(seed, idx, off, n, raw);
+    DS_LAUNCH_CHECK(ctx, "mt_jump_kernel");
+    return DS_OK;
 }
 
 // ---- K8b: Exp(1) variates -----------------------------------------------------
@@ -850,8 +992,8 @@ ds_status generate(ds_ctx* ctx, const double* rates, int32_t n_rates, double dt,
             // RandomStream(seed, "arrivals") (rng.hpp:20-21)
             const uint64_t eng = splitmix64(seed ^ splitmix64(fnv1a("arrivals")));
             uint64_t* raw = reinterpret_cast<uint64_t*>(e);
-            mt_stream_kernel<<<1, kMtThreads, 0, st>>>(eng, D, raw);
-            DS_LAUNCH_CHECK(ctx, "mt_stream_kernel");
+            s = mt_stream(ctx, eng, D, raw, st);
+            if (s != DS_OK) return s;
             int64_t blocks = (D + 255) / 256;
             if (blocks > 148 * 16) blocks = 148 * 16;
             exp_draws_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(raw, D, e);

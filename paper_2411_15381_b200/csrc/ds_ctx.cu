@@ -156,6 +156,7 @@ ds_status ds_ctx_destroy(ds_ctx* ctx) {
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->d_err) cudaFree(ctx->d_err);
     if (ctx->route_flags) cudaFree(ctx->route_flags);
+    if (ctx->jump_polys) cudaFree(ctx->jump_polys);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->copy_stream) {
         cudaStreamSynchronize(ctx->copy_stream);

@@ -31,7 +31,12 @@ struct ds_ctx {
     // counter, zero at allocation and left zero by every launch
     void* route_flags = nullptr;
     size_t route_flags_bytes = 0;
-    unsigned route_attr_set = 0;   // bit per tile size: smem attribute set
+    unsigned route_attr_set = 0;   // kernels whose shared-memory attribute is set
+    // K8's jump-ahead tables on the device: the set-bit exponents of
+    // x^(s L) mod phi for s >= 1 (offsets, then uint16 exponents)
+    void* jump_polys = nullptr;
+    int jump_polys_n = 0;
+    size_t jump_idx_offset = 0;
 };
 
 namespace dsi {
