@@ -19,7 +19,9 @@
 //                   (phi = the engine's characteristic polynomial, degree
 //                   19937; gf2_jump.h, host, cached) selects which of the
 //                   first 19,937 states XOR to the state J words ahead.
-//                   1M draws: 0.54 -> ~0.2 ms (arrivals 0.70 -> 0.38 ms).
+//                   A segment's jump is split over a cluster of 3 CTAs
+//                   (partial states XORed over distributed shared memory).
+//                   1M arrivals 0.70 -> 0.32 ms.
 //   K8b exp_draws   grid-wide: temper, U = (u64 >> 11) * 2^-53,
 //                   e = -log1p(-U) with glibc's log1p restated bit for bit
 //                   (fdlibm_log1p.h; rng.cpp:24-28).
@@ -171,13 +173,35 @@ __global__ void __launch_bounds__(kMtThreads) mt_stream_kernel(uint64_t seed, in
 // the single stream (tests/test_gpu_arrivals.py).
 constexpr int kJumpSeg = 20480;                   // >= 19937: segment 0 holds the base words
 constexpr int kJumpBase = 19937 + 312;            // x_0 .. x_20248
-constexpr int kJumpGroups = 3;                    // the set bits of r split three ways
+constexpr int kJumpGroups = 3;                    // thread groups per CTA
+constexpr int kJumpSplit = 3;                     // CTAs (a cluster) per segment
 constexpr int kJumpThreads = 320 * kJumpGroups;   // 312 state words per group
 constexpr int kJumpMaxBits = 19937;
 constexpr int kJumpSmem = (kJumpBase + kJumpGroups * 312) * 8 + kJumpMaxBits * 2 + 16;
 
+__device__ __forceinline__ unsigned jump_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void jump_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// a 64-bit word of CTA `rank`'s shared memory at this CTA's address `p`
+__device__ __forceinline__ uint64_t jump_peer_load(const uint64_t* p, unsigned rank) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p)), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    uint64_t v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
+    return v;
+}
+
 // idx: the exponents i of r's set bits (uint16, ascending), segment s at
-// idx[off[s-1] .. off[s]).
+// idx[off[s-1] .. off[s]). A cluster of kJumpSplit CTAs per segment: CTA c
+// sums the c-th third of the set bits (its thread groups every third of
+// those), the leader XORs the partial states over distributed shared memory
+// and generates the segment.
 __global__ void __launch_bounds__(kJumpThreads)
 mt_jump_kernel(uint64_t seed, const uint16_t* __restrict__ idx, const int* __restrict__ off,
                int64_t n, uint64_t* __restrict__ raw) {
@@ -185,14 +209,16 @@ mt_jump_kernel(uint64_t seed, const uint16_t* __restrict__ idx, const int* __res
     __shared__ uint64_t ring[4][156];
     uint64_t* part = jw + kJumpBase;
     uint16_t* si = reinterpret_cast<uint16_t*>(part + kJumpGroups * 312);
-    const int s = blockIdx.x + 1, tid = threadIdx.x;
-    const int i0 = off[s - 1], nbits = off[s] - i0;
+    const unsigned rank = jump_rank();
+    const int s = blockIdx.x / kJumpSplit + 1, tid = threadIdx.x;
+    const int i0 = off[s - 1], all = off[s] - i0;
+    const int lo = static_cast<int>(static_cast<int64_t>(all) * rank / kJumpSplit);
+    const int nbits = static_cast<int>(static_cast<int64_t>(all) * (rank + 1) / kJumpSplit) - lo;
     mt_seed(seed, ring);
     for (int i = tid; i < 312; i += kJumpThreads) jw[i] = ring[i / 156][i % 156];
     for (int i = 312 + tid; i < kJumpBase; i += kJumpThreads) jw[i] = raw[i - 312];
-    for (int i = tid; i < nbits; i += kJumpThreads) si[i] = idx[i0 + i];
+    for (int i = tid; i < nbits; i += kJumpThreads) si[i] = idx[i0 + lo + i];
     __syncthreads();
-    // group g takes every third set bit: thread j XORs the words they select
     const int g = tid / 320, j = tid % 320;
     if (j < 312) {
         uint64_t a0 = 0, a1 = 0;
@@ -205,9 +231,16 @@ mt_jump_kernel(uint64_t seed, const uint16_t* __restrict__ idx, const int* __res
         if (k < nbits) a0 ^= wj[si[k]];
         part[g * 312 + j] = a0 ^ a1;
     }
-    __syncthreads();   // ring reused for the segment's state
-    if (tid < 312) ring[tid / 156][tid % 156] = part[tid] ^ part[312 + tid] ^ part[624 + tid];
     __syncthreads();
+    if (tid < 312) part[tid] ^= part[312 + tid] ^ part[624 + tid];   // this CTA's share
+    jump_cluster_sync();
+    if (rank == 0 && tid < 312) {
+        uint64_t v = part[tid];
+        for (unsigned c = 1; c < kJumpSplit; ++c) v ^= jump_peer_load(part + tid, c);
+        ring[tid / 156][tid % 156] = v;
+    }
+    jump_cluster_sync();   // the peers' shared memory was read
+    if (rank != 0) return;
     mt_run(ring, static_cast<int64_t>(s) * kJumpSeg, kJumpSeg, n, raw);
 }
 
@@ -271,7 +304,19 @@ ds_status mt_stream(ds_ctx* ctx, uint64_t seed, int64_t n, uint64_t* raw, cudaSt
                                          kJumpSmem));
         ctx->route_attr_set |= 1u << 20;
     }
-    mt_jump_kernel<<<S - 1, kJumpThreads, kJumpSmem, st>>>(seed, idx, off, n, raw);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((S - 1) * kJumpSplit));
+    cfg.blockDim = dim3(kJumpThreads);
+    cfg.dynamicSmemBytes = kJumpSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kJumpSplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, mt_jump_kernel, seed, idx, off, n, raw));
     DS_LAUNCH_CHECK(ctx, "mt_jump_kernel");
     return DS_OK;
 }
