@@ -396,8 +396,16 @@ ds_status ds_disc_score_device(ds_disc* disc, const uint8_t* nhwc, int64_t n, in
  * image at each threshold with Policy::defers (policies.cpp:37-39, strict <)
  * into ordered heavy lists (row k of heavy_idx holds counts[k] ids, stride n).
  * All pointers are device memory, stream-ordered. Bit-identical to
- * ds_disc_score_device + ds_curve_observe_device + ds_route_device; batches of
- * <= 2048 images run as the discriminator plus one fused tail launch. */
+ * ds_disc_score_device + ds_curve_observe_device + ds_route_device. Batches of
+ * <= 2048 images are ONE launch whose last CTA runs the tail, and consecutive
+ * calls on a stream overlap (programmatic dependent launch): the next call's
+ * pair tiles start on the SMs this batch's last round leaves idle, reading
+ * only its images before it waits for this call to complete. The images of a
+ * call must therefore be written by stream work that completes before the
+ * call (copies, ordinary kernels) -- not by a kernel that itself lets its
+ * dependents start early. Calls on one stream complete in order; the tail's
+ * state lives per (disc, stream). DS_DISC_NO_CHAIN=1 at the first call of a
+ * disc selects two plain launches per batch. */
 ds_status ds_disc_batch_complete_device(ds_disc* disc, const uint8_t* nhwc, int64_t n,
                                         int32_t h, int32_t w, float* conf, ds_curve* curve,
                                         double decay, const double* thresholds,

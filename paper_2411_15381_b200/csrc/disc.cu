@@ -61,6 +61,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -140,6 +141,24 @@ struct DiscParams {
     long long n_img;
     int h, w, px, tokens, tiles_per_img;
     long long* trace;   // debug: per-phase clock64 stamps of CTA 0 (nullptr = off)
+    // Chained light batch (ds_disc_batch_complete_device, n <= kTailMax): the
+    // grid is launched with programmatic stream serialization, lets its
+    // dependent start at once, reads only its images and weights before
+    // griddep_wait, and the last CTA to finish runs the batch tail
+    // (light_batch_tail) -- so the next call's tiles fill the SMs this batch's
+    // last round leaves idle.
+    int chain;
+    unsigned* done;     // CTAs finished (the last one resets it)
+    float* conf;
+    float hb;
+    ds_curve* curve;
+    double decay;
+    const double* thr;
+    int nt;
+    long long index_base;
+    long long* heavy;
+    long long* counts;
+    long long* err;
 };
 
 constexpr int kTraceTiles = 8;
@@ -230,14 +249,103 @@ __device__ __forceinline__ void e1_columns(uint32_t tmem_lane, int c_lo, uint32_
 #endif
 }
 
+constexpr int kStash = 40;
 struct Bars {
     uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
     uint64_t x_full[kXStages], r1_free, e1b_done, aw_full[2], aw_free;
     uint32_t tmem_base;
     float warp_part[2][8];
+    float stash[kStash];   // chained: this CTA's head sums until the previous call completed
 };
 static_assert(sizeof(Bars) <= 512, "barrier block");
+
+// logit = (sum of the image's per-tile head sums, in tile order) / tokens + b_head
+// (L2 loads: the sums may come from other CTAs of a running grid)
+__device__ __forceinline__ float image_score(const float* __restrict__ part, long long i, int tpi,
+                                             int tokens, float hb, int logits) {
+    float s = 0.0f;
+    for (int t = 0; t < tpi; ++t) s += __ldcg(part + i * tpi + t);
+    const float logit = s / static_cast<float>(tokens) + hb;
+    return logits ? logit : 1.0f / (1.0f + expf(-logit));
+}
+
+// One light batch's completion after the discriminator
+// (Simulation::handle_batch_complete, cluster.cpp:288-307): confidences from
+// the head sums (as finalize_kernel), then observe_confidence of each in batch
+// order (profiles.cpp:108-120; the arithmetic of curve.cu's single-CTA replay:
+// bins on threads 0-100, the total alone on thread 128, explicit _rn fp64),
+// then Policy::defers (strict <) at every threshold into ordered heavy lists
+// (as route.cu). Bit-identical to finalize + ds_curve_observe + ds_route.
+// A confidence outside [0, 1] (a NaN from the network) is where the reference
+// throws out of handle_batch_complete: the curve stops before it, only the
+// queries before it are routed, and its index goes to the context's device
+// error word (ds_ctx_take_error). Run by all kT threads of one CTA (kT >= 160);
+// sc / sbin hold n <= kTailMax entries.
+constexpr int kTailThreads = 160, kTailTotalTid = 128, kTailMax = 2048;
+template <int kT>
+__device__ __forceinline__ void light_batch_tail(
+    const float* __restrict__ part, int n, int tpi, int tokens, float hb, float* __restrict__ conf,
+    ds_curve* __restrict__ curve, double decay, const double* __restrict__ thr, int nt,
+    long long index_base, long long* __restrict__ heavy, long long* __restrict__ counts,
+    long long* __restrict__ err, float* sc, unsigned char* sbin, int* s_bad, int* wcnt) {
+    static_assert(kT % 32 == 0 && kT > kTailTotalTid && kT > DS_CURVE_BINS, "tail block");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) *s_bad = n;
+    __syncthreads();
+    for (int i = tid; i < n; i += kT) {
+        const float c = image_score(part, i, tpi, tokens, hb, 0);
+        conf[i] = c;
+        sc[i] = c;
+        const double cd = static_cast<double>(c);
+        if (!(cd >= 0.0) || !(cd <= 1.0)) {
+            atomicMin(s_bad, i);   // the reference throws here; the curve stops before it
+            sbin[i] = 255;
+        } else {
+            int b = static_cast<int>(floor(__dadd_rn(__dmul_rn(cd, 100.0), 1e-9)));
+            b = b < 0 ? 0 : (b > DS_CURVE_BINS - 1 ? DS_CURVE_BINS - 1 : b);
+            sbin[i] = static_cast<unsigned char>(b);
+        }
+    }
+    __syncthreads();
+    const int n_eff = *s_bad;
+    if (tid == 0 && n_eff < n) atomicMin(err, static_cast<long long>(n_eff));
+    const bool scale = decay != 1.0;
+    if (tid < DS_CURVE_BINS) {
+        double m = __ldcg(&curve->bin_mass[tid]);
+        for (int k = 0; k < n_eff; ++k) {
+            if (scale) m = __dmul_rn(m, decay);
+            if (sbin[k] == tid) m = __dadd_rn(m, 1.0);
+        }
+        curve->bin_mass[tid] = m;
+    } else if (tid == kTailTotalTid) {
+        double t = __ldcg(&curve->total_mass);
+        for (int k = 0; k < n_eff; ++k) t = __dadd_rn(scale ? __dmul_rn(t, decay) : t, 1.0);
+        curve->total_mass = t;
+    }
+    for (int k = 0; k < nt; ++k) {
+        const double t = thr[k];
+        long long off = 0;
+        long long* out = heavy + static_cast<long long>(k) * n;
+        for (int base = 0; base < n_eff; base += kT) {
+            const int i = base + tid;
+            const bool p = i < n_eff && static_cast<double>(sc[i]) < t;
+            const unsigned bal = __ballot_sync(0xffffffffu, p);
+            __syncthreads();   // wcnt of the previous chunk consumed
+            if (lane == 0) wcnt[warp] = __popc(bal);
+            __syncthreads();
+            int before = 0, all = 0;
+#pragma unroll
+            for (int w = 0; w < kT / 32; ++w) {
+                before += w < warp ? wcnt[w] : 0;
+                all += wcnt[w];
+            }
+            if (p) out[off + before + __popc(bal & ((1u << lane) - 1u))] = index_base + i;
+            off += all;
+        }
+        if (tid == 0) counts[k] = off;
+    }
+}
 
 __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant__ DiscParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -251,6 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     const long long unit = cluster_id_x(), nunits = nclusters_x();   // pair index / count
 
     if (sbase & 1023u) __trap();   // SW128 operand tiles need 1024-byte alignment
+    if (P.chain) griddep_launch_dependents();   // the next light batch may start now
     if (P.trace && threadIdx.x == 0) {   // debug: per-CTA start time and SM id
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -366,10 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 bulk_prefetch_l2(p0 + off, nb);
             }
         };
-        if (tl == 0) {
-            if (my_tiles > 0) prefetch_tile(0);
-            if (my_tiles > 1) prefetch_tile(1);
-        }
+        if (tl == 0) DS_TRACE(0, 0, 5);
         const uint32_t tmem_lane = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
         const uint64_t s1x2 = f2_pack(P.s1, P.s1);
         uint4 buf[2][8];
@@ -380,7 +486,16 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         const uint8_t* pbase = my_tiles > 0 ? token_base(0) : nullptr;
         if (my_tiles > 0) {
             load_chunk(pbase, 0, buf[0]);
+            if (tl == 0) DS_TRACE(0, 0, 7);
             load_chunk(pbase, 1, buf[1]);
+            if (tl == 0) DS_TRACE(0, 0, 8);
+        }
+        // the rest of the first two tiles into L2 (after the first loads: the
+        // bulk prefetches take a while to issue)
+        if (tl == 0) {
+            if (my_tiles > 0) prefetch_tile(0);
+            if (my_tiles > 1) prefetch_tile(1);
+            DS_TRACE(0, 0, 6);
         }
         int astage = 0;
         uint32_t aphase = 0;
@@ -471,7 +586,17 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
 #pragma unroll
                 for (int w = 0; w < 8; ++w) s += B.warp_part[b][w];
                 const long long f = flat_raw(tile);
-                if (f < n_flat) P.part[f] = s;      // ghost tiles write nothing
+                if (f < n_flat) {                   // ghost tiles write nothing
+                    // chained: the part buffer is the previous call's until that
+                    // completed; the first kStash sums wait in shared memory
+                    if (P.chain && tile < kStash) {
+                        B.stash[tile] = s;
+                    } else {
+                        if (P.chain) griddep_wait();
+                        P.part[f] = s;
+                        if (P.chain) __threadfence();
+                    }
+                }
             }
         };
 
@@ -768,15 +893,34 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         if (P.trace && lane == 0)
             P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
     }
-}
-
-// logit = (sum of the image's per-tile head sums, in tile order) / tokens + b_head
-__device__ __forceinline__ float image_score(const float* __restrict__ part, long long i, int tpi,
-                                             int tokens, float hb, int logits) {
-    float s = 0.0f;
-    for (int t = 0; t < tpi; ++t) s += part[i * tpi + t];
-    const float logit = s / static_cast<float>(tokens) + hb;
-    return logits ? logit : 1.0f / (1.0f + expf(-logit));
+    if (P.chain) {
+        // The last CTA to finish runs the batch tail (its head sums are all
+        // written: every writer fenced before the barrier above). The H1
+        // region is free: every MMA reading it completed before E3's waits.
+        float* sc = reinterpret_cast<float*>(smem + kR1);
+        unsigned char* sbin = smem + kR1 + 4 * kTailMax;
+        int* s_bad = reinterpret_cast<int*>(smem + kR1 + 5 * kTailMax);
+        int* wcnt = s_bad + 1;
+        volatile int* s_last = s_bad + 1 + kThreads / 32;
+        if (threadIdx.x == 0) {
+            griddep_wait();   // the previous call completed: buffer free, counter reset, curve final
+            for (long long t = 0; t < my_tiles && t < kStash; ++t) {
+                const long long f = flat_raw(t);
+                if (f < n_flat) P.part[f] = B.stash[t];
+            }
+            __threadfence();
+            *s_last = atomicAdd(P.done, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (*s_last) {
+            griddep_wait();
+            __threadfence();
+            if (threadIdx.x == 0) *P.done = 0u;   // later grids count only after this one completed
+            light_batch_tail<kThreads>(P.part, static_cast<int>(n_img), tpi, P.tokens, P.hb, P.conf,
+                                       P.curve, P.decay, P.thr, P.nt, P.index_base, P.heavy,
+                                       P.counts, P.err, sc, sbin, s_bad, wcnt);
+        }
+    }
 }
 
 __global__ void finalize_kernel(const float* __restrict__ part, long long n, int tpi, int tokens,
@@ -786,18 +930,8 @@ __global__ void finalize_kernel(const float* __restrict__ part, long long n, int
     out[i] = image_score(part, i, tpi, tokens, hb, logits);
 }
 
-// One light batch's completion after the discriminator, in one launch
-// (Simulation::handle_batch_complete, cluster.cpp:288-307): confidences from
-// the head sums (as finalize_kernel), then observe_confidence of each in batch
-// order (profiles.cpp:108-120; the arithmetic of curve.cu's single-CTA replay:
-// bins on warps 0-3, the total alone on warp 4, explicit _rn fp64), then
-// Policy::defers (strict <) at every threshold into ordered heavy lists (as
-// route.cu). Bit-identical to finalize + ds_curve_observe + ds_route.
-// A confidence outside [0, 1] (a NaN from the network) is where the reference
-// throws out of handle_batch_complete: the curve stops before it, only the
-// queries before it are routed, and its index goes to the context's device
-// error word (ds_ctx_take_error).
-constexpr int kTailThreads = 160, kTailTotalTid = 128, kTailMax = 2048;
+// One light batch's completion after the discriminator, in one launch (the
+// unchained form of the chained disc_kernel's tail; light_batch_tail).
 __global__ void __launch_bounds__(kTailThreads)
 batch_tail_kernel(const float* __restrict__ part, int n, int tpi, int tokens, float hb,
                   float* __restrict__ conf, ds_curve* __restrict__ curve, double decay,
@@ -807,61 +941,8 @@ batch_tail_kernel(const float* __restrict__ part, int n, int tpi, int tokens, fl
     __shared__ float sc[kTailMax];
     __shared__ __align__(16) unsigned char sbin[kTailMax];
     __shared__ int s_bad, wcnt[kTailThreads / 32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_bad = n;
-    __syncthreads();
-    for (int i = tid; i < n; i += kTailThreads) {
-        const float c = image_score(part, i, tpi, tokens, hb, 0);
-        conf[i] = c;
-        sc[i] = c;
-        const double cd = static_cast<double>(c);
-        if (!(cd >= 0.0) || !(cd <= 1.0)) {
-            atomicMin(&s_bad, i);   // the reference throws here; the curve stops before it
-            sbin[i] = 255;
-        } else {
-            int b = static_cast<int>(floor(__dadd_rn(__dmul_rn(cd, 100.0), 1e-9)));
-            b = b < 0 ? 0 : (b > DS_CURVE_BINS - 1 ? DS_CURVE_BINS - 1 : b);
-            sbin[i] = static_cast<unsigned char>(b);
-        }
-    }
-    __syncthreads();
-    const int n_eff = s_bad;
-    if (tid == 0 && n_eff < n) atomicMin(err, static_cast<long long>(n_eff));
-    const bool scale = decay != 1.0;
-    if (tid < DS_CURVE_BINS) {
-        double m = curve->bin_mass[tid];
-        for (int k = 0; k < n_eff; ++k) {
-            if (scale) m = __dmul_rn(m, decay);
-            if (sbin[k] == tid) m = __dadd_rn(m, 1.0);
-        }
-        curve->bin_mass[tid] = m;
-    } else if (tid == kTailTotalTid) {
-        double t = curve->total_mass;
-        for (int k = 0; k < n_eff; ++k) t = __dadd_rn(scale ? __dmul_rn(t, decay) : t, 1.0);
-        curve->total_mass = t;
-    }
-    for (int k = 0; k < nt; ++k) {
-        const double t = thr[k];
-        long long off = 0;
-        long long* out = heavy + static_cast<long long>(k) * n;
-        for (int base = 0; base < n_eff; base += kTailThreads) {
-            const int i = base + tid;
-            const bool p = i < n_eff && static_cast<double>(sc[i]) < t;
-            const unsigned bal = __ballot_sync(0xffffffffu, p);
-            __syncthreads();   // wcnt of the previous chunk consumed
-            if (lane == 0) wcnt[warp] = __popc(bal);
-            __syncthreads();
-            int before = 0, all = 0;
-#pragma unroll
-            for (int w = 0; w < kTailThreads / 32; ++w) {
-                before += w < warp ? wcnt[w] : 0;
-                all += wcnt[w];
-            }
-            if (p) out[off + before + __popc(bal & ((1u << lane) - 1u))] = index_base + i;
-            off += all;
-        }
-        if (tid == 0) counts[k] = off;
-    }
+    light_batch_tail<kTailThreads>(part, n, tpi, tokens, hb, conf, curve, decay, thr, nt,
+                                   index_base, heavy, counts, err, sc, sbin, &s_bad, wcnt);
 }
 
 // A backlog of light batches after one discriminator launch and one curve
@@ -1039,9 +1120,54 @@ struct ds_disc {
     DiscParams params{};       // b1 + head + s1 (device-independent part)
     float hb = 0.0f;           // head bias
     int sms = 0;               // SM count of ctx->device (set once, with the smem attribute)
+    // head-sum buffer + done counter of chained light batches, one per stream
+    // (a chained call's buffer belongs to the previous call on the stream
+    // until that one completes, see DiscParams::chain)
+    struct ChainBuf {
+        cudaStream_t st;
+        float* part;
+        unsigned* done;
+    };
+    ChainBuf chain[8] = {};
+    int n_chain = 0;
+    int chain_off = -1;        // DS_DISC_NO_CHAIN=1: light batches as two launches (A/B runs)
+    int min_per_pair = 1;      // DS_DISC_MIN_PAIR_TILES (experiments): fewer, longer-lived pairs
 };
 
 namespace {
+
+constexpr long long kChainPart = 1 << 20;   // head sums of a chained batch (n * tiles per image)
+
+// The stream's chain buffer, allocated on first use outside stream capture
+// (nullptr: use the unchained launches).
+ds_disc::ChainBuf* chain_buf(ds_disc* d, cudaStream_t st) {
+    if (d->chain_off < 0) {
+        const char* e = std::getenv("DS_DISC_NO_CHAIN");
+        d->chain_off = e && *e == '1' ? 1 : 0;
+    }
+    if (d->chain_off) return nullptr;
+    for (int i = 0; i < d->n_chain; ++i)
+        if (d->chain[i].st == st) return &d->chain[i];
+    if (d->n_chain == 8) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+        return nullptr;
+    void* buf = nullptr;
+    if (cudaMalloc(&buf, sizeof(float) * kChainPart + 256) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (cudaMemset(buf, 0, sizeof(float) * kChainPart + 256) != cudaSuccess) {
+        cudaFree(buf);
+        cudaGetLastError();
+        return nullptr;
+    }
+    ds_disc::ChainBuf& c = d->chain[d->n_chain++];
+    c.st = st;
+    c.part = static_cast<float*>(buf);
+    c.done = reinterpret_cast<unsigned*>(static_cast<char*>(buf) + sizeof(float) * kChainPart);
+    return &c;
+}
 
 struct BatchTail {   // batch_tail_kernel arguments (ds_disc_batch_complete_device)
     ds_curve* curve;
@@ -1055,7 +1181,7 @@ struct BatchTail {   // batch_tail_kernel arguments (ds_disc_batch_complete_devi
 
 ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w, float* out,
                       int logits, cudaStream_t st, long long* trace = nullptr,
-                      const BatchTail* tail = nullptr) {
+                      const BatchTail* tail = nullptr, ds_disc::ChainBuf* chain = nullptr) {
     if (h % 16 || w % 16)
         return dsi::fail(DS_ERR_INVALID_ARGUMENT, "image height and width must be multiples of 16");
     const int tokens = (h / 16) * (w / 16);
@@ -1075,29 +1201,53 @@ ds_status launch_disc(ds_disc* d, const uint8_t* images, int64_t n, int h, int w
     p.trace = trace;
     const long long n_flat = static_cast<long long>(n) * p.tiles_per_img;
     float* part = nullptr;   // one head sum per 128-token tile, every entry written
-    DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * n_flat, st));
+    if (chain) {
+        p.chain = 1;
+        p.done = chain->done;
+        p.conf = out;
+        p.hb = d->hb;
+        p.curve = tail->curve;
+        p.decay = tail->decay;
+        p.thr = tail->thr;
+        p.nt = tail->nt;
+        p.index_base = tail->index_base;
+        p.heavy = tail->heavy;
+        p.counts = tail->counts;
+        p.err = d->ctx->d_err;
+        part = chain->part;
+    } else {
+        DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * n_flat, st));
+    }
     p.part = part;
     if (d->sms == 0) {   // once per ds_disc (one device); kept off the per-launch path
         DS_CUDA_TRY(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, d->ctx->device));
         DS_CUDA_TRY(cudaFuncSetAttribute(disc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kSmemBytes));
     }
+    // as many pairs as give every pair the same number of pair tiles: a pair
+    // with one tile fewer would idle through the last round (and chained
+    // batches start in the SMs it leaves)
     const long long pair_tiles = (n_flat + 1) / 2;
-    const int pairs = static_cast<int>(pair_tiles < d->sms / 2 ? pair_tiles : d->sms / 2);
+    long long per_pair = (pair_tiles + d->sms / 2 - 1) / (d->sms / 2);
+    if (per_pair < d->min_per_pair) per_pair = d->min_per_pair;
+    const int pairs = static_cast<int>((pair_tiles + per_pair - 1) / per_pair);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = kSmemBytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = chain ? 2 : 1;
     DS_CUDA_TRY(cudaLaunchKernelEx(&cfg, disc_kernel, p));
     DS_LAUNCH_CHECK(d->ctx, "disc_kernel");
+    if (chain) return DS_OK;   // the tail ran in the grid's last CTA
     if (tail) {
         batch_tail_kernel<<<1, kTailThreads, 0, st>>>(
             part, static_cast<int>(n), p.tiles_per_img, tokens, d->hb, out, tail->curve, tail->decay,
@@ -1120,6 +1270,7 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
     ds_disc* d = new ds_disc();
     d->ctx = ctx;
     d->seed = weight_seed;
+    if (const char* e = std::getenv("DS_DISC_MIN_PAIR_TILES")) d->min_per_pair = std::max(1, std::atoi(e));
     cudaStream_t st = ctx->stream;
     const size_t nw = static_cast<size_t>(kD1) * kD2 + static_cast<size_t>(kD2) * kD3;
     auto cleanup = [&](ds_status s) {
@@ -1195,6 +1346,8 @@ extern "C" ds_status ds_disc_create(ds_ctx* ctx, uint64_t weight_seed, ds_disc**
 extern "C" ds_status ds_disc_destroy(ds_disc* d) {
     if (!d) return DS_OK;
     cudaStreamSynchronize(d->ctx->stream);
+    if (d->n_chain) cudaDeviceSynchronize();   // chained calls may sit on other streams
+    for (int i = 0; i < d->n_chain; ++i) cudaFree(d->chain[i].part);
     cudaFree(d->d_q1);
     cudaFree(d->d_w);
     cudaFree(d->d_blob);
@@ -1261,7 +1414,9 @@ extern "C" ds_status ds_disc_batch_complete_device(ds_disc* d, const uint8_t* nh
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
     BatchTail tail{curve, decay, thresholds, nt, static_cast<long long>(index_base),
                    reinterpret_cast<long long*>(heavy_idx), reinterpret_cast<long long*>(counts)};
-    return launch_disc(d, nhwc, n, h, w, conf, 0, st, nullptr, &tail);
+    const long long tpi = (static_cast<long long>(h / 16) * (w / 16)) / kM;
+    ds_disc::ChainBuf* chain = n * tpi <= kChainPart ? chain_buf(d, st) : nullptr;
+    return launch_disc(d, nhwc, n, h, w, conf, 0, st, nullptr, &tail, chain);
 }
 
 extern "C" ds_status ds_disc_batches_complete_device(ds_disc* d, const uint8_t* nhwc,
@@ -1331,6 +1486,20 @@ extern "C" ds_status ds_disc_score(ds_disc* d, const uint8_t* nhwc, int64_t n, i
     DS_CUDA_TRY(cudaMemcpyAsync(conf, dconf, sizeof(float) * n, cudaMemcpyDeviceToHost, ctx->stream));
     DS_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return DS_OK;
+}
+
+// Debug entry (not part of include/ds_gpu.h): ds_disc_batch_complete_device
+// (one threshold) with the per-CTA start / end stamps of ds_disc_trace_device.
+extern "C" ds_status ds_disc_batch_trace_device(ds_disc* d, const uint8_t* nhwc, int64_t n,
+                                                int32_t h, int32_t w, float* conf, ds_curve* curve,
+                                                double decay, const double* thr,
+                                                int64_t index_base, int64_t* heavy_idx,
+                                                int64_t* counts, long long* trace, void* stream) {
+    if (!d || n <= 0 || n > kTailMax) return dsi::fail(DS_ERR_INVALID_ARGUMENT, "trace: 1..2048 images");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : d->ctx->stream;
+    BatchTail tail{curve, decay, thr, 1, static_cast<long long>(index_base),
+                   reinterpret_cast<long long*>(heavy_idx), reinterpret_cast<long long*>(counts)};
+    return launch_disc(d, nhwc, n, h, w, conf, 0, st, trace, &tail, chain_buf(d, st));
 }
 
 // Debug entry (not part of include/ds_gpu.h): scores device images and writes

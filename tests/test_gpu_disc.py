@@ -261,3 +261,140 @@ def test_batches_complete_equals_batch_by_batch(disc, sizes_seed):
         want = 500 + offs[b] + np.flatnonzero(c0[offs[b]:offs[b + 1]].astype(np.float64) < thr[b])
         assert np.array_equal(h1[b], want), b
     assert n1[3] == 0 and n1[5] == 0 and n1[4] == sizes[4]
+
+
+def _run_batches(disc, imgs, sizes, thr, stream_ptr=0, between=None):
+    """One ds_disc_batch_complete_device per batch, back to back on one stream
+    (no host sync between calls). Returns conf, the curve bytes, counts, ids."""
+    import torch
+    from paper_2411_15381_b200 import workloads
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(offs[-1])
+    conf = torch.empty(n, dtype=torch.float32, device="cuda")
+    cur = torch.from_numpy(workloads.uniform_prior().reshape(1).view(np.uint8).copy()).cuda()
+    heavy = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    cnt = torch.full((len(sizes),), -1, dtype=torch.int64, device="cuda")
+    dthr = torch.from_numpy(np.asarray(thr, np.float64)).cuda()
+    torch.cuda.synchronize()
+    for b in range(len(sizes)):
+        o = int(offs[b])
+        if between is not None:
+            between(b, o)
+        disc.batch_complete_device(imgs.data_ptr() + o * 512 * 512 * 3, int(sizes[b]), 512, 512,
+                                   conf.data_ptr() + 4 * o, cur.data_ptr(), 0.999,
+                                   dthr.data_ptr() + 8 * b, 1, o, heavy.data_ptr() + 8 * o,
+                                   cnt.data_ptr() + 8 * b, stream_ptr)
+    torch.cuda.synchronize()
+    c = cnt.cpu().numpy()
+    hv = heavy.cpu().numpy()
+    return (conf.cpu().numpy(), cur.cpu().numpy().tobytes(), c,
+            [hv[offs[b]:offs[b] + c[b]] for b in range(len(sizes))])
+
+
+def _same(a, b):
+    (c0, v0, n0, h0), (c1, v1, n1, h1) = a, b
+    assert np.array_equal(c0.view(np.uint32), c1.view(np.uint32))
+    assert v0 == v1
+    assert np.array_equal(n0, n1)
+    for x, y in zip(h0, h1):
+        assert np.array_equal(x, y)
+
+
+@pytest.fixture(scope="module")
+def disc_unchained():
+    """A second discriminator (same weights) whose light batches run as two
+    plain launches: DS_DISC_NO_CHAIN is read at a disc's first batch call."""
+    import os
+    d = native.Discriminator(default_context(), weight_seed=2024)
+    os.environ["DS_DISC_NO_CHAIN"] = "1"
+    try:
+        import torch
+        imgs = torch.from_numpy(disc_oracle.synth_images(1, 0, 1, 512, 512).reshape(-1)).cuda()
+        _run_batches(d, imgs, [1], [0.5])
+    finally:
+        del os.environ["DS_DISC_NO_CHAIN"]
+    return d
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_chained_light_batches_equal_unchained(disc, disc_unchained, seed):
+    """Consecutive light-batch calls overlap (programmatic dependent launch:
+    the next batch's tiles start while this one's last round runs, its writes
+    and tail wait for it); the results are the bits of the unchained launches."""
+    import torch
+    rng = np.random.default_rng(seed)
+    sizes = rng.integers(1, 70, size=40)
+    sizes[7] = 0
+    sizes[8] = 32
+    thr = rng.random(len(sizes))
+    n = int(sizes.sum())
+    imgs = torch.from_numpy(disc_oracle.synth_images(seed, 0, n, 512, 512).reshape(-1)).cuda()
+    _same(_run_batches(disc_unchained, imgs, sizes, thr), _run_batches(disc, imgs, sizes, thr))
+
+
+def test_chained_light_batches_after_image_writes(disc, disc_unchained):
+    """A plain kernel that writes the NEXT batch's images between two calls
+    breaks the chain: the next call must see the new pixels."""
+    import torch
+    sizes = np.full(12, 32)
+    thr = np.full(12, 0.5)
+    n = int(sizes.sum())
+    src = torch.from_numpy(disc_oracle.synth_images(8, 0, n, 512, 512).reshape(-1)).cuda()
+    want = _run_batches(disc_unchained, src, sizes, thr)
+    work = torch.zeros_like(src)
+    per = 512 * 512 * 3
+    s = torch.cuda.Stream()
+
+    def copy_next(b, o):   # this batch's pixels land (on the calls' stream) just before its call
+        with torch.cuda.stream(s):
+            work[o * per:(o + int(sizes[b])) * per].copy_(src[o * per:(o + int(sizes[b])) * per])
+
+    torch.cuda.synchronize()
+    _same(want, _run_batches(disc, work, sizes, thr, stream_ptr=s.cuda_stream, between=copy_next))
+
+
+def test_chained_light_batches_in_cuda_graph_and_two_streams(disc, disc_unchained):
+    """Chained calls captured in a CUDA graph replay bit-identically (the done
+    counter is left zero by every grid), and calls on two streams keep their
+    own chains."""
+    import torch
+    from paper_2411_15381_b200 import workloads
+    sizes = np.full(10, 32)
+    thr = np.linspace(0.1, 0.9, 10)
+    n = int(sizes.sum())
+    imgs = torch.from_numpy(disc_oracle.synth_images(9, 0, n, 512, 512).reshape(-1)).cuda()
+    want = _run_batches(disc_unchained, imgs, sizes, thr)
+    s = torch.cuda.Stream()
+    sp = s.cuda_stream
+    _same(want, _run_batches(disc, imgs, sizes, thr, stream_ptr=sp))   # eager on s
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    conf = torch.empty(n, dtype=torch.float32, device="cuda")
+    prior = torch.from_numpy(workloads.uniform_prior().reshape(1).view(np.uint8).copy()).cuda()
+    cur = prior.clone()
+    heavy = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    cnt = torch.full((len(sizes),), -1, dtype=torch.int64, device="cuda")
+    dthr = torch.from_numpy(thr).cuda()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for b in range(len(sizes)):
+            o = int(offs[b])
+            disc.batch_complete_device(imgs.data_ptr() + o * 512 * 512 * 3, int(sizes[b]), 512,
+                                       512, conf.data_ptr() + 4 * o, cur.data_ptr(), 0.999,
+                                       dthr.data_ptr() + 8 * b, 1, o, heavy.data_ptr() + 8 * o,
+                                       cnt.data_ptr() + 8 * b, sp)
+    for _ in range(3):
+        cur.copy_(prior)
+        heavy.fill_(-1)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        c = cnt.cpu().numpy()
+        hv = heavy.cpu().numpy()
+        got = (conf.cpu().numpy(), cur.cpu().numpy().tobytes(), c,
+               [hv[offs[b]:offs[b] + c[b]] for b in range(len(sizes))])
+        _same(want, got)
+    # a second stream gets its own chain (head-sum buffer and done counter)
+    s2 = torch.cuda.Stream()
+    a = _run_batches(disc, imgs, sizes, thr, stream_ptr=s2.cuda_stream)
+    _same(want, a)
