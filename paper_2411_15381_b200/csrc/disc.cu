@@ -90,6 +90,15 @@ constexpr float kConst = 16.0f;         // value of the constant features
 #endif
 constexpr int kAStages = DS_A_STAGES, kBStages = 6 - DS_A_STAGES;   // 6 x 16 KB of rings
 constexpr int kXStages = 4;             // W1 stages 0-3 land in the H1 region (idle during GEMM1)
+#ifndef DS_AX
+#define DS_AX 1
+#endif
+// GEMM1's A chunks 3 and 5 go to the H1 region's W1 stage 0 / 1 slots once
+// chunks 0 / 1 (which read those weights) completed: with the 2-slot ring,
+// four chunk slots in flight after the first two (chunks 0,2 -> ring slot 0;
+// 1,4 -> slot 1; 3 -> X0; 5 -> X1)
+constexpr bool kAX = DS_AX != 0;
+static_assert(!kAX || kAStages == 2, "the X-slot schedule assumes a 2-slot A ring");
 #ifndef DS_AW
 #define DS_AW 1
 #endif
@@ -253,7 +262,7 @@ constexpr int kStash = 40;
 struct Bars {
     uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
-    uint64_t x_full[kXStages], r1_free, e1b_done, aw_full[2], aw_free;
+    uint64_t x_full[kXStages], r1_free, e1b_done, aw_full[2], aw_free, ax_full[2];
     uint32_t tmem_base;
     float warp_part[2][8];
     float stash[kStash];   // chained: this CTA's head sums until the previous call completed
@@ -392,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         mbar_init(&B.r1_free, 1);
         mbar_init(&B.e1b_done, kWarpArrive ? 4 + 4 * peer : 128 + peer);
         for (int s = 0; s < 2; ++s) mbar_init(&B.aw_full[s], 1);
+        for (int s = 0; s < 2; ++s) mbar_init(&B.ax_full[s], kWarpArrive ? 4 + 4 * peer : 128 + peer);
         mbar_init(&B.aw_free, 1);
         fence_mbar_init();
     }
@@ -499,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         }
         int astage = 0;
         uint32_t aphase = 0;
+        uint32_t fills[2] = {0u, 0u};   // kAX: fills of ring slot 0 / 1 so far
         for (long long tile = 0; tile < my_tiles; ++tile) {
             if (tl == 0) {
                 DS_TRACE(0, tile, 0);
@@ -506,20 +517,39 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             }
 #pragma unroll
             for (int c = 0; c < kChunksPerTile; ++c) {
-                mbar_wait(&B.a_empty[astage], aphase ^ 1);
-                // the A slots carried GEMM2_0's first weight stages after GEMM1
-                if (kAWStages && c == 0 && tile > 0)
-                    mbar_wait(&B.aw_free, static_cast<uint32_t>((tile - 1) & 1));
+                uint32_t st;
+                uint64_t* full;
+                if (kAX && (c == 3 || c == 5)) {
+                    // W1 stage 0 / 1's slot in the H1 region: chunk 0 / 1 read it
+                    // and completed (the wait of chunk 2 / 4 just before)
+                    st = sbase + kR1 + (c == 3 ? 0 : kBHalf);
+                    full = &B.ax_full[c == 3 ? 0 : 1];
+                } else if (kAX) {
+                    const int sl = (c == 1 || c == 4) ? 1 : 0;
+                    mbar_wait(&B.a_empty[sl], (fills[sl] & 1u) ^ 1u);
+                    ++fills[sl];
+                    // the ring slots carried GEMM2_0's first weight stages after GEMM1
+                    if (kAWStages && c == 0 && tile > 0)
+                        mbar_wait(&B.aw_free, static_cast<uint32_t>((tile - 1) & 1));
+                    st = sbase + kARing + sl * kAChunk;
+                    full = &B.a_full[sl];
+                } else {
+                    mbar_wait(&B.a_empty[astage], aphase ^ 1);
+                    // the A slots carried GEMM2_0's first weight stages after GEMM1
+                    if (kAWStages && c == 0 && tile > 0)
+                        mbar_wait(&B.aw_free, static_cast<uint32_t>((tile - 1) & 1));
+                    st = sbase + kARing + astage * kAChunk;
+                    full = &B.a_full[astage];
+                    if (++astage == kAStages) { astage = 0; aphase ^= 1; }
+                }
                 if (tl == 0) DS_TRACE(3, tile, c);
-                const uint32_t st = sbase + kARing + astage * kAChunk;
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     st_shared_v4(st + sw128(tl, j), buf[c & 1][j].x, buf[c & 1][j].y, buf[c & 1][j].z,
                                  buf[c & 1][j].w);
                 fence_proxy_async_smem();
-                group_signal(&B.a_full[astage], 2, 128, tl == 0);
+                group_signal(full, 2, 128, tl == 0);
                 if (tl == 0) DS_TRACE(4, tile, c);
-                if (++astage == kAStages) { astage = 0; aphase ^= 1; }
                 if (c + 2 < kChunksPerTile) load_chunk(pbase, c + 2, buf[c & 1]);
             }
             if (tl == 0) DS_TRACE(0, tile, 1);
@@ -740,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         if (lane == 0 && leader) {
             int as = 0, bs = 0;
             uint32_t ap = 0, bp = 0, pdr = 0, prd = 0, pe3 = 0;
+            uint32_t used[2] = {0u, 0u};   // kAX: fills of ring slot 0 / 1 consumed
             long long trace_tile = 0;   // trace only
             int trace_stage = 0;
             const uint32_t acc12 = tmem, acc3 = tmem + 256;
@@ -780,10 +811,22 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 // G1: 6 u8 A chunks (K = 128 bytes) x 6 int8 weight stages; stages
                 // 0-3 come from the H1 region (x_full), 4-5 from the ring
                 for (int c = 0; c < kChunksPerTile; ++c) {
-                    mbar_wait(&B.a_full[as], ap);
+                    uint32_t a_addr;
+                    if (kAX && (c == 3 || c == 5)) {
+                        mbar_wait(&B.ax_full[c == 3 ? 0 : 1], static_cast<uint32_t>(tile & 1));
+                        a_addr = sbase + kR1 + (c == 3 ? 0 : kBHalf);
+                    } else if (kAX) {
+                        const int sl = (c == 1 || c == 4) ? 1 : 0;
+                        mbar_wait(&B.a_full[sl], used[sl] & 1u);
+                        ++used[sl];
+                        a_addr = sbase + kARing + sl * kAChunk;
+                    } else {
+                        mbar_wait(&B.a_full[as], ap);
+                        a_addr = sbase + kARing + as * kAChunk;
+                    }
                     tc_fence_after();
                     DS_TRACE(5, tile, c);
-                    const uint64_t ad = desc_k_sw128(sbase + kARing + as * kAChunk);
+                    const uint64_t ad = desc_k_sw128(a_addr);
                     uint64_t bd;
                     if (c < kXStages) {
                         mbar_wait(&B.x_full[c], static_cast<uint32_t>(tile & 1));
@@ -797,8 +840,13 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                         umma_i8_pair(acc12, ad + 2 * k, bd + 2 * k, kIdescI8,
                                      (c > 0 || k > 0) ? 1u : 0u);
                     if (c >= kXStages) release_b();
-                    umma_commit_pair(&B.a_empty[as], 0x3);
-                    if (++as == kAStages) { as = 0; ap ^= 1; }
+                    if (kAX) {
+                        if (c == 0 || c == 2) umma_commit_pair(&B.a_empty[0], 0x3);
+                        if (c == 1 || c == 4) umma_commit_pair(&B.a_empty[1], 0x3);
+                    } else {
+                        umma_commit_pair(&B.a_empty[as], 0x3);
+                        if (++as == kAStages) { as = 0; ap ^= 1; }
+                    }
                     if (c == kChunksPerTile - 1) umma_commit_pair(&B.acc12_full, 0x3);
                     // GEMM3_3 of the previous tile between GEMM1 chunks: tensor work
                     // while the next A chunk makes its round trip
