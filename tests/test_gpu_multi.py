@@ -135,7 +135,74 @@ def test_nccl_one_rank_sharded_path_matches_reference():
     assert out and all(out.values()), out
 
 
-def _host_worker(rank, world, port, root, q):
+def _run_edges(ctx, comm, root, n):
+    """Ragged and empty shards: n confidences over comm.size ranks (n < size
+    leaves ranks with nothing; n = 0 leaves all of them empty). Every rank's
+    view must equal one GPU's over the whole sequence."""
+    import torch
+
+    from paper_2411_15381_b200 import abi, native, workloads
+    world, rank = comm.size, comm.rank
+    conf = np.array([0.7, 0.3, 0.5, 0.05, 0.95][:n], np.float64)
+    grid = np.array([0.0, 0.3, 0.5, 1.0], np.float64)
+    nt = len(grid)
+    lo, hi = native.Comm.shard_range(n, world, rank)
+    m = hi - lo
+    dev = torch.device("cuda", 0)
+    dconf = torch.from_numpy(np.concatenate([conf[lo:hi], [0.0]])).to(dev)   # never empty
+    thr = torch.from_numpy(grid).to(dev)
+    heavy = torch.full((nt * max(m, 1),), -7, dtype=torch.int64, device=dev)
+    counts = torch.full((nt,), -7, dtype=torch.int64, device=dev)
+    offs = torch.full((nt,), -7, dtype=torch.int64, device=dev)
+    tot = torch.full((nt,), -7, dtype=torch.int64, device=dev)
+    st = ctx.stream
+    torch.cuda.synchronize()
+    comm.route(dconf.data_ptr(), abi.CONF_F64, m, thr.data_ptr(), nt, lo, heavy.data_ptr(),
+               counts.data_ptr(), offs.data_ptr(), tot.data_ptr(), stream=st)
+    ctx.synchronize()
+    out = {}
+    out["counts"] = bool(np.array_equal(counts.cpu().numpy(),
+                                        [(conf[lo:hi] < t).sum() for t in grid]))
+    out["totals"] = bool(np.array_equal(tot.cpu().numpy(), [(conf < t).sum() for t in grid]))
+    out["offsets"] = bool(np.array_equal(offs.cpu().numpy(), [(conf[:lo] < t).sum() for t in grid]))
+    is_root = rank == root
+    gq = torch.full((nt * max(n, 1),), -1, dtype=torch.int64, device=dev) if is_root else None
+    gc = torch.full((nt,), -1, dtype=torch.int64, device=dev) if is_root else None
+    torch.cuda.synchronize()
+    comm.gather_queues(root, heavy.data_ptr(), m, counts.data_ptr(), nt,
+                       gq.data_ptr() if is_root else 0, n, gc.data_ptr() if is_root else 0,
+                       stream=st)
+    ctx.synchronize()
+    if is_root:
+        gcn = gc.cpu().numpy()
+        q = gq.cpu().numpy()
+        out["queue"] = bool(np.array_equal(gcn, [(conf < t).sum() for t in grid])) and all(
+            np.array_equal(q[k * n:k * n + gcn[k]], np.flatnonzero(conf < grid[k]))
+            for k in range(nt))
+    prior = workloads.uniform_prior()
+    cur = torch.from_numpy(prior.reshape(1).view(np.uint8).copy()).to(dev)
+    sizes = [native.Comm.shard_range(n, world, r)[1] - native.Comm.shard_range(n, world, r)[0]
+             for r in range(world)]
+    torch.cuda.synchronize()
+    comm.curve_observe(cur.data_ptr(), dconf.data_ptr(), abi.CONF_F64, sizes, 0.999, stream=st)
+    ctx.synchronize()
+    want = ctx.curve_observe(prior, conf, 0.999) if n else prior
+    out["curve_bits"] = cur.cpu().numpy().tobytes() == np.asarray(want).tobytes()
+    # byte gather with empty contributions
+    mine = torch.arange(8 * m, dtype=torch.uint8, device=dev) + 8 * lo
+    allb = torch.zeros(8 * max(n, 1), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    total = comm.gather(root, mine.data_ptr() if m else 0, 8 * m,
+                        allb.data_ptr() if is_root else 0, allb.numel() if is_root else 0,
+                        stream=st)
+    ctx.synchronize()
+    if is_root:
+        out["gather"] = total == 8 * n and bool(
+            np.array_equal(allb.cpu().numpy()[:8 * n], np.arange(8 * n, dtype=np.uint8)))
+    return out
+
+
+def _host_worker(rank, world, port, root, q, edge_n=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch
@@ -148,7 +215,7 @@ def _host_worker(rank, world, port, root, q):
         torch.cuda.set_device(0)
         ctx = native.Context(0)
         comm = native.Comm.host(ctx, world, rank, ddist.TorchHostOps())
-        out = _run_sharded(ctx, comm, root)
+        out = _run_sharded(ctx, comm, root) if edge_n is None else _run_edges(ctx, comm, root, edge_n)
         comm.close()
         ctx.close()
         q.put((rank, out, None))
@@ -159,13 +226,12 @@ def _host_worker(rank, world, port, root, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,root", [(2, 0), (3, 2)])
-def test_host_transport_ranks_on_one_gpu_match_reference(world, root):
+def _spawn(world, root, edge_n=None):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_host_worker, args=(r, world, port, root, q))
+    procs = [ctx.Process(target=_host_worker, args=(r, world, port, root, q, edge_n))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -177,9 +243,26 @@ def test_host_transport_ranks_on_one_gpu_match_reference(world, root):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world,root", [(2, 0), (3, 2)])
+def test_host_transport_ranks_on_one_gpu_match_reference(world, root):
+    res = _spawn(world, root)
     for r, out in res.items():
         assert all(out.values()), (r, out)
     assert "queue_digests" in res[root] and "plans_gathered" in res[root]
+
+
+@pytest.mark.parametrize("world,root,n", [(3, 1, 2), (3, 0, 5), (2, 1, 0), (4, 3, 1)])
+def test_host_transport_empty_and_ragged_shards(world, root, n):
+    """Ranks with no queries still take part in every exchange: counts,
+    global offsets and queues, the global curve and byte gathers equal one
+    GPU's results."""
+    res = _spawn(world, root, edge_n=n)
+    for r, out in res.items():
+        assert out and all(out.values()), (r, out)
+    assert "queue" in res[root] and "gather" in res[root]
 
 
 def test_cpp_multi_gpu_driver():
