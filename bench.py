@@ -145,6 +145,44 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml, 2 ms"}
 
 
+def in_kernel_clock(L, disc, images, conf, ctx):
+    """The SM clock the discriminator actually ran at: one traced launch of the
+    step's disc_kernel right after the timed region (GPU still at its load
+    state), every CTA stamping clock64 and globaltimer at its start and end.
+    NVML's clock/power readings are averaged over a longer window than a
+    4.7 ms launch, so they can read max clock while the kernel is power-capped;
+    this is the direct measurement (and a clock-independent cycles per pair
+    tile over the whole launch)."""
+    import ctypes
+
+    import torch
+
+    from paper_2411_15381_b200 import native
+    L.ds_disc_trace_device.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_int64, ctypes.c_int32,
+                                                                ctypes.c_int32] + [ctypes.c_void_p] * 3
+    nt = 8 * 8 * 16
+    tr = torch.zeros(nt + 5 * 160, dtype=torch.int64, device=images.device)
+    native.check(L.ds_disc_trace_device(disc.handle, native.c_p(images.data_ptr()), N_IMG, H, W,
+                                        native.c_p(conf.data_ptr()), native.c_p(tr.data_ptr()),
+                                        native.c_p(ctx.stream)))
+    ctx.synchronize()
+    t = tr.cpu().numpy()
+    ns = t[nt:nt + 480].reshape(160, 3)
+    cyc = t[nt + 480:nt + 800].reshape(160, 2)
+    used = (ns[:, 0] > 0) & (ns[:, 1] > ns[:, 0]) & (cyc[:, 1] > cyc[:, 0])
+    if not used.any():
+        return None
+    mhz = (cyc[used, 1] - cyc[used, 0]) / ((ns[used, 1] - ns[used, 0]) / 1e3)
+    pair_tiles = (N_IMG * (H // 16) * (W // 16) // 128 + 1) // 2
+    per_sm_tiles = pair_tiles / (int(used.sum()) // 2)
+    return {"sm_mhz_median": float(np.median(mhz)), "sm_mhz_min": float(mhz.min()),
+            "sm_mhz_max": float(mhz.max()), "ctas": int(used.sum()),
+            "launch_us": float((ns[used, 1].max() - ns[used, 0].min()) / 1e3),
+            "cycles_per_pair_tile": float(np.median(cyc[used, 1] - cyc[used, 0]) / per_sm_tiles),
+            "how": "clock64 / globaltimer at every CTA's start and end, one traced disc_kernel "
+                   "launch of the step's images right after the timed region"}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -485,6 +523,7 @@ def run_gpu(args):
     barrier()
     torch.cuda.synchronize()
     clocks = sampler.stop()
+    clocks["in_kernel"] = in_kernel_clock(L, disc, images, conf, ctx)
     total_ms = t_start.elapsed_time(t_end)
     disc_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     total_ms, disc_ms = allmax([total_ms, disc_ms])

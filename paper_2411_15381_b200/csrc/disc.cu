@@ -171,6 +171,7 @@ struct DiscParams {
 };
 
 constexpr int kTraceTiles = 8;
+constexpr int kTraceCtas = 160;   // per-CTA stamps: [globaltimer start, end, smid] x 160, then [clock64 start, end] x 160
 #define DS_TRACE(role, tile, ev)                                                          \
     do {                                                                                  \
         if (P.trace && blockIdx.x == 0 && (tile) >= 0 && (tile) < kTraceTiles)            \
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x] = static_cast<long long>(globaltimer());
         P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 2] = smid;
+        P.trace[8 * kTraceTiles * 16 + 3 * kTraceCtas + 2 * blockIdx.x] = clock64();
     }
     if (threadIdx.x < kD1) {
         s_b1[threadIdx.x] = P.b1[threadIdx.x];
@@ -938,8 +940,11 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         // not one: bar.sync counts a warp as arrived when any of its lanes
         // arrives, and lanes 1-31 of the MMA warp get there while lane 0 is
         // still issuing the last tile)
-        if (P.trace && lane == 0)
+        if (P.trace && lane == 0) {
             P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 1] = static_cast<long long>(globaltimer());
+            // with the start pair: this SM's mean clock over the launch
+            P.trace[8 * kTraceTiles * 16 + 3 * kTraceCtas + 2 * blockIdx.x + 1] = clock64();
+        }
     }
     if (P.chain) {
         // The last CTA to finish runs the batch tail (its head sums are all

@@ -30,7 +30,7 @@ conf = torch.empty(2 * B, dtype=torch.float32, device="cuda")
 L.ds_disc_trace_device.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_int64, ctypes.c_int32,
                                                             ctypes.c_int32] + [ctypes.c_void_p] * 3
 NT = 8 * 8 * 16
-tr = [torch.zeros(NT + 3 * 160, dtype=torch.int64, device="cuda") for _ in range(2)]
+tr = [torch.zeros(NT + 5 * 160, dtype=torch.int64, device="cuda") for _ in range(2)]
 sp = native.c_p(ctx.stream)
 for _ in range(5):
     disc.score_device(img.data_ptr(), B, H, H, conf.data_ptr(), ctx.stream)
@@ -41,7 +41,7 @@ for i in range(2):
                                         native.c_p(tr[i].data_ptr()), sp))
 ctx.synchronize()
 t = [x.cpu().numpy() for x in tr]
-ctas = [x[NT:].reshape(160, 3) for x in t]
+ctas = [x[NT:NT + 480].reshape(160, 3) for x in t]
 ctas = [c[c[:, 0] > 0] for c in ctas]
 t0 = ctas[0][:, 0].min()
 for i, c in enumerate(ctas):
@@ -62,7 +62,7 @@ for role in range(8):
 # kernel-boundary gap without host launch overhead
 gs = torch.cuda.Stream()
 g = torch.cuda.CUDAGraph()
-tr2 = [torch.zeros(NT + 3 * 160, dtype=torch.int64, device="cuda") for _ in range(3)]
+tr2 = [torch.zeros(NT + 5 * 160, dtype=torch.int64, device="cuda") for _ in range(3)]
 torch.cuda.synchronize()
 with torch.cuda.graph(g, stream=gs):
     for i in range(3):
@@ -73,7 +73,7 @@ with torch.cuda.graph(g, stream=gs):
 for _ in range(2):
     g.replay()
 torch.cuda.synchronize()
-c2 = [x.cpu().numpy()[NT:].reshape(160, 3) for x in tr2]
+c2 = [x.cpu().numpy()[NT:NT + 480].reshape(160, 3) for x in tr2]
 c2 = [c[c[:, 0] > 0] for c in c2]
 t0 = c2[0][:, 0].min()
 for i, c in enumerate(c2):

@@ -85,7 +85,7 @@ L.ds_disc_batch_trace_device.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_int64,
     [ctypes.c_double, ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 4
 NT = 8 * 8 * 16
 K = 6
-tr = [torch.zeros(NT + 3 * 160, dtype=torch.int64, device="cuda") for _ in range(K)]
+tr = [torch.zeros(NT + 5 * 160, dtype=torch.int64, device="cuda") for _ in range(K)]
 sp = native.c_p(ctx.stream)
 for rep in range(2):
     for i in range(K):
@@ -100,7 +100,7 @@ for rep in range(2):
             native.c_p(cnt.data_ptr() + 8 * i), native.c_p(tr[i].data_ptr()), sp))
     ctx.synchronize()
 t = [x.cpu().numpy() for x in tr]
-ctas = [x[NT:].reshape(160, 3) for x in t]
+ctas = [x[NT:NT + 480].reshape(160, 3) for x in t]
 ctas = [c[c[:, 0] > 0] for c in ctas]
 t0 = ctas[0][:, 0].min()
 for i, c in enumerate(ctas):

@@ -38,7 +38,7 @@ def main():
     import ctypes
     L.ds_disc_trace_device.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_int64, ctypes.c_int32,
                                                                 ctypes.c_int32] + [ctypes.c_void_p] * 3
-    tr = torch.zeros(8 * 8 * 16 + 3 * 160, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(8 * 8 * 16 + 5 * 160, dtype=torch.int64, device="cuda")
     native.check(L.ds_disc_trace_device(disc.handle, native.c_p(img.data_ptr()), n, hw, hw,
                                         native.c_p(conf.data_ptr()), native.c_p(tr.data_ptr()),
                                         native.c_p(ctx.stream)))

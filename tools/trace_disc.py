@@ -27,7 +27,7 @@ def main():
     native.check(L.ds_synth_images_device(ctx.handle, 1, 0, n, 512, 512,
                                           native.c_p(img.data_ptr()), native.c_p(ctx.stream)))
     conf = torch.empty(n, dtype=torch.float32, device="cuda")
-    tr = torch.zeros(8 * 8 * 16 + 3 * 160, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(8 * 8 * 16 + 5 * 160, dtype=torch.int64, device="cuda")
     for _ in range(2):
         native.check(L.ds_disc_trace_device(disc.handle, native.c_p(img.data_ptr()), n, 512, 512,
                                             native.c_p(conf.data_ptr()), native.c_p(tr.data_ptr()),
@@ -35,7 +35,7 @@ def main():
     ctx.synchronize()
     tall = tr.cpu().numpy()
     t = tall[:8 * 8 * 16].reshape(8, 8, 16)
-    cta = tall[8 * 8 * 16:].reshape(160, 3)
+    cta = tall[8 * 8 * 16:8 * 8 * 16 + 480].reshape(160, 3)
     base = t[2, 0, 0]
     names = {0: ["c0_start", "c11_stored"],
              1: ["E1_rdy", "E1_done", "E20_rdy", "E20_done", "E21_rdy", "E21_done", "E22_rdy",
