@@ -29,10 +29,14 @@ __device__ __forceinline__ unsigned long long flag_load(const unsigned long long
     return w;
 }
 
-// Exclusive prefix of this tile's count over tiles [0, tile) of one threshold
-// (warp 0 only; every lane returns it). Each round reads the 128 nearest
-// unread predecessors (4 per lane, all loads in flight together) and stops at
-// the nearest inclusive prefix (P); tiles without one contribute their count.
+// Exclusive prefix of this tile's count over tiles [0, tile) of one sequence
+// (one warp; every lane returns it). Each round covers the 128 nearest
+// unread predecessors (4 per lane at distances 4*lane + q, all loads in
+// flight together) and stops at the nearest inclusive prefix (P); tiles
+// without one contribute their aggregate (A). Only the flags up to the
+// nearest P must be published: a round re-polls while an unpublished flag is
+// nearer than every P it has seen, so a tile never waits for predecessors
+// beyond the P it stops at (formatting tiles, K9, finish far out of order).
 __device__ __forceinline__ long long look_back(const unsigned long long* flags, int tile) {
     const int lane = threadIdx.x & 31;
     long long excl = 0;
@@ -45,7 +49,8 @@ __device__ __forceinline__ long long look_back(const unsigned long long* flags, 
             val[q] = 0;
             if (base - (4 * lane + q) < 0) ready |= 1u << q;   // before tile 0: P of 0
         }
-        while (ready != 0xFu) {
+        int first_p = 4;   // nearest P among this lane's four, once read
+        for (;;) {
             unsigned long long w[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -57,21 +62,31 @@ __device__ __forceinline__ long long look_back(const unsigned long long* flags, 
                     val[q] = w[q] & kValMask;
                     ready |= 1u << q;
                 }
-        }
-        int first_p = 4;
+            // distance 4*lane + q: the nearest unpublished flag and the
+            // nearest P of the window (lane-major order = distance order)
+            int lane_nr = 4, lane_p = 4;
 #pragma unroll
-        for (int q = 3; q >= 0; --q)
-            if (st[q] == kStatusP) first_p = q;
-        const unsigned pmask = __ballot_sync(0xffffffffu, first_p < 4);
-        const int stop = pmask ? __ffs(pmask) - 1 : 32;
+            for (int q = 3; q >= 0; --q) {
+                if (!((ready >> q) & 1u)) lane_nr = q;
+                if (((ready >> q) & 1u) && st[q] == kStatusP) lane_p = q;
+            }
+            const unsigned nr_mask = __ballot_sync(0xffffffffu, lane_nr < 4);
+            const unsigned p_mask = __ballot_sync(0xffffffffu, lane_p < 4);
+            const int nr = nr_mask ? 4 * (__ffs(nr_mask) - 1) + __shfl_sync(0xffffffffu, lane_nr, __ffs(nr_mask) - 1) : 128;
+            const int np = p_mask ? 4 * (__ffs(p_mask) - 1) + __shfl_sync(0xffffffffu, lane_p, __ffs(p_mask) - 1) : 128;
+            if (np < nr || (nr == 128)) {   // everything up to the nearest P (or the window) known
+                first_p = np;
+                break;
+            }
+        }
         long long v = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (lane < stop || (lane == stop && q <= first_p)) v += static_cast<long long>(val[q]);
+            if (4 * lane + q <= first_p && 4 * lane + q < 128) v += static_cast<long long>(val[q]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         excl += v;
-        if (pmask) return excl;
+        if (first_p < 128) return excl;
     }
 }
 

@@ -99,3 +99,55 @@ def test_capacity_and_device_entry(ctx, golden):
     assert n.value == len(want)
     assert dout[:n.value].cpu().numpy().tobytes() == want
     assert int(dout[n.value:].sum()) == 0
+
+
+@pytest.mark.parametrize("shift", [1, 2, 3, 5])
+def test_device_entry_misaligned_out_and_short_capacity(ctx, shift):
+    """Any output alignment gives the same bytes and touches nothing outside
+    the file; a buffer shorter than the file gets DS_ERR_CAPACITY with the full
+    size reported and is left untouched. Many blocks, rows of every length
+    class (random records, NaN/inf/huge/tiny values)."""
+    torch = pytest.importorskip("torch")
+    rec = helpers.random_query_records(np.random.default_rng(40 + shift), 70_001)
+    want = port_csv("queries", rec)
+    L = native.lib()
+    n = native.i64(0)
+    drec = torch.from_numpy(rec.view(np.uint8).copy()).cuda()
+    stream = torch.cuda.current_stream().cuda_stream
+    dout = torch.zeros(len(want) + 64, dtype=torch.uint8, device="cuda")
+    native.check(L.ds_format_queries_csv_device(
+        ctx.handle, ctypes.c_void_p(drec.data_ptr()), len(rec),
+        ctypes.c_void_p(dout.data_ptr() + shift), len(want), ctypes.byref(n),
+        ctypes.c_void_p(stream)))
+    torch.cuda.synchronize()
+    got = dout.cpu().numpy()
+    assert n.value == len(want)
+    assert got[shift:shift + len(want)].tobytes() == want
+    assert int(got[:shift].sum()) == 0 and int(got[shift + len(want):].sum()) == 0
+    cap = len(want) // 2 + shift
+    dout.zero_()
+    with pytest.raises(CapacityError):
+        native.check(L.ds_format_queries_csv_device(
+            ctx.handle, ctypes.c_void_p(drec.data_ptr()), len(rec),
+            ctypes.c_void_p(dout.data_ptr()), cap, ctypes.byref(n), ctypes.c_void_p(stream)))
+    torch.cuda.synchronize()
+    assert n.value == len(want)
+    assert int(dout.sum()) == 0
+
+
+def test_longest_rows(ctx):
+    """Interval rows at their maximum length (every integer at its widest,
+    every real at 13 characters): 225 bytes, inside the kernel's row buffer."""
+    n = 3000
+    s = np.zeros(n, abi.INTERVAL_SNAPSHOT)
+    for f in ("interval_start", "demand_observed", "demand_estimated", "threshold",
+              "mean_delivered_quality"):
+        s[f] = -1.23456e-300
+    for f in ("x1", "x2", "b1", "b2"):
+        s["plan"][f] = np.iinfo(np.int32).min
+    for f in ("arrived", "served_light", "served_heavy", "dropped", "late"):
+        s[f] = np.iinfo(np.uint64).max
+    s["has_mean_delivered_quality"] = 1
+    want = port_csv("intervals", s)
+    assert max(len(r) for r in want.split(b"\n")) + 1 == 225
+    assert ctx.format_intervals_csv(s) == want

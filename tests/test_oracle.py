@@ -240,6 +240,20 @@ int main(void) {
             bad++;
         }
     }
+    for (long i = 0; i < n / 4; i++) {   /* the integer columns (operator<<) */
+        uint64_t u = xr() >> (xr() % 64);
+        if (i % 16 == 0) u = (i % 32 == 0) ? 0xffffffffffffffffull : (uint64_t)(i / 16);
+        snprintf(a, sizeof a, "%llu", (unsigned long long)u);
+        int k = ds_fmt_u64(u, b);
+        b[k] = 0;
+        if (strcmp(a, b)) { if (bad < 5) printf("u64 %s restated=%s\n", a, b); bad++; }
+        int64_t s = (int64_t)u;
+        if (i % 64 == 1) s = INT64_MIN;
+        snprintf(a, sizeof a, "%lld", (long long)s);
+        k = ds_fmt_i64(s, b);
+        b[k] = 0;
+        if (strcmp(a, b)) { if (bad < 5) printf("i64 %s restated=%s\n", a, b); bad++; }
+    }
     printf("bad=%ld\n", bad);
     return bad != 0;
 }
@@ -267,6 +281,7 @@ def _compile_and_run(tmp_path, name, source, defines=()):
 
 FMT6_PROGRAM = r'''
 #include <math.h>
+#include <stdint.h>
 #include <stdio.h>
 #include <string.h>
 #include "fmt6.h"
@@ -296,6 +311,20 @@ int main(void) {
         b[k] = 0;
         if (strcmp(a, b)) { if (bad < 5) printf("%a: libc=%s restated=%s\n", x, a, b); bad++; }
     }
+    for (long i = 0; i < n / 4; i++) {   /* the integer columns (operator<<) */
+        uint64_t u = xr() >> (xr() % 64);
+        if (i % 16 == 0) u = (i % 32 == 0) ? 0xffffffffffffffffull : (uint64_t)(i / 16);
+        snprintf(a, sizeof a, "%llu", (unsigned long long)u);
+        int k = ds_fmt_u64(u, b);
+        b[k] = 0;
+        if (strcmp(a, b)) { if (bad < 5) printf("u64 %s restated=%s\n", a, b); bad++; }
+        int64_t s = (int64_t)u;
+        if (i % 64 == 1) s = INT64_MIN;
+        snprintf(a, sizeof a, "%lld", (long long)s);
+        k = ds_fmt_i64(s, b);
+        b[k] = 0;
+        if (strcmp(a, b)) { if (bad < 5) printf("i64 %s restated=%s\n", a, b); bad++; }
+    }
     printf("bad=%ld\n", bad);
     return bad != 0;
 }
@@ -306,7 +335,8 @@ int main(void) {
 def test_fmt6_restatement_matches_host_printf(tmp_path, path):
     """paper_2411_15381_b200/csrc/fmt6.h (the device's "%.6g", metrics.cpp:67-71)
     compiled for the host equals the host snprintf byte for byte: 4M doubles
-    through the 128-bit fast path, 1M with the 1280-bit path forced."""
+    through the 128-bit fast path, 1M with the 1280-bit path forced, and the
+    integer columns (ds_fmt_u64 / ds_fmt_i64 against %llu / %lld)."""
     defines = ["N=4000000"] if path == "fast" else ["N=1000000", "DS_FMT_FORCE_BIG"]
     r = _compile_and_run(tmp_path, "fmt6", FMT6_PROGRAM, defines)
     assert r.returncode == 0, r.stdout
