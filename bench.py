@@ -56,7 +56,7 @@ N_PLAN = 4096
 CANDS_PER_PROBLEM = 101 * 32 * 32
 N_LATENT = 1_000_000
 DECAY = 0.999
-CPU_DISC_SAMPLE = 96          # images for the CPU port of the discriminator
+CPU_DISC_SAMPLE = 256         # images for the CPU port of the discriminator
 CPU_PLAN_SAMPLE = 256         # problems for the CPU reference planner
 CPU_LATENT_SAMPLE = 200_000   # queries for the CPU reference scorer
 WL_RATES = [2500.0] * 400     # 400 s at 2,500 qps: 1,000,811 arrivals at seed 3
@@ -195,8 +195,9 @@ def dist_env():
 # ---------------------------------------------------------------------------
 
 def cpu_images_leg(n_img: int):
-    """The CPU port of the discriminator (oracle/disc_oracle.py, numpy on all
-    cores) + the reference's own route loop (oracle/_ref, cluster.cpp:290-306)
+    """The CPU port of the discriminator (oracle/disc_oracle.disc_forward_fast:
+    fp32 BLAS with the exact centred layer 1, one image per BLAS call, images
+    spread over every host thread) + the reference's own route loop (oracle/_ref, cluster.cpp:290-306)
     at all 101 thresholds over the same confidences."""
     from oracle import disc_oracle, lib
     from paper_2411_15381_b200 import abi, workloads
@@ -208,7 +209,7 @@ def cpu_images_leg(n_img: int):
     prior = np.zeros((), abi.CURVE)
     s = np.asarray(workloads.SHIPPED_PRIOR_SAMPLES, np.float64)
     t0 = time.perf_counter()
-    conf = disc_oracle.disc_forward(imgs, wts).astype(np.float64)
+    conf = disc_oracle.disc_forward_fast(imgs, wts).astype(np.float64)
     idx = np.zeros(n_img, np.int64)
     cnt = np.zeros(1, np.int64)
     if lib.ref_available():
@@ -1231,8 +1232,8 @@ def cpu_legs(line, args, c_host, prior, gpu_curve, pro, cas, grid, goffs, gpu_pl
     cv, ck, cpu_conf = cpu_images_leg(CPU_DISC_SAMPLE)
     line["cpu_baseline"] = {"value": cv, "unit": "images/s", "cores": threads,
                             "kind": "port" if ck != "reference" else ck,
-                            "sample": f"{CPU_DISC_SAMPLE} images 512x512: numpy port of "
-                                      "the discriminator (no reference network) + the "
+                            "sample": f"{CPU_DISC_SAMPLE} images 512x512: numpy fp32 port of "
+                                      "the discriminator on every host thread (no reference network) + the "
                                       "reference route loop at 101 thresholds"}
     g = c_host[:len(cpu_conf)]
     rel = np.abs(g - cpu_conf) / np.maximum(np.abs(cpu_conf), 1e-2)

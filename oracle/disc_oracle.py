@@ -88,6 +88,58 @@ def disc_forward(images: np.ndarray, wts: dict, logits: bool = False) -> np.ndar
     return out
 
 
+def disc_forward_fast(images: np.ndarray, wts: dict, threads: int = 0,
+                      chunk: int = 1) -> np.ndarray:
+    """disc_forward for TIMING (the bench's CPU baseline), as fast as numpy
+    gets on the host: layer 1 in fp32 on CENTRED pixels (x - 128 in [-128,
+    127], |q1| <= 127, so every partial sum is an integer below
+    768*128*127 < 2^24 and exact in fp32 in any order: acc = (x-128) @ q1 +
+    128 * colsum(q1), the same integers as the fp64 path), images in chunks
+    of `chunk` per BLAS call, chunks spread over `threads` host threads with
+    single-threaded BLAS in each (numpy's elementwise passes are single
+    threaded; threads over chunks use every core for them too). Same values
+    as disc_forward up to fp32 summation order in layers 2-3."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    q1 = wts["q1"].astype(np.float32)
+    q1c = np.float32(128.0) * q1.astype(np.float64).sum(0).astype(np.float32)
+    s1 = np.float32(wts["s1"])
+    w2 = bf16_bits_to_f32(wts["w2"])
+    w3 = bf16_bits_to_f32(wts["w3"])
+    b1, b2, b3 = (np.asarray(wts[k], np.float32) for k in ("b1", "b2", "b3"))
+    hw = np.asarray(wts["head_w"], np.float32)
+    out = np.zeros(len(images), np.float32)
+    t = len(images[0].reshape(-1)) // 768 if len(images) else 0
+
+    def run(lo):
+        hi = min(lo + chunk, len(images))
+        x = patches(images[lo:hi]).reshape(-1, 768)
+        x -= np.float32(128.0)
+        acc = x @ q1
+        acc += q1c
+        h1 = round_bf16(gelu_tanh(acc * s1 + b1))
+        h2 = round_bf16(np.maximum(h1 @ w2 + b2, 0.0))
+        h3 = np.maximum(h2 @ w3 + b3, 0.0)
+        sc = (h3 @ hw).reshape(hi - lo, t)
+        for j in range(hi - lo):
+            lg = np.float32(sc[j].mean(dtype=np.float64)) + np.float32(wts["head_b"])
+            out[lo + j] = 1.0 / (1.0 + np.exp(-np.float64(lg)))
+
+    threads = threads or (os.cpu_count() or 1)
+    try:
+        from threadpoolctl import threadpool_limits
+        limit = threadpool_limits(1, user_api="blas")
+    except Exception:   # noqa: BLE001 -- without threadpoolctl BLAS oversubscribes
+        limit = None
+    try:
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(run, range(0, len(images), chunk)))
+    finally:
+        if limit is not None:
+            limit.restore_original_limits()
+    return out
+
+
 # ---- host restatement of the deterministic weights (disc.cu gen_weights_kernel,
 # fold_bias_kernel and ds_disc_create's head) -------------------------------------
 

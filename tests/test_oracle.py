@@ -387,3 +387,15 @@ def test_disc_numpy_oracle_agrees_with_torch_reference():
     a = disc_oracle.disc_forward(imgs, w).astype(np.float64)
     b = disc_forward_torch(imgs, w)
     assert np.all(np.abs(a - b) <= 1e-3 * np.maximum(np.abs(a), 1e-2)), np.abs(a - b).max()
+
+
+def test_disc_fast_cpu_port_equals_oracle():
+    """The bench's CPU baseline (disc_forward_fast: centred fp32 layer 1,
+    threads over images) computes the oracle's values: layer 1's integers are
+    exact either way; layers 2-3 may differ only by fp32 summation order."""
+    from oracle import disc_oracle
+    w = disc_oracle.gen_weights(2024, calibrate=True)
+    imgs = disc_oracle.synth_images(6, 0, 5, 256, 512)
+    a = disc_oracle.disc_forward(imgs, w).astype(np.float64)
+    b = disc_oracle.disc_forward_fast(imgs, w, threads=3).astype(np.float64)
+    assert np.all(np.abs(a - b) <= 1e-6 * np.maximum(np.abs(a), 1e-2)), np.abs(a - b).max()
