@@ -112,6 +112,10 @@ constexpr bool kWarpArrive = DS_WARP_ARRIVE != 0;
 #define DS_G33_IL 0   // >0: the previous tile's GEMM3_3 K-chunk q is issued after GEMM1 chunk DS_G33_IL + q
 #endif
 constexpr int kG33Il = DS_G33_IL;
+#ifndef DS_PREFETCH
+#define DS_PREFETCH 1
+#endif
+constexpr int kPrefetch = DS_PREFETCH;   // image tiles two ahead into L2: 1 bulk (TMA), 2 lines (LSU), 0 off
 #ifndef DS_EXP_FAST_E1
 #define DS_EXP_FAST_E1 0
 #endif
@@ -487,6 +491,19 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 bulk_prefetch_l2(p0 + off, nb);
             }
         };
+        // DS_PREFETCH: 1 = one thread's bulk prefetches (TMA unit), 2 = every
+        // builder thread prefetches lines through the LSU, 0 = none
+        auto prefetch_lines = [&](long long tile) {
+            const long long f = flat_of(tile);
+            const long long img = f / tpi;
+            const int tok0 = static_cast<int>(f % tpi) * kM;
+            const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
+            const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
+            const long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
+            for (long long off = static_cast<long long>(tl) * 128; off < bytes; off += 128 * 128)
+                prefetch_l2_line(p0 + off);
+        };
+        (void)prefetch_lines;
         if (tl == 0) DS_TRACE(0, 0, 5);
         const uint32_t tmem_lane = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
         const uint64_t s1x2 = f2_pack(P.s1, P.s1);
@@ -504,19 +521,24 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         }
         // the rest of the first two tiles into L2 (after the first loads: the
         // bulk prefetches take a while to issue)
-        if (tl == 0) {
+        if (kPrefetch == 1 && tl == 0) {
             if (my_tiles > 0) prefetch_tile(0);
             if (my_tiles > 1) prefetch_tile(1);
-            DS_TRACE(0, 0, 6);
         }
+        if (kPrefetch == 2) {
+            if (my_tiles > 0) prefetch_lines(0);
+            if (my_tiles > 1) prefetch_lines(1);
+        }
+        if (tl == 0) DS_TRACE(0, 0, 6);
         int astage = 0;
         uint32_t aphase = 0;
         uint32_t fills[2] = {0u, 0u};   // kAX: fills of ring slot 0 / 1 so far
         for (long long tile = 0; tile < my_tiles; ++tile) {
             if (tl == 0) {
                 DS_TRACE(0, tile, 0);
-                if (tile + 2 < my_tiles) prefetch_tile(tile + 2);
+                if (kPrefetch == 1 && tile + 2 < my_tiles) prefetch_tile(tile + 2);
             }
+            if (kPrefetch == 2 && tile + 2 < my_tiles) prefetch_lines(tile + 2);
 #pragma unroll
             for (int c = 0; c < kChunksPerTile; ++c) {
                 uint32_t st;

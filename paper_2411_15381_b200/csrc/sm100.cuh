@@ -83,6 +83,11 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gm
         : "memory");
 }
 
+// One 128-byte line into L2 through the LSU (not the TMA unit).
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+    asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p));
+}
+
 // Bulk prefetch of a global byte range into L2 (no smem, no completion).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes)

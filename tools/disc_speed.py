@@ -4,6 +4,7 @@ A/B harness for kernel variants (build with DS_EXTRA_NVCC=-D... first)."""
 import os
 import sys
 
+import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -45,9 +46,18 @@ def main():
     ctx.synchronize()
     t = tr[:8 * 8 * 16].view(8, 8, 16)[2, :, 0].cpu().tolist()
     d = sorted(t[i + 1] - t[i] for i in range(1, 7))
+    # whole launch: every CTA's clock64 span / its pair tiles, and its SM clock
+    allt = tr.cpu().numpy()
+    ns = allt[8 * 8 * 16:8 * 8 * 16 + 480].reshape(160, 3)
+    cy = allt[8 * 8 * 16 + 480:].reshape(160, 2)
+    u = (ns[:, 1] > ns[:, 0]) & (cy[:, 1] > cy[:, 0])
+    pair_tiles = (n * (hw // 16) ** 2 // 128 + 1) // 2
+    span = cy[u, 1] - cy[u, 0]
+    launch_cpt = float(np.median(span)) / (pair_tiles / (u.sum() // 2))
+    mhz = float(np.median(span / ((ns[u, 1] - ns[u, 0]) / 1e3)))
     print(f"{os.environ.get('DS_EXTRA_NVCC', 'default')}: {n / ms * 1000:.0f} images/s "
           f"({ms:.3f} ms / {n} images {hw}x{hw}); cycles/tile median {d[len(d) // 2]} "
-          f"(tiles 2-7: {d}); conf[0:3] = {[round(x, 6) for x in conf[:3].tolist()]}")
+          f"(tiles 2-7: {d}); launch cycles/pair tile {launch_cpt:.0f} at {mhz:.0f} MHz; conf[0:3] = {[round(x, 6) for x in conf[:3].tolist()]}")
 
 
 if __name__ == "__main__":
