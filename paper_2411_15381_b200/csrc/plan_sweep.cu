@@ -42,12 +42,12 @@ constexpr int kMaxGrid = (1 << 24) - 1;
 constexpr unsigned long long kNone = ~0ull;
 
 struct PlanSmem {
-    double e1[kMaxB], e2[kMaxB], T1[kMaxB], T2[kMaxB];
+    double e1[kMaxB], e2[kMaxB], T1[kMaxB], T2[kMaxB], rT2[kMaxB];
     int b1[kMaxB], b2[kMaxB], x1[kMaxB];
     unsigned long long lat[kMaxB];      // bit j set: (b1_i, b2_j) latency-feasible
     double prefix[DS_CURVE_BINS + 1];
     double ft[kTChunk];
-    int x2[kTChunk * kMaxB];
+    uint16_t x2[kTChunk * kMaxB];   // <= kMaxServers + 1
     unsigned long long red[kThreads / 32];
     unsigned long long red2[kThreads / 32];
 };
@@ -71,6 +71,23 @@ __device__ __forceinline__ int min_servers(double need, double per, int cap) {
     if (x < 1) x = 1;
     while (x <= cap && __dmul_rn(static_cast<double>(x), per) < need) ++x;
     return x;
+}
+
+// min_servers with the quotient's ceiling from a reciprocal: y = need *
+// fl(1/per) is within ~2.5 ulp of fl(need/per), so when y is more than
+// 2^-49 * y (>= 8 ulp) from every integer the two have the same ceiling; only
+// near an integer (or for huge quotients) is the correctly rounded division
+// done. Decision-identical to min_servers.
+// On that fast path q >= y + g, so q * per exceeds need by ~2^-49 relative
+// and fl(q * per) >= need: the reference's increment loop would not run.
+__device__ __forceinline__ int min_servers_r(double need, double per, double rper, int cap) {
+    if (need <= 0.0) return 0;
+    const double y = __dmul_rn(need, rper);
+    const double q = ceil(y);
+    const double g = __dmul_rn(y, 0x1p-49);
+    if (__dsub_rn(q, y) > g && __dsub_rn(y, __dsub_rn(q, 1.0)) > g)
+        return q < static_cast<double>(cap) + 1.0 ? static_cast<int>(q) : cap + 1;   // q >= 1
+    return min_servers(need, per, cap);
 }
 
 // profiles.cpp:67-71
@@ -124,6 +141,8 @@ __device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int
                                      int n1, int n2, int i0, int i1, int j0, int j1,
                                      double need_light, double total, int S) {
     const int ni = i1 - i0, nj = j1 - j0;
+    if (ni <= 0 || nj <= 0) return kNone;
+    const int dq = kThreads / nj, dr = kThreads % nj;   // a kThreads step in (row, column)
     unsigned long long best = kNone;
     int parity = 0;
     for (int hi = t_hi; hi > t_lo; hi -= kTChunk) {
@@ -132,9 +151,19 @@ __device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int
         for (int k = threadIdx.x; k < cnt; k += kThreads)
             s.ft[k] = __dmul_rn(need_light, deferral_fraction(s, total, grid[lo + k]));
         __syncthreads();
-        for (int k = threadIdx.x; k < cnt * nj; k += kThreads) {
-            const int tl = k / nj, j = j0 + k % nj;
-            s.x2[tl * kMaxB + j] = min_servers(s.ft[tl], s.T2[j], S);
+        // flat index k = tl * nj + (j - j0), stepped by kThreads without a
+        // division per entry (one per thread: dq, dr)
+        {
+            int tl = threadIdx.x / nj, j = j0 + threadIdx.x % nj;
+            for (int k = threadIdx.x; k < cnt * nj; k += kThreads) {
+                s.x2[tl * kMaxB + j] = static_cast<uint16_t>(min_servers_r(s.ft[tl], s.T2[j], s.rT2[j], S));
+                tl += dq;
+                j += dr;
+                if (j >= j1) {
+                    j -= nj;
+                    ++tl;
+                }
+            }
         }
         __syncthreads();
         // Each thread owns fixed (b1, b2) pairs -- the latency and x1 checks
@@ -147,13 +176,20 @@ __device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int
         // in the chunk are a prefix [0, k] of it and its first valid t from the
         // top is k: found by binary search instead of walking down from the top.
         unsigned long long mine = kNone;
+        int pi_ = i0 + threadIdx.x / nj, pj = j0 + threadIdx.x % nj;
         for (int pr = threadIdx.x; pr < ni * nj; pr += kThreads) {
-            const int i = i0 + pr / nj, j = j0 + pr % nj;
+            const int i = pi_, j = pj;
+            pi_ += dq;
+            pj += dr;
+            if (pj >= j1) {
+                pj -= nj;
+                ++pi_;
+            }
             if (!((s.lat[i] >> j) & 1ull)) continue;
             const int x1 = s.x1[i];
             if (x1 > S) continue;
             const int cap = S - x1;
-            const int* col = s.x2 + j;
+            const uint16_t* col = s.x2 + j;
             if (col[0] > cap) continue;            // even the chunk's lowest t is invalid
             int a = 0, b = cnt - 1;                // col[a * kMaxB] <= cap
             while (a < b) {
@@ -252,7 +288,10 @@ __device__ void cheapest(const double* e, const double* T, const int* b, int n, 
     bb = best_b;
 }
 
-__global__ void __launch_bounds__(kThreads)
+#ifndef DS_PLAN_MINB
+#define DS_PLAN_MINB 6   // 40 registers: 6 CTAs (48 warps) per SM
+#endif
+__global__ void __launch_bounds__(kThreads, DS_PLAN_MINB)
 plan_sweep_kernel(const ds_problem* __restrict__ problems, int n,
                   const ds_cascade* __restrict__ cascades,
                   const double* __restrict__ grid_values,
@@ -289,6 +328,7 @@ plan_sweep_kernel(const ds_problem* __restrict__ problems, int n,
         s.b2[j] = b;
         s.e2[j] = e;
         s.T2[j] = __ddiv_rn(static_cast<double>(b), e);
+        s.rT2[j] = __drcp_rn(s.T2[j]);
     } else if (tid >= 128 && tid - 128 <= DS_CURVE_BINS) {
         // the cascade's sequential prefix table (built once per call by
         // curve_prefix_kernel, in the reference's summation order)
@@ -584,6 +624,12 @@ ds_status launch_sweep(ds_ctx* ctx, const ds_problem* problems, int32_t n,
     double* tab = nullptr;
     DS_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&tab),
                                 sizeof(double) * (DS_CURVE_BINS + 1) * n_cascades, st));
+    static bool carveout = [] {   // all of the unified L1 as shared memory: more CTAs per SM
+        cudaFuncSetAttribute(plan_sweep_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        return true;
+    }();
+    (void)carveout;
     curve_prefix_kernel<<<(n_cascades + 31) / 32, 32, 0, st>>>(cascades, n_cascades, tab);
     DS_LAUNCH_CHECK(ctx, "curve_prefix_kernel");
     plan_sweep_kernel<<<n, kThreads, 0, st>>>(problems, n, cascades, grid_values, grid_offsets,

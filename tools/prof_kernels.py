@@ -32,8 +32,7 @@ def main(which):
     if which in ("plan", "all"):
         sys.path.insert(0, ROOT)
         import bench
-        pro, cas, grid, offs = bench.planner_inputs()
-        bench.sampled_curves(cas)
+        pro, cas, grid, offs, _ = bench.planner_inputs()   # the fixture's curves
         for _ in range(3):
             ctx.plan_batch(pro, cas, grid, offs)
     if which in ("latent", "all"):
