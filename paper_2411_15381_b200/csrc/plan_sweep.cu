@@ -118,10 +118,15 @@ __device__ __forceinline__ unsigned long long block_min(unsigned long long v,
     v = warp_min(v);
     if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = v;
     __syncthreads();
-    unsigned long long r = buf[0];
+    // the 8 warp minima on lanes 0-7 of every warp, reduced by shuffles
+    const int lane = threadIdx.x & 31;
+    unsigned long long r = lane < kThreads / 32 ? buf[lane] : kNone;
 #pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) r = buf[w] < r ? buf[w] : r;
-    return r;
+    for (int o = kThreads / 64; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, r, o);
+        r = w < r ? w : r;
+    }
+    return __shfl_sync(0xffffffffu, r, 0);
 }
 
 // Candidate::better_than tie key at equal threshold (allocator.cpp:57-67).
@@ -153,7 +158,14 @@ __device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int
         __syncthreads();
         // flat index k = tl * nj + (j - j0), stepped by kThreads without a
         // division per entry (one per thread: dq, dr)
-        {
+        if (dr == 0) {
+            // nj divides kThreads (the 32-batch profiles): a thread's column
+            // never changes, its T2 and 1/T2 stay in registers
+            const int j = j0 + threadIdx.x % nj;
+            const double per = s.T2[j], rper = s.rT2[j];
+            for (int tl = threadIdx.x / nj; tl < cnt; tl += dq)
+                s.x2[tl * kMaxB + j] = static_cast<uint16_t>(min_servers_r(s.ft[tl], per, rper, S));
+        } else {
             int tl = threadIdx.x / nj, j = j0 + threadIdx.x % nj;
             for (int k = threadIdx.x; k < cnt * nj; k += kThreads) {
                 s.x2[tl * kMaxB + j] = static_cast<uint16_t>(min_servers_r(s.ft[tl], s.T2[j], s.rT2[j], S));
@@ -191,12 +203,12 @@ __device__ unsigned long long search(PlanSmem& s, const double* grid, int G, int
             const int cap = S - x1;
             const uint16_t* col = s.x2 + j;
             if (col[0] > cap) continue;            // even the chunk's lowest t is invalid
-            int a = 0, b = cnt - 1;                // col[a * kMaxB] <= cap
-            while (a < b) {
-                const int mid = (a + b + 1) >> 1;
-                if (col[mid * kMaxB] <= cap) a = mid;
-                else b = mid - 1;
-            }
+            // the last a with col[a * kMaxB] <= cap: branch-free steps of
+            // 64, 32, ..., 1 (cnt <= kTChunk = 128)
+            int a = 0;
+#pragma unroll
+            for (int step = kTChunk / 2; step > 0; step >>= 1)
+                if (a + step < cnt && col[(a + step) * kMaxB] <= cap) a += step;
             const unsigned long long key =
                 (static_cast<unsigned long long>(G - 1 - (lo + a)) << 40) +
                 (static_cast<unsigned long long>(col[a * kMaxB]) << 28) + tie_key(x1, 0, i, j);
