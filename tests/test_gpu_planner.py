@@ -81,6 +81,54 @@ def test_planner_matches_port_on_fresh_instances(ctx):
         assert_plans_equal(got, ref, "fresh-vs-reference")
 
 
+def test_planner_server_counts_at_integer_quotients(ctx):
+    """Demands whose heavy-side server count need / T2 lands ON or one ulp
+    beside an integer for most thresholds (uniform prior: f(k/100) = k/100;
+    T2 in {4, 3, 2.5, 10/3, ...}; lambda * D = 400 -> need ~ 4k): every
+    x2 entry of these problems takes min_servers' exact-division fallback or
+    sits at its edge (plan_sweep.cu min_servers_r). Plans equal the C
+    restatement's (and the reference's when oracle/_ref exists). Mixed batch
+    counts (32 and 7 heavy sizes) cover both x2 table layouts."""
+    port = lib.port()
+    heavy32 = {b: b / 4.0 for b in range(1, 33)}                       # T2 = 4
+    heavy32.update({b: b / 3.0 for b in range(2, 33, 3)})              # T2 = 3
+    heavy32.update({b: b / 2.5 for b in range(3, 33, 5)})              # T2 = 2.5
+    heavy7 = {1: 0.3, 2: 0.6, 3: 0.9, 5: 1.25, 8: 2.4, 12: 3.0, 20: 6.0}   # T2 = 10/3, 4, ...
+    light = {b: b / 40.0 for b in (1, 2, 4, 8, 16, 32)}                # T1 = 40
+    cas = np.zeros(2, abi.CASCADE)
+    cas[0] = workloads.make_cascade(light, heavy32, 1e3)
+    cas[1] = workloads.make_cascade(light, heavy7, 1e3)
+    probs = []
+    for ci in range(2):
+        for s in (3, 8, 16, 64, 128, 1000):
+            for d in (100.0, 300.0, 400.0, 1000.0, 1234.5, 4000.0, 12.0):
+                for lam in (1.0, 1.05):
+                    p = np.zeros(1, abi.PROBLEM)
+                    p["demand_qps"] = d
+                    p["overprovision_lambda"] = lam
+                    p["queue_sentinel_seconds"] = 1e6
+                    p["total_servers"] = s
+                    p["cascade"] = ci
+                    p["mode"] = abi.SOLVE
+                    probs.append(p)
+    pro = np.concatenate(probs)
+    grid = workloads.make_grid(0.01)
+    offs = np.array([0, len(grid)], np.int32)
+    got = ctx.plan_batch(pro, cas, grid, offs)
+    want = np.zeros(len(pro), abi.PLAN)
+    st = np.zeros(len(pro), np.int32)
+    port.dso_plan_batch(abi.ptr(pro), len(pro), abi.ptr(cas), abi.ptr(grid), abi.ptr(offs),
+                        abi.ptr(want), abi.ptr(st), 8)
+    assert not st.any()
+    assert want["feasible"].any() and not want["feasible"].all()
+    assert_plans_equal(got, want, "integer-quotients")
+    if lib.ref_available():
+        ref = np.zeros(len(pro), abi.PLAN)
+        assert lib.ref().dsref_plan_batch(abi.ptr(pro), len(pro), abi.ptr(cas), len(cas),
+                                          abi.ptr(grid), abi.ptr(offs), 1, abi.ptr(ref), 8) == 0
+        assert_plans_equal(got, ref, "integer-quotients-vs-reference")
+
+
 # ---- test_allocator.cpp known answers, through the reference-shaped API ---------
 
 def toy_cascade(slo=100.0):      # helpers.hpp:53-61
