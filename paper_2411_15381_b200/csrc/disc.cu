@@ -381,11 +381,92 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         P.trace[8 * kTraceTiles * 16 + 3 * blockIdx.x + 2] = smid;
         P.trace[8 * kTraceTiles * 16 + 3 * kTraceCtas + 2 * blockIdx.x] = clock64();
     }
+    // Flat 128-token tiles f = image * tiles_per_img + tile-in-image; pair tile
+    // k covers f = 2k (leader) and 2k + 1 (peer), and the pairs take pair
+    // tiles round robin (k = unit, unit + nunits, ...), so a small batch still
+    // spreads over every SM pair. A pair tile whose second half runs past the
+    // end recomputes the last tile and writes nothing (a "ghost").
+    const long long n_img = P.n_img;
+    const int tpi = P.tiles_per_img;
+    const long long n_flat = n_img * tpi;
+    const long long n_pair_tiles = (n_flat + 1) / 2;
+    const long long my_tiles = unit < n_pair_tiles ? (n_pair_tiles - 1 - unit) / nunits + 1 : 0;
+    const long long img_bytes = static_cast<long long>(P.h) * P.w * 3;
+    const long long row_bytes = static_cast<long long>(P.w) * 3;
+    auto flat_raw = [&](long long tile) { return 2 * (unit + tile * nunits) + rank; };
+    auto flat_of = [&](long long tile) {                   // this CTA's flat tile
+        const long long f = flat_raw(tile);
+        return f < n_flat ? f : n_flat - 1;
+    };
+
+
+    // ---- A-builder helpers (warps 0-3; thread tl = token of the 128-token tile)
+    const int tl = threadIdx.x;
+    auto token_base = [&](long long tile) -> const uint8_t* {
+        const long long f = flat_of(tile);
+        const long long img = f / tpi;
+        const int tok = static_cast<int>(f % tpi) * kM + tl;
+        const int py = tok / P.px, px = tok - py * P.px;
+        return P.images + img * img_bytes + (static_cast<long long>(py) * 16) * row_bytes +
+               px * 48;
+    };
+    auto piece = [&](const uint8_t* base, int q) -> const uint8_t* {
+        return base + (q / 3) * row_bytes + (q % 3) * 16;
+    };
+    // The pixels of a tile are one contiguous byte range of whole patch
+    // rows (or a small superset); bulk-prefetch it into L2.
+    auto prefetch_tile = [&](long long tile) {
+        const long long f = flat_of(tile);
+        const long long img = f / tpi;
+        const int tok0 = static_cast<int>(f % tpi) * kM;
+        const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
+        const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
+        const long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
+        for (long long off = 0; off < bytes; off += 65536) {
+            const uint32_t nb = static_cast<uint32_t>(bytes - off < 65536 ? bytes - off : 65536);
+            bulk_prefetch_l2(p0 + off, nb);
+        }
+    };
+    // DS_PREFETCH: 1 = one thread's bulk prefetches (TMA unit), 2 = every
+    // builder thread prefetches lines through the LSU, 0 = none
+    auto prefetch_lines = [&](long long tile) {
+        const long long f = flat_of(tile);
+        const long long img = f / tpi;
+        const int tok0 = static_cast<int>(f % tpi) * kM;
+        const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
+        const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
+        const long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
+        for (long long off = static_cast<long long>(tl) * 128; off < bytes; off += 128 * 128)
+            prefetch_l2_line(p0 + off);
+    };
+    (void)prefetch_lines;
+    uint4 buf[2][8];
+    auto load_chunk = [&](const uint8_t* base, int c, uint4 (&b)[8]) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) b[j] = ld_global_nc_v4(piece(base, 8 * c + j));
+    };
+    // The A-builders' first loads (tile 0's chunks 0 and 1) go out before the
+    // set-up below (barrier init, TMEM allocation, cluster barrier: ~3.4K
+    // cycles), which they do not depend on -- a CTA's first GEMM1 otherwise
+    // waits for cold HBM reads issued only after it (config-1 batches run 1-2
+    // pair tiles per CTA). The set-up itself runs on warps 12-13, so it does
+    // not wait for these loads to issue.
+    if (kPrefetch == 1 && warp == 14 && lane == 0 && my_tiles > 0) prefetch_tile(0);
+    const uint8_t* pbase = nullptr;
+    if (warp < 4 && my_tiles > 0) {
+        if (tl == 0) DS_TRACE(0, 0, 5);
+        pbase = token_base(0);
+        load_chunk(pbase, 0, buf[0]);
+        if (tl == 0) DS_TRACE(0, 0, 7);
+        load_chunk(pbase, 1, buf[1]);
+        if (tl == 0) DS_TRACE(0, 0, 8);
+    }
+
     if (threadIdx.x < kD1) {
         s_b1[threadIdx.x] = P.b1[threadIdx.x];
         s_hw[threadIdx.x] = P.hw[threadIdx.x];
     }
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 12 * 32) {
         // The leader's barriers also count the peer's single relayed arrival;
         // weight-stage barriers get both halves' bytes through cta_group::2 TMA.
         const uint32_t peer = leader ? 1u : 0u;
@@ -441,90 +522,16 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         }
     };
 
-    // Flat 128-token tiles f = image * tiles_per_img + tile-in-image; pair tile
-    // k covers f = 2k (leader) and 2k + 1 (peer), and the pairs take pair
-    // tiles round robin (k = unit, unit + nunits, ...), so a small batch still
-    // spreads over every SM pair. A pair tile whose second half runs past the
-    // end recomputes the last tile and writes nothing (a "ghost").
-    const long long n_img = P.n_img;
-    const int tpi = P.tiles_per_img;
-    const long long n_flat = n_img * tpi;
-    const long long n_pair_tiles = (n_flat + 1) / 2;
-    const long long my_tiles = unit < n_pair_tiles ? (n_pair_tiles - 1 - unit) / nunits + 1 : 0;
-    const long long img_bytes = static_cast<long long>(P.h) * P.w * 3;
-    const long long row_bytes = static_cast<long long>(P.w) * 3;
-    auto flat_raw = [&](long long tile) { return 2 * (unit + tile * nunits) + rank; };
-    auto flat_of = [&](long long tile) {                   // this CTA's flat tile
-        const long long f = flat_raw(tile);
-        return f < n_flat ? f : n_flat - 1;
-    };
-
     if (warp < 4) {
         // ===================== A-builder (128 threads, thread = token) =========
         // Chunk c of a tile holds K bytes [128c, 128c+128) of every token: the
         // 16-byte pieces q = 8c..8c+7 of its 768-byte patch vector (piece q is
         // patch row dy = q/3, 16-byte run q%3), stored unchanged as the u8 A
         // operand (SW128 chunk j = q%8 of the token's row).
-        const int tl = threadIdx.x;
-        auto token_base = [&](long long tile) -> const uint8_t* {
-            const long long f = flat_of(tile);
-            const long long img = f / tpi;
-            const int tok = static_cast<int>(f % tpi) * kM + tl;
-            const int py = tok / P.px, px = tok - py * P.px;
-            return P.images + img * img_bytes + (static_cast<long long>(py) * 16) * row_bytes +
-                   px * 48;
-        };
-        auto piece = [&](const uint8_t* base, int q) -> const uint8_t* {
-            return base + (q / 3) * row_bytes + (q % 3) * 16;
-        };
-        // The pixels of a tile are one contiguous byte range of whole patch
-        // rows (or a small superset); bulk-prefetch it into L2.
-        auto prefetch_tile = [&](long long tile) {
-            const long long f = flat_of(tile);
-            const long long img = f / tpi;
-            const int tok0 = static_cast<int>(f % tpi) * kM;
-            const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
-            const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
-            const long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
-            for (long long off = 0; off < bytes; off += 65536) {
-                const uint32_t nb = static_cast<uint32_t>(bytes - off < 65536 ? bytes - off : 65536);
-                bulk_prefetch_l2(p0 + off, nb);
-            }
-        };
-        // DS_PREFETCH: 1 = one thread's bulk prefetches (TMA unit), 2 = every
-        // builder thread prefetches lines through the LSU, 0 = none
-        auto prefetch_lines = [&](long long tile) {
-            const long long f = flat_of(tile);
-            const long long img = f / tpi;
-            const int tok0 = static_cast<int>(f % tpi) * kM;
-            const int py0 = tok0 / P.px, py1 = (tok0 + kM - 1) / P.px;
-            const uint8_t* p0 = P.images + img * img_bytes + static_cast<long long>(py0) * 16 * row_bytes;
-            const long long bytes = static_cast<long long>(py1 - py0 + 1) * 16 * row_bytes;
-            for (long long off = static_cast<long long>(tl) * 128; off < bytes; off += 128 * 128)
-                prefetch_l2_line(p0 + off);
-        };
-        (void)prefetch_lines;
-        if (tl == 0) DS_TRACE(0, 0, 5);
         const uint32_t tmem_lane = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
         const uint64_t s1x2 = f2_pack(P.s1, P.s1);
-        uint4 buf[2][8];
-        auto load_chunk = [&](const uint8_t* base, int c, uint4 (&b)[8]) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) b[j] = ld_global_nc_v4(piece(base, 8 * c + j));
-        };
-        const uint8_t* pbase = my_tiles > 0 ? token_base(0) : nullptr;
-        if (my_tiles > 0) {
-            load_chunk(pbase, 0, buf[0]);
-            if (tl == 0) DS_TRACE(0, 0, 7);
-            load_chunk(pbase, 1, buf[1]);
-            if (tl == 0) DS_TRACE(0, 0, 8);
-        }
-        // the rest of the first two tiles into L2 (after the first loads: the
-        // bulk prefetches take a while to issue)
-        if (kPrefetch == 1 && tl == 0) {
-            if (my_tiles > 0) prefetch_tile(0);
-            if (my_tiles > 1) prefetch_tile(1);
-        }
+        // the rest of the first two tiles into L2 (kPrefetch 1: warp 14 issues
+        // tile 0's and 1's bulk prefetches, which take ~1K cycles each to issue)
         if (kPrefetch == 2) {
             if (my_tiles > 0) prefetch_lines(0);
             if (my_tiles > 1) prefetch_lines(1);
@@ -765,8 +772,13 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         }
     } else if (warp == 14) {
         // ===================== W1 stages 0-3 into the H1 region ================
+        // (and, kPrefetch 1, the bulk L2 prefetch of the image tile 1 at the
+        // start: the A-builders are storing tile 0 then; later tiles are
+        // prefetched by a builder thread two tiles ahead -- issued here, during
+        // GEMM1, they cost ~0.6K cycles per pair tile)
         if (lane == 0) {
             const uint64_t policy = policy_evict_last();
+            if (kPrefetch == 1 && my_tiles > 1) prefetch_tile(1);
             for (long long tile = 0; tile < my_tiles; ++tile) {
                 if (tile > 0) mbar_wait(&B.r1_free, static_cast<uint32_t>((tile - 1) & 1));
                 for (int k = 0; k < kXStages; ++k) {

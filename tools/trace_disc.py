@@ -69,5 +69,42 @@ def main():
                   f"{int(t[5, tile, c] - base):8d}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 2 and sys.argv[2] == "prologue"):
     main()
+
+
+def prologue(n=5000):
+    """Tile 0 of CTA 0 in detail: the A-builder's first loads / prefetches and
+    per-chunk store times, the MMA's per-chunk waits, the weight stages."""
+    ctx = native.Context(0)
+    L = native.lib()
+    L.ds_disc_trace_device.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_int64, ctypes.c_int32,
+                                                                ctypes.c_int32] + [ctypes.c_void_p] * 3
+    disc = native.Discriminator(ctx, 2024)
+    img = torch.empty(n * 512 * 512 * 3, dtype=torch.uint8, device="cuda")
+    native.check(L.ds_synth_images_device(ctx.handle, 1, 0, n, 512, 512,
+                                          native.c_p(img.data_ptr()), native.c_p(ctx.stream)))
+    conf = torch.empty(n, dtype=torch.float32, device="cuda")
+    tr = torch.zeros(8 * 8 * 16 + 5 * 160, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        native.check(L.ds_disc_trace_device(disc.handle, native.c_p(img.data_ptr()), n, 512, 512,
+                                            native.c_p(conf.data_ptr()), native.c_p(tr.data_ptr()),
+                                            native.c_p(ctx.stream)))
+    ctx.synchronize()
+    tall = tr.cpu().numpy()
+    t = tall[:8 * 8 * 16].reshape(8, 8, 16)
+    c0 = tall[8 * 8 * 16 + 480]   # CTA 0's clock64 at its start
+    rel = lambda v: int(v - c0) if v else -1   # noqa: E731
+    print("CTA 0 tile 0, cycles after the CTA's first instruction:")
+    print("  builder: first loads", rel(t[0, 0, 5]), "chunk0 issued", rel(t[0, 0, 7]),
+          "chunk1 issued", rel(t[0, 0, 8]), "prefetches issued", rel(t[0, 0, 6]),
+          "loop top", rel(t[0, 0, 0]), "all stored", rel(t[0, 0, 1]))
+    print("  MMA: tile start", rel(t[2, 0, 0]), "G1 issued", rel(t[2, 0, 1]), "E1 seen", rel(t[2, 0, 3]))
+    for c in range(6):
+        print(f"  chunk {c}: slot free {rel(t[3, 0, c])}  stored {rel(t[4, 0, c])}  MMA saw {rel(t[5, 0, c])}")
+    for k in range(8):
+        print(f"  weight stage {k}: producer issued {rel(t[6, 0, k])}  MMA saw (next_b #{k}) {rel(t[7, 0, k])}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 2 and sys.argv[2] == "prologue":
+    prologue(int(sys.argv[1]))
