@@ -85,7 +85,9 @@ __device__ __forceinline__ int min_servers_r(double need, double per, double rpe
     const double y = __dmul_rn(need, rper);
     const double q = ceil(y);
     const double g = __dmul_rn(y, 0x1p-49);
-    if (__dsub_rn(q, y) > g && __dsub_rn(y, __dsub_rn(q, 1.0)) > g)
+    // (a subnormal 1/per or y would carry fewer bits than the bound assumes)
+    if (rper >= 0x1p-1022 && y >= 0x1p-1022 && __dsub_rn(q, y) > g &&
+        __dsub_rn(y, __dsub_rn(q, 1.0)) > g)
         return q < static_cast<double>(cap) + 1.0 ? static_cast<int>(q) : cap + 1;   // q >= 1
     return min_servers(need, per, cap);
 }

@@ -95,11 +95,15 @@ def test_planner_server_counts_at_integer_quotients(ctx):
     heavy32.update({b: b / 2.5 for b in range(3, 33, 5)})              # T2 = 2.5
     heavy7 = {1: 0.3, 2: 0.6, 3: 0.9, 5: 1.25, 8: 2.4, 12: 3.0, 20: 6.0}   # T2 = 10/3, 4, ...
     light = {b: b / 40.0 for b in (1, 2, 4, 8, 16, 32)}                # T1 = 40
-    cas = np.zeros(2, abi.CASCADE)
+    # extreme profiles: T2 near 1e308 makes 1/T2 subnormal (the fast path's
+    # accuracy bound does not hold there: it must take the exact division)
+    heavy_x = {1: 1e-308, 2: 3e-308, 4: 5e-300, 8: 1e-3}
+    cas = np.zeros(3, abi.CASCADE)
     cas[0] = workloads.make_cascade(light, heavy32, 1e3)
     cas[1] = workloads.make_cascade(light, heavy7, 1e3)
+    cas[2] = workloads.make_cascade(light, heavy_x, 1e3)
     probs = []
-    for ci in range(2):
+    for ci in range(3):
         for s in (3, 8, 16, 64, 128, 1000):
             for d in (100.0, 300.0, 400.0, 1000.0, 1234.5, 4000.0, 12.0):
                 for lam in (1.0, 1.05):
