@@ -112,6 +112,9 @@ constexpr bool kWarpArrive = DS_WARP_ARRIVE != 0;
 #define DS_G33_IL 0   // >0: the previous tile's GEMM3_3 K-chunk q is issued after GEMM1 chunk DS_G33_IL + q
 #endif
 constexpr int kG33Il = DS_G33_IL;
+#ifndef DS_A_REORDER
+#define DS_A_REORDER 0   // 1: the A-builders store chunks 2 and 3 before loading 4 and 5
+#endif
 #ifndef DS_PREFETCH
 #define DS_PREFETCH 1
 #endif
@@ -581,7 +584,17 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                 fence_proxy_async_smem();
                 group_signal(full, 2, 128, tl == 0);
                 if (tl == 0) DS_TRACE(4, tile, c);
+#if DS_A_REORDER
+                // chunks 2 and 3 stored back to back (X0 is free as soon as
+                // slot 0 is), then the loads of chunks 4 and 5
+                if (c < 2) load_chunk(pbase, c + 2, buf[c & 1]);
+                if (c == 3) {
+                    load_chunk(pbase, 4, buf[0]);
+                    load_chunk(pbase, 5, buf[1]);
+                }
+#else
                 if (c + 2 < kChunksPerTile) load_chunk(pbase, c + 2, buf[c & 1]);
+#endif
             }
             if (tl == 0) DS_TRACE(0, tile, 1);
             // E1 help: columns [kE1Split, 256) once GEMM1 of this tile landed. The
