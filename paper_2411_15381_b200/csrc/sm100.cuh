@@ -424,11 +424,29 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                  : "memory");
 }
 
+// The A-builders' pixel loads: 16 bytes per lane at a 48-byte stride (a
+// token's patch row), the three 16-byte runs of a row by three instructions
+// -- with L1 allocation (evict-first) the second and third hit the lines the
+// first brought in: 25.4K -> 24.7K cycles per pair tile (profiles/disc_l1_r2.txt).
+// 0 = L1::no_allocate (the round-1 choice), 1 = default L1 policy.
+#ifndef DS_A_L1
+#define DS_A_L1 2
+#endif
 __device__ __forceinline__ uint4 ld_global_nc_v4(const void* p) {
     uint4 r;
+#if DS_A_L1 == 1
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+#elif DS_A_L1 == 2
+    asm volatile("ld.global.nc.L1::evict_first.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
+#endif
     return r;
 }
 
