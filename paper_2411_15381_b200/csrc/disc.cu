@@ -113,7 +113,7 @@ constexpr bool kWarpArrive = DS_WARP_ARRIVE != 0;
 #endif
 constexpr int kG33Il = DS_G33_IL;
 #ifndef DS_A_REORDER
-#define DS_A_REORDER 0   // 1: the A-builders store chunks 2 and 3 before loading 4 and 5
+#define DS_A_REORDER 1   // the A-builders store chunks 2 and 3 before loading 4 and 5 (0: interleaved)
 #endif
 #ifndef DS_PREFETCH
 #define DS_PREFETCH 1
