@@ -119,6 +119,9 @@ constexpr int kG33Il = DS_G33_IL;
 #define DS_PREFETCH 1
 #endif
 constexpr int kPrefetch = DS_PREFETCH;   // image tiles two ahead into L2: 1 bulk (TMA), 2 lines (LSU), 0 off
+#ifndef DS_EXP_NO_ALOAD
+#define DS_EXP_NO_ALOAD 0
+#endif
 #ifndef DS_EXP_FAST_E1
 #define DS_EXP_FAST_E1 0
 #endif
@@ -445,8 +448,18 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     (void)prefetch_lines;
     uint4 buf[2][8];
     auto load_chunk = [&](const uint8_t* base, int c, uint4 (&b)[8]) {
+#if DS_EXP_NO_ALOAD
+        // TIMING EXPERIMENT ONLY (wrong results): no pixel loads
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t x = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(base)) * 2654435761u +
+                               static_cast<uint32_t>(97 * c + 7919 * j);
+            b[j] = make_uint4(x, x * 3u, x * 5u, x * 7u);
+        }
+#else
 #pragma unroll
         for (int j = 0; j < 8; ++j) b[j] = ld_global_nc_v4(piece(base, 8 * c + j));
+#endif
     };
     // The A-builders' first loads (tile 0's chunks 0 and 1) go out before the
     // set-up below (barrier init, TMEM allocation, cluster barrier: ~3.4K
