@@ -119,6 +119,9 @@ constexpr int kG33Il = DS_G33_IL;
 #define DS_PREFETCH 1
 #endif
 constexpr int kPrefetch = DS_PREFETCH;   // image tiles two ahead into L2: 1 bulk (TMA), 2 lines (LSU), 0 off
+#ifndef DS_EXP_NO_TANH
+#define DS_EXP_NO_TANH 0
+#endif
 #ifndef DS_EXP_NO_ALOAD
 #define DS_EXP_NO_ALOAD 0
 #endif
@@ -130,6 +133,9 @@ constexpr int kPrefetch = DS_PREFETCH;   // image tiles two ahead into L2: 1 bul
 #endif
 #ifndef DS_E1_PIPE
 #define DS_E1_PIPE 0
+#endif
+#ifndef DS_E1_SINGLE
+#define DS_E1_SINGLE 0
 #endif
 #ifndef DS_E1_SPLIT
 #define DS_E1_SPLIT 192
@@ -189,18 +195,27 @@ constexpr int kTraceCtas = 160;   // per-CTA stamps: [globaltimer start, end, sm
     } while (0)
 
 // GELU_tanh(s1 * acc + b) of two adjacent s32 accumulator columns with paired
-// fp32 ops: x = fma(acc, s1, b); u = x (k + k c x^2); gelu = h + h tanh(u),
-// h = x / 2. (s = {s1, s1}, b = {b[c], b[c+1]})
+// fp32 ops, in halves: with h = x / 2 = fma(acc, s1/2, b/2) (exactly half of
+// fma(acc, s1, b): scaling by 2 commutes with the rounding), u = x (k + k c
+// x^2) = h (2k + 8 k c h^2) -- the same roundings, every factor of 2 exact --
+// and gelu = h + h tanh(u) = fma(tanh(u), h, h). Bit-identical to the form
+// with x, one paired multiply (h = 0.5 x) fewer per two columns.
+// (s = {s1/2, s1/2}, b = {b[c]/2, b[c+1]/2})
 __device__ __forceinline__ uint32_t gelu2_bf16x2(uint32_t a0, uint32_t a1, uint64_t s, uint64_t b) {
-    const uint64_t x = f2_fma(f2_pack(static_cast<float>(static_cast<int>(a0)),
+    const uint64_t h = f2_fma(f2_pack(static_cast<float>(static_cast<int>(a0)),
                                       static_cast<float>(static_cast<int>(a1))), s, b);
-    const uint64_t kk = f2_pack(0.7978845608028654f, 0.7978845608028654f);
-    const uint64_t kc = f2_pack(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
-    const uint64_t u = f2_mul(x, f2_fma(f2_mul(x, x), kc, kk));
+    const uint64_t kk = f2_pack(2.0f * 0.7978845608028654f, 2.0f * 0.7978845608028654f);
+    const uint64_t kc = f2_pack(8.0f * (0.7978845608028654f * 0.044715f),
+                                8.0f * (0.7978845608028654f * 0.044715f));
+    const uint64_t u = f2_mul(h, f2_fma(f2_mul(h, h), kc, kk));
     float u0, u1;
     f2_unpack(u, u0, u1);
-    const uint64_t h = f2_mul(x, f2_pack(0.5f, 0.5f));
+#if DS_EXP_NO_TANH
+    // TIMING EXPERIMENT ONLY (wrong results): the tanh replaced by a clamp
+    const uint64_t g = f2_fma(f2_pack(fminf(u0, 1.0f), fminf(u1, 1.0f)), h, h);
+#else
     const uint64_t g = f2_fma(f2_pack(tanh_approx(u0), tanh_approx(u1)), h, h);
+#endif
     float g0, g1;
     f2_unpack(g, g0, g1);
     return pack_bf16x2(g0, g1);
@@ -250,6 +265,15 @@ __device__ __forceinline__ void e1_columns(uint32_t tmem_lane, int c_lo, uint32_
         if (g + 1 < kN32) tmem_ld_x32_async(tmem_lane + c_lo + 32 * (g + 1), nxt);
         emit(cur, c_lo + 32 * g);
         if (g + 1 < kN32) tmem_wait_ld32(nxt);
+    }
+#elif DS_E1_SINGLE
+    // one 32-column TMEM load at a time (half the registers of the pair form)
+#pragma unroll 1
+    for (int g = 0; g < kN32; ++g) {
+        uint32_t v[32];
+        const int c0 = c_lo + 32 * g;
+        tmem_ld_x32_sync(tmem_lane + c0, v);
+        emit(v, c0);
     }
 #else
 #pragma unroll 1
@@ -479,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
     }
 
     if (threadIdx.x < kD1) {
-        s_b1[threadIdx.x] = P.b1[threadIdx.x];
+        s_b1[threadIdx.x] = 0.5f * P.b1[threadIdx.x];   // E1 works in halves (gelu2_bf16x2)
         s_hw[threadIdx.x] = P.hw[threadIdx.x];
     }
     if (threadIdx.x == 12 * 32) {
@@ -545,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         // patch row dy = q/3, 16-byte run q%3), stored unchanged as the u8 A
         // operand (SW128 chunk j = q%8 of the token's row).
         const uint32_t tmem_lane = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
-        const uint64_t s1x2 = f2_pack(P.s1, P.s1);
+        const uint64_t s1x2 = f2_pack(0.5f * P.s1, 0.5f * P.s1);   // halves, as s_b1
         // the rest of the first two tiles into L2 (kPrefetch 1: warp 14 issues
         // tile 0's and 1's bulk prefetches, which take ~1K cycles each to issue)
         if (kPrefetch == 2) {
@@ -636,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         const uint32_t row = 32 * q + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(32 * q) << 16;
         const bool first = ew == 0 && lane == 0;
-        const uint64_t s1x2 = f2_pack(P.s1, P.s1);
+        const uint64_t s1x2 = f2_pack(0.5f * P.s1, 0.5f * P.s1);   // halves, as s_b1
         uint32_t p12 = 0, p3 = 0, pfree = 0;
 
         // E3: ReLU(acc3) . w_head over this thread's 128 columns -> per-image sum
