@@ -134,6 +134,14 @@ constexpr int kPrefetch = DS_PREFETCH;   // image tiles two ahead into L2: 1 bul
 #ifndef DS_E1_PIPE
 #define DS_E1_PIPE 0
 #endif
+#ifndef DS_E1_EARLY
+#define DS_E1_EARLY 1
+#endif
+// E1 hands GEMM2_0 its operands piecewise: "every TMEM read of the GEMM1
+// accumulator done" (acc_read: GEMM2_0 may overwrite it) and H1 K-chunk 0 / 1
+// stored (h1c) come before the rest of E1, so GEMM2_0's first K-chunks run
+// while E1 still computes and stores K-chunks 2 (epilogue) and 3 (builders).
+constexpr bool kE1Early = DS_E1_EARLY != 0;
 #ifndef DS_E1_SINGLE
 #define DS_E1_SINGLE 0
 #endif
@@ -141,6 +149,8 @@ constexpr int kPrefetch = DS_PREFETCH;   // image tiles two ahead into L2: 1 bul
 #define DS_E1_SPLIT 192
 #endif
 constexpr int kE1Split = DS_E1_SPLIT;   // E1 columns [0,192): epilogue warps; [192,256): A-builders
+static_assert(!kE1Early || (kE1Split == 192 && !DS_E1_PIPE && !DS_E1_SINGLE),
+              "the early E1 hand-off assumes the 192/64 split and the paired TMEM loads");
 static_assert(kE1Split % 64 == 0 && kE1Split >= 64 && kE1Split <= 256, "E1 split: 32-column blocks per half");
 // shared memory map (bytes, per CTA)
 constexpr int kR1 = 0;                              // H1: 4 K-chunks x 16 KB (bf16, SW128)
@@ -226,32 +236,37 @@ __device__ __forceinline__ uint32_t sw128(uint32_t row, uint32_t chunk) {
     return (row >> 3) * 1024u + (row & 7u) * 128u + ((chunk ^ (row & 7u)) << 4);
 }
 
+// GELU of 32 loaded accumulator columns [cbase, cbase + 32) of row `row`
+// -> bf16 -> the SW128 H1 tile (4 K-chunks of 16 KB).
+__device__ __forceinline__ void e1_emit32(const uint32_t (&v)[32], int cbase, uint32_t row,
+                                          uint32_t h1, const float* s_b1, uint64_t s1x2) {
+#pragma unroll
+    for (int e = 0; e < 32; e += 8) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = cbase + e + 2 * u;
+#if DS_EXP_FAST_E1
+            // TIMING EXPERIMENT ONLY (wrong results): E1 without the GELU math
+            (void)s1x2;
+            pk[u] = v[e + 2 * u] ^ v[e + 2 * u + 1] ^ static_cast<uint32_t>(c);
+#else
+            pk[u] = gelu2_bf16x2(v[e + 2 * u], v[e + 2 * u + 1], s1x2,
+                                 *reinterpret_cast<const uint64_t*>(s_b1 + c));
+#endif
+        }
+        const int f = cbase + e;
+        st_shared_v4(h1 + (f >> 6) * 16384u + sw128(row, (f & 63) >> 3), pk[0], pk[1], pk[2],
+                     pk[3]);
+    }
+}
+
 // E1 over columns [c_lo, c_lo + 32*n32) of this thread's TMEM lane (row):
 // GELU(s1 * acc + b1) -> bf16 -> the SW128 H1 tile (4 K-chunks of 16 KB).
 template <int kN32>
 __device__ __forceinline__ void e1_columns(uint32_t tmem_lane, int c_lo, uint32_t row,
                                            uint32_t h1, const float* s_b1, uint64_t s1x2) {
-    auto emit = [&](const uint32_t (&v)[32], int cbase) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int c = cbase + e + 2 * u;
-#if DS_EXP_FAST_E1
-                // TIMING EXPERIMENT ONLY (wrong results): E1 without the GELU math
-                (void)s1x2;
-                pk[u] = v[e + 2 * u] ^ v[e + 2 * u + 1] ^ static_cast<uint32_t>(c);
-#else
-                pk[u] = gelu2_bf16x2(v[e + 2 * u], v[e + 2 * u + 1], s1x2,
-                                     *reinterpret_cast<const uint64_t*>(s_b1 + c));
-#endif
-            }
-            const int f = cbase + e;
-            st_shared_v4(h1 + (f >> 6) * 16384u + sw128(row, (f & 63) >> 3), pk[0], pk[1], pk[2],
-                         pk[3]);
-        }
-    };
+    auto emit = [&](const uint32_t (&v)[32], int cbase) { e1_emit32(v, cbase, row, h1, s_b1, s1x2); };
 #if DS_E1_PIPE
     // software-pipelined: block g+1's TMEM load is in flight while block g is
     // activated (two 32-register buffers, as many as the unpipelined form)
@@ -298,6 +313,7 @@ struct Bars {
     uint64_t a_full[kAStages], a_empty[kAStages], b_full[kBStages], b_empty[kBStages];
     uint64_t acc12_full, drained, h2_ready, h2_free, acc3_full, acc3_empty;
     uint64_t x_full[kXStages], r1_free, e1b_done, aw_full[2], aw_free, ax_full[2];
+    uint64_t acc_read, h1c[2];   // kE1Early hand-offs
     uint32_t tmem_base;
     float warp_part[2][8];
     float stash[kStash];   // chained: this CTA's head sums until the previous call completed
@@ -530,6 +546,9 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         for (int s = 0; s < 2; ++s) mbar_init(&B.aw_full[s], 1);
         for (int s = 0; s < 2; ++s) mbar_init(&B.ax_full[s], kWarpArrive ? 4 + 4 * peer : 128 + peer);
         mbar_init(&B.aw_free, 1);
+        // all E1 threads (epilogue 256 + builders 128; the peer's two groups relay once each)
+        mbar_init(&B.acc_read, kWarpArrive ? 12 + 12 * peer : 384 + 2 * peer);
+        for (int s = 0; s < 2; ++s) mbar_init(&B.h1c[s], kWarpArrive ? 4 + 4 * peer : 128 + peer);
         fence_mbar_init();
     }
     if (warp == 13) tmem_alloc2<512>(&B.tmem_base);
@@ -638,7 +657,19 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             // acc12_full phase of E1(tile) has parity tile & 1; the barrier cannot
             // be behind it (the A slots just freed were released after GEMM2_3 of
             // the previous tile) nor past it (GEMM2_0 waits for e1b_done).
-            if constexpr (kE1Split < 256) {
+            if constexpr (kE1Early) {
+                // H1 K-chunk 3: load, tell GEMM2_0 the accumulator reads are
+                // done, then activate and store
+                mbar_wait(&B.acc12_full, static_cast<uint32_t>(tile & 1));
+                tc_fence_after();
+                uint32_t v0[32], v1[32];
+                tmem_ld2_x32_sync(tmem_lane + 192, tmem_lane + 224, v0, v1);
+                tc_fence_before();
+                group_signal(&B.acc_read, 2, 128, tl == 0);
+                e1_emit32(v0, 192, tl, sbase + kR1, s_b1, s1x2);
+                e1_emit32(v1, 224, tl, sbase + kR1, s_b1, s1x2);
+                fence_proxy_async_smem();
+            } else if constexpr (kE1Split < 256) {
                 mbar_wait(&B.acc12_full, static_cast<uint32_t>(tile & 1));
                 tc_fence_after();
                 e1_columns<(256 - kE1Split) / 32>(tmem_lane, kE1Split, tl, sbase + kR1, s_b1, s1x2);
@@ -718,11 +749,33 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
             p12 ^= 1;
             tc_fence_after();
             DS_TRACE(1, tile, 0);
-            e1_columns<kE1Split / 64>(tmem + lane_addr, (kE1Split / 2) * half, row, sbase + kR1, s_b1,
-                                      s1x2);
-            fence_proxy_async_smem();
-            tc_fence_before();
-            group_signal(&B.drained, 3, 256, first);
+            if constexpr (kE1Early) {
+                // H1 K-chunk `half` (columns [64 half, 64 half + 64)) first ...
+                {
+                    uint32_t v0[32], v1[32];
+                    const int c0 = 64 * half;
+                    tmem_ld2_x32_sync(tmem + lane_addr + c0, tmem + lane_addr + c0 + 32, v0, v1);
+                    e1_emit32(v0, c0, row, sbase + kR1, s_b1, s1x2);
+                    e1_emit32(v1, c0 + 32, row, sbase + kR1, s_b1, s1x2);
+                }
+                fence_proxy_async_smem();
+                group_signal(&B.h1c[half], 4 + half, 128, (ew & 3) == 0 && lane == 0);
+                // ... then this half's 32 columns of K-chunk 2: after their load
+                // the accumulator is free for GEMM2_0
+                uint32_t v[32];
+                tmem_ld_x32_sync(tmem + lane_addr + 128 + 32 * half, v);
+                tc_fence_before();
+                group_signal(&B.acc_read, 3, 256, first);
+                e1_emit32(v, 128 + 32 * half, row, sbase + kR1, s_b1, s1x2);
+                fence_proxy_async_smem();
+                group_signal(&B.drained, 3, 256, first);   // K-chunk 2 stored
+            } else {
+                e1_columns<kE1Split / 64>(tmem + lane_addr, (kE1Split / 2) * half, row, sbase + kR1,
+                                          s_b1, s1x2);
+                fence_proxy_async_smem();
+                tc_fence_before();
+                group_signal(&B.drained, 3, 256, first);
+            }
             DS_TRACE(1, tile, 1);
 
             // ---- E2_j: acc[0,256) -> ReLU -> bf16 (registers) -> H2 (R2) --------
@@ -959,12 +1012,26 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     umma_commit_pair(&B.acc3_full, 0x3);
                 }
                 DS_TRACE(2, tile, 2);
-                wait_bar(&B.drained, pdr);           // E1: acc drained, H1 stored
-                mbar_wait(&B.e1b_done, static_cast<uint32_t>(tile & 1));   // the builders' E1 columns
+                if constexpr (kE1Early) {
+                    // E1's accumulator reads done and H1 K-chunk 0 stored; chunks
+                    // 1-3 are awaited one by one below
+                    mbar_wait(&B.acc_read, static_cast<uint32_t>(tile & 1));
+                    mbar_wait(&B.h1c[0], static_cast<uint32_t>(tile & 1));
+                } else {
+                    wait_bar(&B.drained, pdr);           // E1: acc drained, H1 stored
+                    mbar_wait(&B.e1b_done, static_cast<uint32_t>(tile & 1));   // the builders' E1 columns
+                }
                 tc_fence_after();
                 DS_TRACE(2, tile, 3);
                 // G2_0: its first kAWStages weight stages sit in the A slots
                 for (int kc = 0; kc < 4; ++kc) {
+                    if constexpr (kE1Early) {
+                        if (kc == 1) mbar_wait(&B.h1c[1], static_cast<uint32_t>(tile & 1));
+                        if (kc == 2) mbar_wait(&B.drained, pdr);   // epilogue's K-chunk 2
+                        if (kc == 3) mbar_wait(&B.e1b_done, static_cast<uint32_t>(tile & 1));
+                        if (kc == 2) pdr ^= 1;
+                        if (kc > 0) tc_fence_after();
+                    }
                     const uint64_t ad = desc_k_sw128(sbase + kR1 + kc * kAChunk);
                     uint64_t bd;
                     if (kc < kAWStages) {
