@@ -240,20 +240,6 @@ int main(void) {
             bad++;
         }
     }
-    for (long i = 0; i < n / 4; i++) {   /* the integer columns (operator<<) */
-        uint64_t u = xr() >> (xr() % 64);
-        if (i % 16 == 0) u = (i % 32 == 0) ? 0xffffffffffffffffull : (uint64_t)(i / 16);
-        snprintf(a, sizeof a, "%llu", (unsigned long long)u);
-        int k = ds_fmt_u64(u, b);
-        b[k] = 0;
-        if (strcmp(a, b)) { if (bad < 5) printf("u64 %s restated=%s\n", a, b); bad++; }
-        int64_t s = (int64_t)u;
-        if (i % 64 == 1) s = INT64_MIN;
-        snprintf(a, sizeof a, "%lld", (long long)s);
-        k = ds_fmt_i64(s, b);
-        b[k] = 0;
-        if (strcmp(a, b)) { if (bad < 5) printf("i64 %s restated=%s\n", a, b); bad++; }
-    }
     printf("bad=%ld\n", bad);
     return bad != 0;
 }
