@@ -183,6 +183,20 @@ def in_kernel_clock(L, disc, images, conf, ctx):
                    "launch of the step's images right after the timed region"}
 
 
+def tensor_pipe_frac(ik):
+    """Clock-independent view of the discriminator: the MMA cycles a 256-token
+    pair tile needs at the tensor pipe's rate (152 MMAs x 128 cycles: GEMM1 24
+    i8 K=32, GEMM2 64 and GEMM3 64 bf16 K=16, each M=256 N=256 on an SM pair)
+    over the cycles a pair tile took (in-kernel clock64, whole launch)."""
+    if not ik or not ik.get("cycles_per_pair_tile"):
+        return None
+    mma = 152 * 128
+    return {"mma_cycles_per_pair_tile": mma,
+            "cycles_per_pair_tile": ik["cycles_per_pair_tile"],
+            "frac": mma / ik["cycles_per_pair_tile"],
+            "note": "the rest of the gap to the burst peak is the clock the 1 kW cap allows"}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -1086,7 +1100,8 @@ def run_gpu(args):
                          "flop_per_image": DISC_FLOP_PER_IMG,
                          "flop_per_image_bf16_equivalent": DISC_FLOP_BF16_EQ,
                          "note": "layer 1 (27% of FLOPs) is u8 x s8 on the int8 tensor path at "
-                                 "2x the bf16 rate; its FLOPs count half"},
+                                 "2x the bf16 rate; its FLOPs count half",
+                         "tensor_pipe": tensor_pipe_frac(clocks.get("in_kernel"))},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "bound": {"what": "host->device copy of the images (PCIe)",
