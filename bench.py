@@ -194,7 +194,8 @@ def tensor_pipe_frac(ik):
     return {"mma_cycles_per_pair_tile": mma,
             "cycles_per_pair_tile": ik["cycles_per_pair_tile"],
             "frac": mma / ik["cycles_per_pair_tile"],
-            "note": "the rest of the gap to the burst peak is the clock the 1 kW cap allows"}
+            "note": "tensor-pipe utilisation per cycle; TFLOP/s also depends on the SM clock "
+                    "the 1 kW cap allows (see clocks.in_kernel)"}
 
 
 def dist_env():
