@@ -27,20 +27,24 @@
 // (128 of the 256 output rows), so each SM streams 0.6 MB of weights per 128
 // tokens instead of 1.2 MB; one thread of the leader CTA issues M = 256 MMAs
 // that read both CTAs' shared memory and write both CTAs' TMEM.
-//   warps 0-3   A-builder: 128-bit loads of 16 B pixel runs (thread = token)
-//               stored as-is into a 2-stage SW128 ring (6 chunks of K = 128
-//               bytes per tile); one thread bulk-prefetches the tiles two
-//               ahead into L2; after GEMM1 they also run E1 on columns
-//               [192, 256)
+//   warps 0-3   A-builder: 128-bit loads of 16 B pixel runs (thread = token;
+//               L1-allocating, so a patch row's three runs share sectors)
+//               stored as-is into a 2-stage SW128 ring plus two W1 slots of
+//               the H1 region (6 chunks of K = 128 bytes per tile); a CTA's
+//               first two chunks are loaded before the set-up barriers; one
+//               thread bulk-prefetches the tiles two ahead into L2; after
+//               GEMM1 they also run E1 on columns [192, 256)
 //   warps 4-11  epilogue: tcgen05.ld of this CTA's TMEM lanes, activation,
 //               bf16 pack, SW128 stores of H1/H2 (next GEMM's A operand), and
 //               the head dot product (E3, per-tile sum)
 //   warp 12     weight producer: tensor-map TMA of this CTA's 16 KB half of
 //               each pre-swizzled 32 KB stage (256 rows x 128 B, SW128; L2
 //               evict-last) into a 4-stage ring; completion lands on the
-//               LEADER's barrier (cta_group::2)
+//               LEADER's barrier (cta_group::2); its lane 0 also initialises
+//               the barriers (off the A-builders, whose first loads go first)
 //   warp 13     TMEM allocator (both CTAs) + the MMA-issuing thread (leader)
 //   warp 14     W1 stages 0-3 into the H1 region, which is idle during GEMM1
+//               (and the L2 prefetch of a CTA's first two tiles)
 // Every weight stage and A chunk is 4 MMAs (K = 64 bf16 / 128 int8), so the
 // issuing thread waits once per 512 MMA-cycles (waits every 2 MMAs cost the
 // tensor pipe ~15%, tools/i8_rate_probe.cu).
@@ -54,7 +58,10 @@
 // The epilogue signals "accumulator drained" as soon as its TMEM loads land
 // (packed bf16 values stay in registers) and stores H2_j only after the GEMM3
 // still reading the previous H2 chunk committed, so G2_{j+1} overlaps E2_j and
-// G3_3(i-1) overlaps E1(i). GEMM2_0's first two weight stages are parked in the
+// G3_3(i-1) overlaps E1(i). E1 hands GEMM2_0 its operands piecewise
+// (acc_read: every TMEM read of the GEMM1 accumulator done; then H1 K-chunks
+// 0/1, 2 and 3 as they are stored), so GEMM2_0's first K-chunks run while E1
+// still activates. GEMM2_0's first two weight stages are parked in the
 // A slots (free from GEMM1's end until the next tile's first chunks), loaded
 // right after GEMM1 by warp 14; E3(i-1) runs after E2_0(i).
 #include <cuda.h>
