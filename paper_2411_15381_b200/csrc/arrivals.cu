@@ -794,8 +794,12 @@ ds_status target_sum(ds_ctx* ctx, const double* e, int64_t D, double* T, cudaStr
     ts_write_kernel<<<g, kTsThreads, 0, st>>>(D, r, special, bspec, seg, fail, T);
     DS_LAUNCH_CHECK(ctx, "ts_write_kernel");
     // fallback: the single-CTA exact scan, a no-op unless a check failed
-    DS_CUDA_TRY(cudaFuncSetAttribute(target_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kSumSmem)));
+    if (!(ctx->route_attr_set & (1u << 21))) {   // once per context
+        DS_CUDA_TRY(cudaFuncSetAttribute(target_sum_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSumSmem)));
+        ctx->route_attr_set |= 1u << 21;
+    }
     const int* gate = std::getenv("DS_TARGET_SUM_SEQUENTIAL") ? nullptr : fail;   // test hook
     target_sum_kernel<<<1, kSumThreads, kSumSmem, st>>>(e, D, T, gate);
     DS_LAUNCH_CHECK(ctx, "target_sum_kernel");

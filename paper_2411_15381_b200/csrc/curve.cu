@@ -11,6 +11,10 @@
 // staged through shared memory.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -702,15 +706,30 @@ SpecPlan spec_plan(ds_ctx* ctx, int64_t n, int32_t dtype, double decay) {
     }();
     SpecPlan p;
     if (env_off || n < spec::kMinN) return p;
-    int sms = 0, occ = 0;
     int L = env_l > 0 ? env_l : spec::kDefaultL;
     L = (L + 15) / 16 * 16;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess)
-        return p;
+    // the SM count and the kernel's occupancy, queried once per (device,
+    // kernel): the queries cost tens of microseconds of host time per call
     const void* fn = spec_kernel_for(dtype, decay != 1.0);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, spec::kThreads,
-                                                      static_cast<size_t>(spec::kMaxL)) != cudaSuccess)
-        return p;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, std::pair<int, int>> cache;
+    int sms = 0, occ = 0;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find({ctx->device, fn});
+        if (it != cache.end()) {
+            sms = it->second.first;
+            occ = it->second.second;
+        } else {
+            if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) !=
+                    cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, spec::kThreads,
+                                                              static_cast<size_t>(spec::kMaxL)) !=
+                    cudaSuccess)
+                return p;
+            cache[{ctx->device, fn}] = {sms, occ};
+        }
+    }
     const int64_t max_blocks = static_cast<int64_t>(occ) * sms;   // at the largest segment
     int64_t S = (n + L - 1) / L;
     if (S + 1 > max_blocks) {
