@@ -1279,8 +1279,10 @@ def cpu_legs(line, args, c_host, prior, gpu_curve, pro, cas, grid, goffs, gpu_pl
     line["planner"]["parity_cpu_vs_gpu"] = bool(cpu_plans.tobytes() == gpu_plans.tobytes())
     line["planner"]["speedup_vs_cpu_all_threads"] = pt / (line["planner"]["ms_per_batch"] / 1e3)
     lv, lk, lconf_cpu, lidx_cpu = cpu_latent_leg(CPU_LATENT_SAMPLE, threads)
+    lv1, _, _, _ = cpu_latent_leg(CPU_LATENT_SAMPLE // 4, 1)
     line["latent"]["cpu_baseline"] = {
         "value": lv, "unit": "queries/s", "cores": threads, "kind": lk,
+        "one_thread": {"value": lv1, "sample": f"{CPU_LATENT_SAMPLE // 4} queries"},
         "sample": f"{CPU_LATENT_SAMPLE} queries: sample_query on {threads} threads + "
                   "sequential observe/defers loop"}
     g = lconf_host[:CPU_LATENT_SAMPLE]
