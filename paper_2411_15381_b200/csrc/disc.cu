@@ -119,6 +119,9 @@ constexpr bool kWarpArrive = DS_WARP_ARRIVE != 0;
 #define DS_G33_IL 0   // >0: the previous tile's GEMM3_3 K-chunk q is issued after GEMM1 chunk DS_G33_IL + q
 #endif
 constexpr int kG33Il = DS_G33_IL;
+#ifndef DS_A_RECOMPUTE
+#define DS_A_RECOMPUTE 1
+#endif
 #ifndef DS_A_REORDER
 #define DS_A_REORDER 1   // the A-builders store chunks 2 and 3 before loading 4 and 5 (0: interleaved)
 #endif
@@ -640,10 +643,25 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
                     if (++astage == kAStages) { astage = 0; aphase ^= 1; }
                 }
                 if (tl == 0) DS_TRACE(3, tile, c);
+#if DS_A_RECOMPUTE
+                {
+                    // the row's SW128 base and swizzle recomputed per chunk
+                    // (an opaque copy keeps the compiler from hoisting the eight
+                    // addresses out of the loop, where they were spilled)
+                    uint32_t r = static_cast<uint32_t>(tl);
+                    asm volatile("" : "+r"(r));
+                    const uint32_t rb = st + (r >> 3) * 1024u + (r & 7u) * 128u, r7 = r & 7u;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        st_shared_v4(rb + ((static_cast<uint32_t>(j) ^ r7) << 4), buf[c & 1][j].x,
+                                     buf[c & 1][j].y, buf[c & 1][j].z, buf[c & 1][j].w);
+                }
+#else
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     st_shared_v4(st + sw128(tl, j), buf[c & 1][j].x, buf[c & 1][j].y, buf[c & 1][j].z,
                                  buf[c & 1][j].w);
+#endif
                 fence_proxy_async_smem();
                 group_signal(full, 2, 128, tl == 0);
                 if (tl == 0) DS_TRACE(4, tile, c);
