@@ -560,12 +560,18 @@ __global__ void __launch_bounds__(kThreads, 1) disc_kernel(const __grid_constant
         mbar_init(&B.acc_read, kWarpArrive ? 12 + 12 * peer : 384 + 2 * peer);
         for (int s = 0; s < 2; ++s) mbar_init(&B.h1c[s], kWarpArrive ? 4 + 4 * peer : 128 + peer);
         fence_mbar_init();
+        DS_TRACE(6, 7, 0);   // debug: set-up phases of CTA 0 (slots unused by 2-tile CTAs)
     }
-    if (warp == 13) tmem_alloc2<512>(&B.tmem_base);
+    if (warp == 13) {
+        tmem_alloc2<512>(&B.tmem_base);
+        if (lane == 0) DS_TRACE(6, 7, 1);
+    }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) DS_TRACE(6, 7, 2);
     cluster_sync();   // peer barriers initialised before any remote arrive
     tc_fence_after();
+    if (threadIdx.x == 0) DS_TRACE(6, 7, 3);
     const uint32_t tmem = B.tmem_base;
 
     // A role's arrival on the LEADER's barrier: the leader's threads arrive

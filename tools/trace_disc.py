@@ -99,6 +99,8 @@ def prologue(n=5000):
     print("  builder: first loads", rel(t[0, 0, 5]), "chunk0 issued", rel(t[0, 0, 7]),
           "chunk1 issued", rel(t[0, 0, 8]), "prefetches issued", rel(t[0, 0, 6]),
           "loop top", rel(t[0, 0, 0]), "all stored", rel(t[0, 0, 1]))
+    print("  set-up: barriers initialised", rel(t[6, 7, 0]), "TMEM allocated", rel(t[6, 7, 1]),
+          "CTA barrier", rel(t[6, 7, 2]), "cluster barrier", rel(t[6, 7, 3]))
     print("  MMA: tile start", rel(t[2, 0, 0]), "G1 issued", rel(t[2, 0, 1]), "E1 seen", rel(t[2, 0, 3]))
     for c in range(6):
         print(f"  chunk {c}: slot free {rel(t[3, 0, c])}  stored {rel(t[4, 0, c])}  MMA saw {rel(t[5, 0, c])}")
