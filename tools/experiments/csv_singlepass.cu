@@ -404,3 +404,6 @@ extern "C" ds_status ds_format_g6(ds_ctx* ctx, const double* values, int64_t n, 
 // (lookback.cuh); it did not change this result. A faster fmt6 digit stage
 // (32-bit digit arithmetic, 9-digit u64 chunks) measured 10% SLOWER in the
 // three-pass kernel (1.17 vs 1.06 ms) and was dropped.
+// Also measured (round 2): the three-pass design with each thread's row rendered
+// into a 260-byte slot of SHARED memory instead of its local-memory buffer:
+// 2.96 ms vs 1.07 ms (generic byte stores into shared memory, divergent columns).
